@@ -1,0 +1,252 @@
+/*
+ * climber.h — C ABI of libclimber.so: B200-native "single user, multiple items"
+ * (SUMI) ranking inference for Climber (arXiv 2502.09888).
+ *
+ * The calls follow the paper's statement of the serving problem (PAPER.md
+ * L257, §3.2 Deployment): "the system first generates multi-layered key-value
+ * (KV) cache vectors from user features, then fetches candidate item features
+ * from the feature server, and finally computes attention-based interactions
+ * between the item features and cached KV representations."
+ *
+ *   climber_encode_user(events, r)        -> kv handle   (multi-layer K/V cache)
+ *   climber_score_items(kv, items[M])     -> scores[M]   (SUMI attention + BGF)
+ *
+ * What is computed (PAPER.md, readings G1-G28 of SURVEY.md §8(c)):
+ *   - MSE extraction (Eq. 1-2): per strategy a_k, the most recent n_k
+ *     events whose action/scenario pass the strategy's filters, chronological.
+ *   - N_b blocks of L adaptive Transformer layers (Eq. 3): pre-RMSNorm,
+ *     QKV, softmax(QK^T / (sqrt(d_h) * tau[l][k][r][head])) V, W_O + residual,
+ *     RMSNorm, FFN (d -> 4d SiLU -> d) + residual.  History attention is causal
+ *     (hist_causal = 1) or bidirectional (0); every candidate attends to the
+ *     whole history of its block plus itself only (L255: full-visible +
+ *     diagonal masks).  Relative bias f_b is 0 on this path (G6).
+ *   - Bit-wise gating fusion (Eq. 4): one fusion ATL over the N_b block
+ *     outputs (temperature tau_f[r][head], no mask), squeeze-and-excitation gate
+ *     FC(N_b d -> N_b d / se_reduction) + b, ReLU, FC + b, sigmoid, product.
+ *   - Head: score = w_head . vec(Y) + b_head, an fp32 logit (G18).
+ *
+ * Conventions for every call:
+ *   - Return value: climber_status.  No C++ exception or abort crosses the ABI.
+ *     On failure climber_last_error() (thread-local) describes the cause.
+ *   - Host-checkable errors (NULL, sizes, config) return synchronously and
+ *     enqueue nothing.  Data-dependent errors (ids out of range, decreasing
+ *     timestamps) are detected on the device: they set the ctx's device error
+ *     word, the affected scores become NaN, and climber_stream_status() reports
+ *     them.
+ *   - "dev" pointers are CUDA device pointers, "host" pointers are CPU memory.
+ *     Device inputs are borrowed until the stream reaches the call.  Outputs
+ *     written to device memory are valid after the stream is synchronised.
+ *   - One ctx owns one scratch workspace: calls that compute (encode / score)
+ *     must be issued on one stream at a time per ctx (or externally ordered).
+ *   - Determinism: same inputs give bit-identical scores; no float atomics, no
+ *     split-K.  Permuting candidates permutes scores bit-exactly.
+ */
+#ifndef CLIMBER_H_
+#define CLIMBER_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CLIMBER_ABI_VERSION 1
+
+typedef enum {
+  CLIMBER_OK = 0,
+  CLIMBER_E_INVALID_ARG = 1,   /* NULL pointer, M < 1, M > max_candidates, B < 1, ... */
+  CLIMBER_E_CONFIG = 2,        /* d % h, unequal budgets, tau <= 0 or non-finite, empty masks */
+  CLIMBER_E_OUT_OF_RANGE = 3,  /* item/action/scenario id outside the vocabulary (device-detected) */
+  CLIMBER_E_UNSORTED = 4,      /* decreasing timestamps in a lifecycle sequence (device-detected) */
+  CLIMBER_E_CAPACITY = 5,      /* K/V page pool, handle table or arena exhausted */
+  CLIMBER_E_STALE = 6,         /* handle released, from another ctx, or double release */
+  CLIMBER_E_CUDA = 7,          /* a CUDA runtime call failed */
+  CLIMBER_E_NCCL = 8,          /* a collective failed */
+  CLIMBER_E_NUMERIC = 9,       /* non-finite score (checked when CLIMBER_SYNC_CHECK=1) */
+  CLIMBER_E_UNSUPPORTED = 10   /* valid request this build does not implement */
+} climber_status;
+
+typedef enum { CLIMBER_BF16 = 0, CLIMBER_FP32 = 1 } climber_dtype;
+
+/* Model + capacity configuration.  Budgets are equal by construction
+ * (n_k = n / N_b), so a single n_k describes all blocks. */
+typedef struct {
+  int32_t abi_version;      /* must be CLIMBER_ABI_VERSION */
+  int32_t d;                /* model width; d % n_heads == 0; d % 32 == 0 */
+  int32_t n_heads;          /* h; d_h = d / h in {16, 32, 64} */
+  int32_t n_layers;         /* L >= 1, ATLs per block */
+  int32_t n_blocks;         /* N_b in [1, 8], one per extraction strategy */
+  int32_t n_k;              /* per-block budget, multiple of 32, <= 1024 */
+  int32_t ffn_mult;         /* F = ffn_mult * d (4, G8) */
+  int32_t se_reduction;     /* squeeze-and-excitation reduction (4, G17) */
+  int32_t vocab;            /* item vocabulary size V */
+  int32_t n_actions;        /* action vocabulary (<= 64) */
+  int32_t n_scenarios;      /* R (<= 64) */
+  int32_t max_candidates;   /* max M per request */
+  int32_t hist_causal;      /* 1: causal history attention (G1), 0: bidirectional */
+  int32_t dtype;            /* climber_dtype: BF16 (tcgen05 path) or FP32 (verification build) */
+  int32_t page_tokens;      /* K/V page size in tokens; must be 64 */
+  float rms_eps;            /* RMSNorm epsilon (1e-6, G7) */
+  int32_t max_batch_users;  /* max users per batched call */
+  int32_t max_wave_users;   /* users encoded per internal wave (scratch sizing) */
+  int32_t max_wave_pairs;   /* candidate pairs scored per internal wave (scratch sizing) */
+  int64_t kv_pages;         /* K/V page-pool capacity in pages */
+} climber_config;
+
+/* One extraction strategy a_k (Eq. 2): keep event e iff
+ * (action_mask >> action[e]) & 1 and (scenario_mask >> scenario[e]) & 1. */
+typedef struct {
+  uint64_t action_mask;
+  uint64_t scenario_mask;
+} climber_strategy;
+
+/* A lifecycle sequence S (Eq. 1), structure of arrays, chronological
+ * (non-decreasing ts; ties keep input order).  DEVICE pointers. */
+typedef struct {
+  const int32_t* item;      /* [n_s] item ids in [0, vocab) */
+  const uint8_t* action;    /* [n_s] action ids in [0, n_actions) */
+  const uint8_t* scenario;  /* [n_s] scenario ids in [0, n_scenarios) */
+  const int64_t* ts;        /* [n_s] timestamps, non-decreasing */
+} climber_events;
+
+/* Parameters: HOST fp32 arrays, row-major, matrices in [in][out] layout.
+ * They are copied (and, for BF16, rounded RNE to bf16 and transposed to the
+ * K-major layout the tensor cores read) into the arena at climber_create; the
+ * caller may free them afterwards.  Shapes (F = ffn_mult d, D = N_b d,
+ * Hs = D / se_reduction, QKV columns are [Q | K | V], heads contiguous d_h): */
+typedef struct {
+  const float* emb_item;  /* [vocab][d]        */
+  const float* emb_act;   /* [n_actions][d]    */
+  const float* emb_scn;   /* [n_scenarios][d]  */
+  const float* g1;        /* [N_b][L][d]       pre-attention RMSNorm gain */
+  const float* w_qkv;     /* [N_b][L][d][3d]   f_QKV */
+  const float* w_o;       /* [N_b][L][d][d]    */
+  const float* g2;        /* [N_b][L][d]       pre-FFN RMSNorm gain */
+  const float* w1;        /* [N_b][L][d][F]    */
+  const float* w2;        /* [N_b][L][F][d]    */
+  const float* tau;       /* [L][N_b][R][h]    f_tc(a_k, r) per head, > 0 */
+  const float* f_g1;      /* fusion ATL: [d]   */
+  const float* f_w_qkv;   /* [d][3d] */
+  const float* f_w_o;     /* [d][d]  */
+  const float* f_g2;      /* [d]     */
+  const float* f_w1;      /* [d][F]  */
+  const float* f_w2;      /* [F][d]  */
+  const float* tau_f;     /* [R][h]  */
+  const float* w_se1;     /* [D][Hs] */
+  const float* b_se1;     /* [Hs]    */
+  const float* w_se2;     /* [Hs][D] */
+  const float* b_se2;     /* [D]     */
+  const float* w_head;    /* [D]     */
+  float b_head;
+} climber_weights;
+
+typedef struct climber_ctx_s* climber_ctx_t;
+typedef struct climber_kv_s* climber_kv_t;   /* one user's multi-layer K/V cache */
+typedef void* climber_stream_t;               /* a cudaStream_t (NULL = legacy default) */
+
+/* Device bytes climber_create needs for this config (weights + K/V page pool +
+ * handle tables + scratch).  Returns 0 for an invalid config. */
+size_t climber_arena_bytes(const climber_config* cfg);
+
+/* Create a context.  `arena` is a DEVICE buffer of >= climber_arena_bytes(cfg)
+ * bytes, 256-byte aligned, borrowed for the ctx's lifetime (e.g. a torch
+ * tensor).  `strategies` is a host array of n_blocks entries.  Multi-GPU
+ * candidate sharding (rank/world/nccl_uid) is NEXT: world must be 1 and
+ * nccl_uid NULL in this build, else CLIMBER_E_UNSUPPORTED.  Synchronous. */
+climber_status climber_create(const climber_config* cfg, const climber_strategy* strategies,
+                              const climber_weights* weights, void* arena, size_t arena_bytes,
+                              int32_t rank, int32_t world, const void* nccl_uid,
+                              climber_ctx_t* out);
+
+/* Destroy: synchronises the device, releases host state; the arena is the
+ * caller's to free afterwards.  Outstanding handles become invalid. */
+climber_status climber_destroy(climber_ctx_t ctx);
+
+/* Encode one user (PAPER.md L257 step 1): validate and extract (Eq. 2), embed,
+ * run the N_b block stacks over the history and write every layer's K and V
+ * (bf16 or fp32 per dtype) into pages of the ctx pool.  `events` holds DEVICE
+ * pointers to n_s >= 0 events; `scenario_r` is the request scenario r (G4).
+ * The handle is returned synchronously; its contents are valid in stream order. */
+climber_status climber_encode_user(climber_ctx_t ctx, const climber_events* events, int64_t n_s,
+                                   int32_t scenario_r, climber_stream_t stream, climber_kv_t* out);
+
+/* Batched encode of B users.  ev_offsets: HOST int64[B+1], user b's events are
+ * [ev_offsets[b], ev_offsets[b+1]) of the DEVICE arrays in `events`.
+ * scenario_r: HOST int32[B].  out: HOST array of B handles. */
+climber_status climber_encode_users(climber_ctx_t ctx, int32_t B, const int64_t* ev_offsets,
+                                    const climber_events* events, const int32_t* scenario_r,
+                                    climber_stream_t stream, climber_kv_t* out);
+
+/* Score M candidates of one user against its cache (PAPER.md L255, L257 step
+ * 3).  items: DEVICE int32[M], 1 <= M <= max_candidates; scores: DEVICE
+ * float[M], logits in candidate order. */
+climber_status climber_score_items(climber_ctx_t ctx, climber_kv_t kv, const int32_t* items,
+                                   int32_t M, float* scores, climber_stream_t stream);
+
+/* Batched scoring: user b's candidates are items[cand_offsets[b] ..
+ * cand_offsets[b+1]) (cand_offsets: HOST int64[B+1], each count in
+ * [1, max_candidates]); scores are written at the same positions. */
+climber_status climber_score_items_batched(climber_ctx_t ctx, int32_t B, const climber_kv_t* kvs,
+                                           const int64_t* cand_offsets, const int32_t* items,
+                                           float* scores, climber_stream_t stream);
+
+/* End-to-end convenience call with HOST buffers: copies the events and the
+ * candidates to the device, encodes, scores, copies the scores back to
+ * `scores` (HOST float[cand_offsets[B]]), releases the handles and
+ * synchronises `stream`.  Same layouts as the batched calls, host memory. */
+climber_status climber_rank_host(climber_ctx_t ctx, int32_t B, const int64_t* ev_offsets,
+                                 const int32_t* item, const uint8_t* action, const uint8_t* scenario,
+                                 const int64_t* ts, const int32_t* scenario_r,
+                                 const int64_t* cand_offsets, const int32_t* items, float* scores,
+                                 climber_stream_t stream);
+
+/* Return a handle's pages to the pool.  The caller must ensure no enqueued
+ * work still reads it.  Double release -> CLIMBER_E_STALE. */
+climber_status climber_kv_release(climber_ctx_t ctx, climber_kv_t kv);
+
+/* Multi-GPU K/V replication for candidate sharding — NEXT;
+ * returns CLIMBER_E_UNSUPPORTED in this build. */
+climber_status climber_kv_broadcast(climber_ctx_t ctx, climber_kv_t* kv, int32_t root,
+                                    climber_stream_t stream);
+
+/* Synchronise `stream` and report the first device-side error recorded since
+ * the last call (then clear it): OK, E_OUT_OF_RANGE, E_UNSORTED, E_CUDA. */
+climber_status climber_stream_status(climber_ctx_t ctx, climber_stream_t stream);
+
+/* Thread-local description of the last failure on this thread ("" if none). */
+const char* climber_last_error(void);
+
+/* ---- debug exports (synchronous; for bit-exact parity tests) ---- */
+
+/* Canonical extraction result (G12): idx HOST int32[N_b][n_k], event indices
+ * relative to the user's first event, left-padded with -1; vlen HOST int32[N_b]. */
+climber_status climber_debug_extract(climber_ctx_t ctx, climber_kv_t kv, int32_t* idx, int32_t* vlen);
+
+/* Canonical SUMI masks for M candidates, evaluated on the device from the same
+ * visibility rule the attention kernels use: HOST uint8[N_b][(n_k+M)^2],
+ * row-major, history slots left-padded, 1 = attend. */
+climber_status climber_debug_mask(climber_ctx_t ctx, climber_kv_t kv, int32_t M, uint8_t* mask);
+
+/* One layer/block of the cache, gathered from its pages in canonical order:
+ * K, V HOST arrays [vlen][d] of float (dtype FP32) or uint16 bf16 bits (BF16);
+ * rows = vlen[block] of the most recent extraction. */
+climber_status climber_debug_kv(climber_ctx_t ctx, climber_kv_t kv, int32_t layer, int32_t block,
+                                void* K, void* V);
+
+/* The bf16 tensor-core GEMM of the path in isolation: D[m][n] += sum_k
+ * A[m][k] * B[n][k] (fp32 accumulate, fp32 residual-add epilogue).  DEVICE
+ * pointers: A bf16 [M][K], B bf16 [N][K], D float [M][N]; K % 64 == 0,
+ * N % 128 == 0 (else E_UNSUPPORTED).  use_tc = 0 runs the SIMT kernel.
+ * Asynchronous on `stream`. */
+climber_status climber_debug_gemm(const void* A, const void* B, float* D, int64_t M, int32_t N, int32_t K,
+                                  int32_t use_tc, climber_stream_t stream);
+
+/* Number of kernel launches the library has enqueued since the ctx was
+ * created (bench evidence for "gpu_launches"). */
+int64_t climber_launch_count(climber_ctx_t ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CLIMBER_H_ */

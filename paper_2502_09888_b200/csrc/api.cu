@@ -1,0 +1,881 @@
+// libclimber C ABI (include/climber.h): context, arena carving, K/V page pool,
+// handles, and the per-request orchestration of the SUMI hot path
+// (SURVEY §3 call stacks 1-2; PAPER.md L257 serving steps).
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/climber.h"
+#include "kernels.cuh"
+
+using namespace climber;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_last_error;
+
+static climber_status fail(climber_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+#define CU(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) return fail(CLIMBER_E_CUDA, "%s: %s", #x, cudaGetErrorString(e_)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+struct Carver {
+  char* base;  // nullptr: dry run (size only)
+  size_t off = 0;
+  template <typename P>
+  void take(P*& p, size_t bytes) {
+    off = (off + 255) & ~size_t(255);
+    p = base ? reinterpret_cast<P*>(base + off) : nullptr;
+    off += bytes;
+  }
+};
+
+struct SlotState {
+  uint32_t gen = 1;
+  bool live = false;
+  int r = 0;
+  std::vector<int> pages;
+};
+
+struct climber_ctx_s {
+  climber_config cfg;
+  Dims D;
+  size_t esz;           // bytes per stored element (2 bf16, 4 fp32)
+  uint16_t ctx_id;
+  std::vector<climber_strategy> strat;
+  // weights (device)
+  void *e_item, *e_act, *e_scn;
+  float *g1, *g2, *tau, *fg1, *fg2, *tau_f, *b_se1, *b_se2, *w_head;
+  void *w_qkv, *w_o, *w1, *w2, *fw_qkv, *fw_o, *fw1, *fw2, *w_se1, *w_se2;
+  float b_head;
+  unsigned long long *amask, *smask;
+  // K/V pool + per-slot tables (device)
+  void* pool;
+  long long n_pages;
+  int per_slot;  // pages per handle = Nb * L * ppb
+  int max_slots;
+  int *ptab, *vlen_all, *idx_all, *bad_all, *err;
+  // per-call metadata (device) and its pinned host staging
+  int64_t *d_ev_off, *d_cand_off;
+  int *d_slots, *d_r, *d_ptab_stage;
+  char* h_stage;
+  size_t stage_bytes;
+  cudaEvent_t stage_evt;
+  // scratch (device)
+  long long rows_cap;
+  float* X;
+  void *H, *QKV, *O, *Fh;
+  // host bookkeeping
+  std::mutex mu;
+  std::vector<int> free_pages;
+  std::vector<int> free_slots;
+  std::vector<SlotState> slots;
+  long long launches = 0;
+  bool use_tc = true;
+  bool sync_check = false;
+  // rank_host staging (device, lazily allocated)
+  void* io = nullptr;
+  size_t io_bytes = 0;
+};
+
+static uint16_t g_next_ctx_id = 1;
+static std::mutex g_ctx_mu;
+
+static climber_kv_t make_handle(const climber_ctx_s* c, int slot, uint32_t gen) {
+  uint64_t v = (uint64_t(c->ctx_id) << 48) | (uint64_t(gen & 0xFFFFFF) << 24) | uint64_t(slot + 1);
+  return reinterpret_cast<climber_kv_t>(v);
+}
+
+static climber_status resolve(climber_ctx_s* c, climber_kv_t kv, int* slot_out) {
+  uint64_t v = reinterpret_cast<uint64_t>(kv);
+  if (!kv) return fail(CLIMBER_E_INVALID_ARG, "null kv handle");
+  if ((v >> 48) != c->ctx_id) return fail(CLIMBER_E_STALE, "kv handle belongs to another ctx");
+  int slot = int(v & 0xFFFFFF) - 1;
+  uint32_t gen = uint32_t((v >> 24) & 0xFFFFFF);
+  if (slot < 0 || slot >= c->max_slots) return fail(CLIMBER_E_STALE, "kv handle slot out of range");
+  const SlotState& s = c->slots[slot];
+  if (!s.live || (s.gen & 0xFFFFFF) != gen) return fail(CLIMBER_E_STALE, "kv handle released or stale");
+  *slot_out = slot;
+  return CLIMBER_OK;
+}
+
+static bool dims_from(const climber_config* cfg, Dims* D, std::string* why) {
+  if (cfg->abi_version != CLIMBER_ABI_VERSION) { *why = "abi_version mismatch"; return false; }
+  if (cfg->d <= 0 || cfg->n_heads <= 0 || cfg->d % cfg->n_heads) { *why = "d % n_heads != 0"; return false; }
+  int dh = cfg->d / cfg->n_heads;
+  if (dh != 16 && dh != 32 && dh != 64) { *why = "d_h must be 16, 32 or 64"; return false; }
+  if (cfg->d % 32) { *why = "d must be a multiple of 32"; return false; }
+  if (cfg->n_layers < 1 || cfg->n_blocks < 1 || cfg->n_blocks > 8) { *why = "need L >= 1, 1 <= N_b <= 8"; return false; }
+  if (cfg->n_k < 32 || cfg->n_k % 32 || cfg->n_k > 1024) { *why = "n_k must be a multiple of 32 in [32, 1024]"; return false; }
+  if (cfg->ffn_mult < 1 || cfg->se_reduction < 1 || (cfg->n_blocks * cfg->d) % cfg->se_reduction ||
+      ((cfg->n_blocks * cfg->d) / cfg->se_reduction) % 16) { *why = "bad ffn_mult / se_reduction"; return false; }
+  if (cfg->vocab < 1 || cfg->n_actions < 1 || cfg->n_actions > 64 || cfg->n_scenarios < 1 || cfg->n_scenarios > 64) {
+    *why = "bad vocabulary sizes"; return false; }
+  if (cfg->max_candidates < 1) { *why = "max_candidates < 1"; return false; }
+  if (cfg->dtype != CLIMBER_BF16 && cfg->dtype != CLIMBER_FP32) { *why = "bad dtype"; return false; }
+  if (cfg->page_tokens != PAGE) { *why = "page_tokens must be 64"; return false; }
+  if (!(cfg->rms_eps >= 0.f)) { *why = "rms_eps < 0"; return false; }
+  if (cfg->max_batch_users < 1 || cfg->max_wave_users < 1 || cfg->max_wave_pairs < cfg->max_candidates ||
+      cfg->kv_pages < 1) { *why = "bad capacity fields (max_wave_pairs must be >= max_candidates)"; return false; }
+  D->d = cfg->d; D->h = cfg->n_heads; D->dh = dh; D->L = cfg->n_layers; D->Nb = cfg->n_blocks; D->nk = cfg->n_k;
+  D->F = cfg->ffn_mult * cfg->d; D->Dse = cfg->n_blocks * cfg->d; D->Hse = D->Dse / cfg->se_reduction;
+  D->V = cfg->vocab; D->A = cfg->n_actions; D->R = cfg->n_scenarios; D->Mmax = cfg->max_candidates;
+  D->causal = cfg->hist_causal ? 1 : 0; D->ppb = (cfg->n_k + PAGE - 1) / PAGE; D->eps = cfg->rms_eps;
+  return true;
+}
+
+static void carve(climber_ctx_s* c, Carver& cv) {
+  const Dims& D = c->D;
+  const size_t e = c->esz;
+  const size_t d = D.d, L = D.L, Nb = D.Nb, F = D.F;
+  cv.take(c->e_item, (size_t)D.V * d * e);
+  cv.take(c->e_act, (size_t)D.A * d * e);
+  cv.take(c->e_scn, (size_t)D.R * d * e);
+  cv.take(c->g1, Nb * L * d * 4);
+  cv.take(c->g2, Nb * L * d * 4);
+  cv.take(c->w_qkv, Nb * L * 3 * d * d * e);
+  cv.take(c->w_o, Nb * L * d * d * e);
+  cv.take(c->w1, Nb * L * F * d * e);
+  cv.take(c->w2, Nb * L * d * F * e);
+  cv.take(c->tau, L * Nb * D.R * D.h * 4);
+  cv.take(c->fg1, d * 4);
+  cv.take(c->fg2, d * 4);
+  cv.take(c->fw_qkv, 3 * d * d * e);
+  cv.take(c->fw_o, d * d * e);
+  cv.take(c->fw1, F * d * e);
+  cv.take(c->fw2, d * F * e);
+  cv.take(c->tau_f, (size_t)D.R * D.h * 4);
+  cv.take(c->w_se1, (size_t)D.Hse * D.Dse * e);
+  cv.take(c->b_se1, (size_t)D.Hse * 4);
+  cv.take(c->w_se2, (size_t)D.Dse * D.Hse * e);
+  cv.take(c->b_se2, (size_t)D.Dse * 4);
+  cv.take(c->w_head, (size_t)D.Dse * 4);
+  cv.take(c->amask, Nb * 8);
+  cv.take(c->smask, Nb * 8);
+  // K/V pool: page = [2][h][64][dh]
+  c->per_slot = D.Nb * D.L * D.ppb;
+  c->n_pages = c->cfg.kv_pages;
+  c->max_slots = (int)(c->n_pages / c->per_slot);
+  cv.take(c->pool, (size_t)c->n_pages * 2 * PAGE * d * e);
+  size_t S = (size_t)(c->max_slots > 0 ? c->max_slots : 1);
+  cv.take(c->ptab, S * c->per_slot * 4);
+  cv.take(c->vlen_all, S * Nb * 4);
+  cv.take(c->idx_all, S * Nb * D.nk * 4);
+  cv.take(c->bad_all, S * 4);
+  cv.take(c->err, 256);
+  // per-call metadata
+  size_t Bm = c->cfg.max_batch_users;
+  cv.take(c->d_ev_off, (Bm + 1) * 8);
+  cv.take(c->d_cand_off, (2 * Bm + 1) * 8);
+  cv.take(c->d_slots, Bm * 4);
+  cv.take(c->d_r, Bm * 4);
+  cv.take(c->d_ptab_stage, Bm * c->per_slot * 4);
+  // scratch
+  long long rows_h = (long long)c->cfg.max_wave_users * D.nk;
+  long long rows_c = (long long)c->cfg.max_wave_pairs * D.Nb;
+  c->rows_cap = rows_h > rows_c ? rows_h : rows_c;
+  size_t R = (size_t)c->rows_cap;
+  cv.take(c->X, R * d * 4);
+  cv.take(c->H, R * d * e);
+  cv.take(c->QKV, R * 3 * d * e);
+  cv.take(c->O, R * d * e);
+  cv.take(c->Fh, R * F * e);
+}
+
+// ---------------------------------------------------------------------------
+// weight upload (host fp32 [in][out] -> device T, GEMM B operands K-major)
+// ---------------------------------------------------------------------------
+static uint16_t bf16_rne(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+struct Uploader {
+  climber_ctx_s* c;
+  std::vector<char> buf;
+  climber_status st = CLIMBER_OK;
+  // copy `n` values, optionally transposing each of `batch` [rows][cols] matrices
+  void put(void* dst, const float* src, size_t batch, size_t rows, size_t cols, bool transpose, bool as_T) {
+    if (st != CLIMBER_OK) return;
+    size_t n = batch * rows * cols, es = as_T ? c->esz : 4;
+    buf.resize(n * es);
+    for (size_t b = 0; b < batch; ++b)
+      for (size_t i = 0; i < rows; ++i)
+        for (size_t j = 0; j < cols; ++j) {
+          size_t si = b * rows * cols + i * cols + j;
+          size_t di = transpose ? b * rows * cols + j * rows + i : si;
+          float v = src[si];
+          if (es == 2) {
+            uint16_t h = bf16_rne(v);
+            memcpy(&buf[di * 2], &h, 2);
+          } else {
+            memcpy(&buf[di * 4], &v, 4);
+          }
+        }
+    cudaError_t e = cudaMemcpy(dst, buf.data(), n * es, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) st = fail(CLIMBER_E_CUDA, "weight upload: %s", cudaGetErrorString(e));
+  }
+};
+
+extern "C" size_t climber_arena_bytes(const climber_config* cfg) {
+  if (!cfg) return 0;
+  climber_ctx_s c;
+  std::string why;
+  if (!dims_from(cfg, &c.D, &why)) return 0;
+  c.cfg = *cfg;
+  c.esz = cfg->dtype == CLIMBER_BF16 ? 2 : 4;
+  Carver cv{nullptr};
+  carve(&c, cv);
+  return cv.off + 256;
+}
+
+extern "C" climber_status climber_create(const climber_config* cfg, const climber_strategy* strategies,
+                                         const climber_weights* w, void* arena, size_t arena_bytes, int32_t rank,
+                                         int32_t world, const void* nccl_uid, climber_ctx_t* out) {
+  try {
+    if (!cfg || !strategies || !w || !arena || !out) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+    if (world != 1 || rank != 0 || nccl_uid)
+      return fail(CLIMBER_E_UNSUPPORTED, "multi-GPU candidate sharding is not in this build (world must be 1)");
+    if (reinterpret_cast<uintptr_t>(arena) % 256) return fail(CLIMBER_E_INVALID_ARG, "arena must be 256-byte aligned");
+    std::string why;
+    Dims D;
+    if (!dims_from(cfg, &D, &why)) return fail(CLIMBER_E_CONFIG, "config: %s", why.c_str());
+    for (int k = 0; k < cfg->n_blocks; ++k)
+      if (!strategies[k].action_mask || !strategies[k].scenario_mask)
+        return fail(CLIMBER_E_CONFIG, "strategy %d has an empty filter", k);
+    const float* need[] = {w->emb_item, w->emb_act, w->emb_scn, w->g1, w->w_qkv, w->w_o, w->g2, w->w1, w->w2,
+                           w->tau, w->f_g1, w->f_w_qkv, w->f_w_o, w->f_g2, w->f_w1, w->f_w2, w->tau_f,
+                           w->w_se1, w->b_se1, w->w_se2, w->b_se2, w->w_head};
+    for (const float* p : need)
+      if (!p) return fail(CLIMBER_E_INVALID_ARG, "null weight pointer");
+    size_t ntau = (size_t)D.L * D.Nb * D.R * D.h;
+    for (size_t i = 0; i < ntau; ++i)
+      if (!(w->tau[i] > 0.f) || !std::isfinite(w->tau[i])) return fail(CLIMBER_E_CONFIG, "tau[%zu] <= 0 or non-finite", i);
+    for (size_t i = 0; i < (size_t)D.R * D.h; ++i)
+      if (!(w->tau_f[i] > 0.f) || !std::isfinite(w->tau_f[i])) return fail(CLIMBER_E_CONFIG, "tau_f[%zu] <= 0 or non-finite", i);
+
+    auto* c = new climber_ctx_s();
+    c->cfg = *cfg;
+    c->D = D;
+    c->esz = cfg->dtype == CLIMBER_BF16 ? 2 : 4;
+    {
+      std::lock_guard<std::mutex> g(g_ctx_mu);
+      c->ctx_id = g_next_ctx_id++;
+      if (g_next_ctx_id == 0) g_next_ctx_id = 1;
+    }
+    c->strat.assign(strategies, strategies + cfg->n_blocks);
+    Carver dry{nullptr};
+    carve(c, dry);
+    if (dry.off + 256 > arena_bytes) {
+      delete c;
+      return fail(CLIMBER_E_CAPACITY, "arena too small: need %zu bytes", dry.off + 256);
+    }
+    if (c->max_slots < 1) {
+      delete c;
+      return fail(CLIMBER_E_CAPACITY, "kv_pages %lld < pages per handle", (long long)cfg->kv_pages);
+    }
+    Carver cv{reinterpret_cast<char*>(arena)};
+    carve(c, cv);
+    const char* env = getenv("CLIMBER_GEMM");
+    c->use_tc = !(env && strcmp(env, "simt") == 0);
+    const char* sc = getenv("CLIMBER_SYNC_CHECK");
+    c->sync_check = sc && atoi(sc) != 0;
+
+    const size_t d = D.d, L = D.L, Nb = D.Nb, F = D.F;
+    Uploader up{c};
+    up.put(c->e_item, w->emb_item, 1, D.V, d, false, true);
+    up.put(c->e_act, w->emb_act, 1, D.A, d, false, true);
+    up.put(c->e_scn, w->emb_scn, 1, D.R, d, false, true);
+    up.put(c->g1, w->g1, 1, Nb * L, d, false, false);
+    up.put(c->g2, w->g2, 1, Nb * L, d, false, false);
+    up.put(c->w_qkv, w->w_qkv, Nb * L, d, 3 * d, true, true);
+    up.put(c->w_o, w->w_o, Nb * L, d, d, true, true);
+    up.put(c->w1, w->w1, Nb * L, d, F, true, true);
+    up.put(c->w2, w->w2, Nb * L, F, d, true, true);
+    up.put(c->tau, w->tau, 1, 1, ntau, false, false);
+    up.put(c->fg1, w->f_g1, 1, 1, d, false, false);
+    up.put(c->fg2, w->f_g2, 1, 1, d, false, false);
+    up.put(c->fw_qkv, w->f_w_qkv, 1, d, 3 * d, true, true);
+    up.put(c->fw_o, w->f_w_o, 1, d, d, true, true);
+    up.put(c->fw1, w->f_w1, 1, d, F, true, true);
+    up.put(c->fw2, w->f_w2, 1, F, d, true, true);
+    up.put(c->tau_f, w->tau_f, 1, 1, (size_t)D.R * D.h, false, false);
+    up.put(c->w_se1, w->w_se1, 1, D.Dse, D.Hse, true, true);
+    up.put(c->b_se1, w->b_se1, 1, 1, D.Hse, false, false);
+    up.put(c->w_se2, w->w_se2, 1, D.Hse, D.Dse, true, true);
+    up.put(c->b_se2, w->b_se2, 1, 1, D.Dse, false, false);
+    up.put(c->w_head, w->w_head, 1, 1, D.Dse, false, false);
+    if (up.st != CLIMBER_OK) {
+      delete c;
+      return up.st;
+    }
+    c->b_head = w->b_head;
+    std::vector<unsigned long long> am(Nb), sm(Nb);
+    for (size_t k = 0; k < Nb; ++k) {
+      am[k] = strategies[k].action_mask;
+      sm[k] = strategies[k].scenario_mask;
+    }
+    CU(cudaMemcpy(c->amask, am.data(), Nb * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(c->smask, sm.data(), Nb * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemset(c->err, 0, 256));
+    // host state
+    c->free_pages.resize(c->n_pages);
+    for (long long i = 0; i < c->n_pages; ++i) c->free_pages[i] = (int)(c->n_pages - 1 - i);
+    c->slots.resize(c->max_slots);
+    c->free_slots.resize(c->max_slots);
+    for (int i = 0; i < c->max_slots; ++i) c->free_slots[i] = c->max_slots - 1 - i;
+    size_t Bm = cfg->max_batch_users;
+    c->stage_bytes = (Bm + 1) * 8 + (2 * Bm + 1) * 8 + Bm * 8 + Bm * (size_t)c->per_slot * 4 + 1024;
+    CU(cudaMallocHost(&c->h_stage, c->stage_bytes));
+    CU(cudaEventCreateWithFlags(&c->stage_evt, cudaEventDisableTiming));
+    CU(cudaEventRecord(c->stage_evt, 0));
+    CU(cudaDeviceSynchronize());
+    *out = c;
+    return CLIMBER_OK;
+  } catch (const std::exception& ex) {
+    return fail(CLIMBER_E_CUDA, "create: %s", ex.what());
+  } catch (...) {
+    return fail(CLIMBER_E_CUDA, "create: unknown exception");
+  }
+}
+
+extern "C" climber_status climber_destroy(climber_ctx_t c) {
+  if (!c) return fail(CLIMBER_E_INVALID_ARG, "null ctx");
+  cudaDeviceSynchronize();
+  if (c->h_stage) cudaFreeHost(c->h_stage);
+  if (c->io) cudaFree(c->io);
+  cudaEventDestroy(c->stage_evt);
+  delete c;
+  return CLIMBER_OK;
+}
+
+// ---------------------------------------------------------------------------
+// GEMM dispatch: tcgen05 tensor cores for bf16, SIMT for the fp32 build
+// ---------------------------------------------------------------------------
+template <typename T>
+static void gemm(climber_ctx_s* c, const T* A, long long lda, const T* B, long long ldb, long long M, int N, int K,
+                 const Epilogue& e, cudaStream_t s) {
+  c->launches++;
+  if constexpr (std::is_same<T, bf16>::value) {
+    if (c->use_tc && gemm_tc_supported(M, N, K, lda, ldb)) {
+      launch_gemm_tc(A, lda, B, ldb, M, N, K, e, s);
+      return;
+    }
+  }
+  launch_gemm_simt<T>(A, lda, B, ldb, M, N, K, e, s);
+}
+
+static Epilogue epi_store(void* out, long long ldo, int act = ACT_NONE, const float* bias = nullptr) {
+  Epilogue e{};
+  e.kind = EPI_STORE; e.act = act; e.out = out; e.ldo = ldo; e.bias = bias;
+  return e;
+}
+static Epilogue epi_resid(float* out, long long ldo) {
+  Epilogue e{};
+  e.kind = EPI_RESID; e.out = out; e.ldo = ldo;
+  return e;
+}
+
+// ---------------------------------------------------------------------------
+// encode: one wave of U users (SURVEY §3 call stack 1)
+// ---------------------------------------------------------------------------
+template <typename T>
+static void encode_wave(climber_ctx_s* c, const EventsDev& ev, int u0, int U, cudaStream_t s) {
+  const Dims& D = c->D;
+  const long long rows = (long long)U * D.nk;
+  const long long d = D.d, F = D.F;
+  const int* wslot = c->d_slots + u0;
+  const int* wr = c->d_r + u0;
+  launch_extract(ev, c->d_ev_off + u0, wslot, U, c->amask, c->smask, c->idx_all, c->vlen_all, c->bad_all, c->err, D, s);
+  c->launches++;
+  T* H = (T*)c->H;
+  T* Qb = (T*)c->QKV;
+  T* O = (T*)c->O;
+  T* Fh = (T*)c->Fh;
+  for (int k = 0; k < D.Nb; ++k) {
+    launch_embed_hist<T>(ev, c->d_ev_off + u0, wslot, U, c->idx_all, c->vlen_all, c->bad_all, (const T*)c->e_item,
+                         (const T*)c->e_act, (const T*)c->e_scn, c->X, k, D, s);
+    c->launches++;
+    for (int l = 0; l < D.L; ++l) {
+      const size_t kl = (size_t)k * D.L + l;
+      launch_rmsnorm<T>(c->X, d, c->g1 + kl * d, H, d, rows, D.d, D.eps, s);
+      c->launches++;
+      Epilogue e{};
+      e.kind = EPI_QKV_PAGES; e.out = Qb; e.ldo = d; e.pool = c->pool; e.ptab = c->ptab; e.wave_slot = wslot;
+      e.blk = k; e.layer = l; e.d = D.d; e.h = D.h; e.dh = D.dh; e.nk = D.nk; e.Nb = D.Nb; e.L = D.L; e.ppb = D.ppb;
+      const T* Wqkv = (const T*)c->w_qkv + kl * 3 * d * d;
+      if (l < D.L - 1) {
+        e.col_off = 0;
+        gemm<T>(c, H, d, Wqkv, d, rows, 3 * D.d, D.d, e, s);
+        launch_attn_hist<T>(Qb, wslot, wr, U, (const T*)c->pool, c->ptab, c->vlen_all, c->tau, O, k, l, D, s);
+        c->launches++;
+        gemm<T>(c, O, d, (const T*)c->w_o + kl * d * d, d, rows, D.d, D.d, epi_resid(c->X, d), s);
+        launch_rmsnorm<T>(c->X, d, c->g2 + kl * d, H, d, rows, D.d, D.eps, s);
+        c->launches++;
+        gemm<T>(c, H, d, (const T*)c->w1 + kl * F * d, d, rows, D.F, D.d, epi_store(Fh, F, ACT_SILU), s);
+        gemm<T>(c, Fh, F, (const T*)c->w2 + kl * d * F, F, rows, D.d, D.F, epi_resid(c->X, d), s);
+      } else {
+        // last layer: only K/V of the history are ever read -> N = 2d
+        e.col_off = D.d;
+        gemm<T>(c, H, d, Wqkv + d * d, d, rows, 2 * D.d, D.d, e, s);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// score: one wave of U users / P pairs (SURVEY §3 call stack 2)
+// ---------------------------------------------------------------------------
+template <typename T>
+static void score_wave(climber_ctx_s* c, const int32_t* items, const int64_t* wcand, int u0, int U, long long P,
+                       int Mmax_wave, float* scores, cudaStream_t s) {
+  const Dims& D = c->D;
+  const long long d = D.d, F = D.F, Nb = D.Nb, ldC = Nb * d;
+  const int* wslot = c->d_slots + u0;
+  const int* wr = c->d_r + u0;
+  T* H = (T*)c->H;
+  T* QKV = (T*)c->QKV;
+  T* O = (T*)c->O;
+  T* Fh = (T*)c->Fh;
+  float* X = c->X;  // C[p][k][d]
+  launch_embed_cand<T>(items, wcand, wr, U, P, (const T*)c->e_item, (const T*)c->e_scn, X, c->err, D, s);
+  c->launches++;
+  for (int k = 0; k < D.Nb; ++k) {
+    float* Ck = X + k * d;
+    for (int l = 0; l < D.L; ++l) {
+      const size_t kl = (size_t)k * D.L + l;
+      launch_rmsnorm<T>(Ck, ldC, c->g1 + kl * d, H, d, P, D.d, D.eps, s);
+      c->launches++;
+      gemm<T>(c, H, d, (const T*)c->w_qkv + kl * 3 * d * d, d, P, 3 * D.d, D.d, epi_store(QKV, 3 * d), s);
+      launch_attn_sumi<T>(QKV, wcand, wslot, wr, U, Mmax_wave, (const T*)c->pool, c->ptab, c->vlen_all, c->tau, O, k,
+                          l, D, s);
+      c->launches++;
+      gemm<T>(c, O, d, (const T*)c->w_o + kl * d * d, d, P, D.d, D.d, epi_resid(Ck, ldC), s);
+      launch_rmsnorm<T>(Ck, ldC, c->g2 + kl * d, H, d, P, D.d, D.eps, s);
+      c->launches++;
+      gemm<T>(c, H, d, (const T*)c->w1 + kl * F * d, d, P, D.F, D.d, epi_store(Fh, F, ACT_SILU), s);
+      gemm<T>(c, Fh, F, (const T*)c->w2 + kl * d * F, F, P, D.d, D.F, epi_resid(Ck, ldC), s);
+    }
+  }
+  // ---- BGF (Eq. 4): fusion ATL over the N_b tokens of every pair, rows = P*N_b
+  const long long R = P * Nb;
+  launch_rmsnorm<T>(X, d, c->fg1, H, d, R, D.d, D.eps, s);
+  c->launches++;
+  gemm<T>(c, H, d, (const T*)c->fw_qkv, d, R, 3 * D.d, D.d, epi_store(QKV, 3 * d), s);
+  launch_attn_fusion<T>(QKV, wcand, wr, U, P, c->tau_f, O, D, s);
+  c->launches++;
+  gemm<T>(c, O, d, (const T*)c->fw_o, d, R, D.d, D.d, epi_resid(X, d), s);
+  launch_rmsnorm<T>(X, d, c->fg2, H, d, R, D.d, D.eps, s);
+  c->launches++;
+  gemm<T>(c, H, d, (const T*)c->fw1, d, R, D.F, D.d, epi_store(Fh, F, ACT_SILU), s);
+  gemm<T>(c, Fh, F, (const T*)c->fw2, F, R, D.d, D.F, epi_resid(X, d), s);
+  // ---- squeeze-and-excitation gate on vec(G) = X viewed as [P][N_b d]
+  const T* G = nullptr;
+  if constexpr (std::is_same<T, float>::value) {
+    G = X;
+  } else {
+    launch_convert<T>(X, H, P * D.Dse, s);
+    c->launches++;
+    G = H;
+  }
+  T* Z1 = O;  // [P][Hse]
+  gemm<T>(c, G, D.Dse, (const T*)c->w_se1, D.Dse, P, D.Hse, D.Dse, epi_store(Z1, D.Hse, ACT_RELU, c->b_se1), s);
+  Epilogue eg{};
+  eg.kind = EPI_GATE; eg.out = X; eg.ldo = D.Dse; eg.bias = c->b_se2;
+  gemm<T>(c, Z1, D.Hse, (const T*)c->w_se2, D.Hse, P, D.Dse, D.Hse, eg, s);
+  // ---- head (G18)
+  launch_head(X, c->w_head, c->b_head, scores, P, D.Dse, s);
+  c->launches++;
+}
+
+// ---------------------------------------------------------------------------
+// staging of per-call metadata (one H2D copy per call, pinned buffer reused
+// only after the previous call's copy completed)
+// ---------------------------------------------------------------------------
+struct Stage {
+  int64_t* ev_off;
+  int64_t* cand_off;
+  int* slots;
+  int* r;
+  int* ptab;
+};
+
+static Stage stage_layout(climber_ctx_s* c, char* base) {
+  size_t Bm = c->cfg.max_batch_users;
+  Stage st;
+  st.ev_off = reinterpret_cast<int64_t*>(base);
+  st.cand_off = st.ev_off + (Bm + 1);
+  st.slots = reinterpret_cast<int*>(st.cand_off + (2 * Bm + 1));
+  st.r = st.slots + Bm;
+  st.ptab = st.r + Bm;
+  return st;
+}
+
+static climber_status stage_upload(climber_ctx_s* c, int B, bool with_ptab, cudaStream_t s) {
+  size_t Bm = c->cfg.max_batch_users;
+  Stage h = stage_layout(c, c->h_stage);
+  CU(cudaMemcpyAsync(c->d_ev_off, h.ev_off, (B + 1) * 8, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(c->d_cand_off, h.cand_off, (2 * Bm + 1) * 8, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(c->d_slots, h.slots, B * 4, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(c->d_r, h.r, B * 4, cudaMemcpyHostToDevice, s));
+  if (with_ptab) {
+    CU(cudaMemcpyAsync(c->d_ptab_stage, h.ptab, (size_t)B * c->per_slot * 4, cudaMemcpyHostToDevice, s));
+    launch_scatter_ptab(c->d_ptab_stage, c->d_slots, B, c->per_slot, c->ptab, s);
+    c->launches++;
+  }
+  CU(cudaEventRecord(c->stage_evt, s));
+  return CLIMBER_OK;
+}
+
+static climber_status check_launch(climber_ctx_s* c, cudaStream_t s) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(CLIMBER_E_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+  if (c->sync_check) {
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fail(CLIMBER_E_CUDA, "sync check: %s", cudaGetErrorString(e));
+  }
+  return CLIMBER_OK;
+}
+
+// ---------------------------------------------------------------------------
+// encode
+// ---------------------------------------------------------------------------
+extern "C" climber_status climber_encode_users(climber_ctx_t c, int32_t B, const int64_t* ev_offsets,
+                                               const climber_events* events, const int32_t* scenario_r,
+                                               climber_stream_t stream, climber_kv_t* out) {
+  try {
+    if (!c || !ev_offsets || !events || !scenario_r || !out) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+    if (B < 1 || B > c->cfg.max_batch_users) return fail(CLIMBER_E_INVALID_ARG, "B=%d outside [1, max_batch_users]", B);
+    for (int b = 0; b < B; ++b) {
+      if (ev_offsets[b + 1] < ev_offsets[b]) return fail(CLIMBER_E_INVALID_ARG, "ev_offsets decreasing at %d", b);
+      if (scenario_r[b] < 0 || scenario_r[b] >= c->D.R) return fail(CLIMBER_E_OUT_OF_RANGE, "scenario_r[%d] out of range", b);
+    }
+    if (ev_offsets[B] > ev_offsets[0] &&
+        (!events->item || !events->action || !events->scenario || !events->ts))
+      return fail(CLIMBER_E_INVALID_ARG, "null event array");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    std::vector<int> slots(B);
+    {
+      std::lock_guard<std::mutex> g(c->mu);
+      if ((int)c->free_slots.size() < B || (long long)c->free_pages.size() < (long long)B * c->per_slot)
+        return fail(CLIMBER_E_CAPACITY, "K/V page pool exhausted (%zu free slots)", c->free_slots.size());
+      CU(cudaEventSynchronize(c->stage_evt));
+      Stage h = stage_layout(c, c->h_stage);
+      for (int b = 0; b < B; ++b) {
+        int slot = c->free_slots.back();
+        c->free_slots.pop_back();
+        SlotState& st = c->slots[slot];
+        st.live = true;
+        st.r = scenario_r[b];
+        st.pages.resize(c->per_slot);
+        for (int i = 0; i < c->per_slot; ++i) {
+          st.pages[i] = c->free_pages.back();
+          c->free_pages.pop_back();
+          h.ptab[(size_t)b * c->per_slot + i] = st.pages[i];
+        }
+        slots[b] = slot;
+        h.slots[b] = slot;
+        h.r[b] = scenario_r[b];
+        h.ev_off[b] = ev_offsets[b];
+        out[b] = make_handle(c, slot, st.gen);
+      }
+      h.ev_off[B] = ev_offsets[B];
+      climber_status rs = stage_upload(c, B, true, s);
+      if (rs != CLIMBER_OK) return rs;
+    }
+    EventsDev ev{events->item, events->action, events->scenario, events->ts};
+    for (int u0 = 0; u0 < B; u0 += c->cfg.max_wave_users) {
+      int U = B - u0 < c->cfg.max_wave_users ? B - u0 : c->cfg.max_wave_users;
+      if (c->cfg.dtype == CLIMBER_BF16) encode_wave<bf16>(c, ev, u0, U, s);
+      else encode_wave<float>(c, ev, u0, U, s);
+      climber_status rs = check_launch(c, s);
+      if (rs != CLIMBER_OK) return rs;
+    }
+    return CLIMBER_OK;
+  } catch (...) {
+    return fail(CLIMBER_E_CUDA, "encode: exception");
+  }
+}
+
+extern "C" climber_status climber_encode_user(climber_ctx_t c, const climber_events* events, int64_t n_s,
+                                              int32_t scenario_r, climber_stream_t stream, climber_kv_t* out) {
+  if (n_s < 0) return fail(CLIMBER_E_INVALID_ARG, "n_s < 0");
+  int64_t off[2] = {0, n_s};
+  return climber_encode_users(c, 1, off, events, &scenario_r, stream, out);
+}
+
+// ---------------------------------------------------------------------------
+// score
+// ---------------------------------------------------------------------------
+extern "C" climber_status climber_score_items_batched(climber_ctx_t c, int32_t B, const climber_kv_t* kvs,
+                                                      const int64_t* cand_offsets, const int32_t* items,
+                                                      float* scores, climber_stream_t stream) {
+  try {
+    if (!c || !kvs || !cand_offsets || !items || !scores) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+    if (B < 1 || B > c->cfg.max_batch_users) return fail(CLIMBER_E_INVALID_ARG, "B=%d outside [1, max_batch_users]", B);
+    for (int b = 0; b < B; ++b) {
+      long long m = cand_offsets[b + 1] - cand_offsets[b];
+      if (m < 1 || m > c->cfg.max_candidates)
+        return fail(CLIMBER_E_INVALID_ARG, "user %d has M=%lld outside [1, max_candidates]", b, m);
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    // waves: consecutive users while pairs <= max_wave_pairs and users <= max_wave_users
+    struct Wave { int u0, U, Mmax; long long P; int coff; };
+    std::vector<Wave> waves;
+    {
+      std::lock_guard<std::mutex> g(c->mu);
+      std::vector<int> slots(B);
+      for (int b = 0; b < B; ++b) {
+        climber_status rs = resolve(c, kvs[b], &slots[b]);
+        if (rs != CLIMBER_OK) return rs;
+      }
+      CU(cudaEventSynchronize(c->stage_evt));
+      Stage h = stage_layout(c, c->h_stage);
+      int coff = 0;
+      for (int u0 = 0; u0 < B;) {
+        Wave w{u0, 0, 0, 0, coff};
+        while (u0 + w.U < B && w.U < c->cfg.max_wave_users) {
+          long long m = cand_offsets[u0 + w.U + 1] - cand_offsets[u0 + w.U];
+          if (w.P + m > c->cfg.max_wave_pairs) break;
+          w.P += m;
+          w.Mmax = w.Mmax > m ? w.Mmax : (int)m;
+          w.U++;
+        }
+        for (int i = 0; i <= w.U; ++i) h.cand_off[coff + i] = cand_offsets[u0 + i] - cand_offsets[u0];
+        coff += w.U + 1;
+        waves.push_back(w);
+        u0 += w.U;
+      }
+      for (int b = 0; b < B; ++b) {
+        h.slots[b] = slots[b];
+        h.r[b] = c->slots[slots[b]].r;
+      }
+      h.ev_off[0] = 0;
+      climber_status rs = stage_upload(c, B, false, s);
+      if (rs != CLIMBER_OK) return rs;
+    }
+    for (const Wave& w : waves) {
+      const int32_t* it = items + cand_offsets[w.u0];
+      float* sc = scores + cand_offsets[w.u0];
+      const int64_t* wc = c->d_cand_off + w.coff;
+      if (c->cfg.dtype == CLIMBER_BF16) score_wave<bf16>(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
+      else score_wave<float>(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
+      climber_status rs = check_launch(c, s);
+      if (rs != CLIMBER_OK) return rs;
+    }
+    return CLIMBER_OK;
+  } catch (...) {
+    return fail(CLIMBER_E_CUDA, "score: exception");
+  }
+}
+
+extern "C" climber_status climber_score_items(climber_ctx_t c, climber_kv_t kv, const int32_t* items, int32_t M,
+                                              float* scores, climber_stream_t stream) {
+  int64_t off[2] = {0, M};
+  return climber_score_items_batched(c, 1, &kv, off, items, scores, stream);
+}
+
+extern "C" climber_status climber_kv_release(climber_ctx_t c, climber_kv_t kv) {
+  if (!c) return fail(CLIMBER_E_INVALID_ARG, "null ctx");
+  std::lock_guard<std::mutex> g(c->mu);
+  int slot;
+  climber_status rs = resolve(c, kv, &slot);
+  if (rs != CLIMBER_OK) return rs;
+  SlotState& st = c->slots[slot];
+  for (int p : st.pages) c->free_pages.push_back(p);
+  st.pages.clear();
+  st.live = false;
+  st.gen = (st.gen + 1) & 0xFFFFFF;
+  if (st.gen == 0) st.gen = 1;
+  c->free_slots.push_back(slot);
+  return CLIMBER_OK;
+}
+
+extern "C" climber_status climber_kv_broadcast(climber_ctx_t c, climber_kv_t* kv, int32_t root,
+                                               climber_stream_t stream) {
+  (void)c; (void)kv; (void)root; (void)stream;
+  return fail(CLIMBER_E_UNSUPPORTED, "climber_kv_broadcast: multi-GPU candidate sharding is NEXT (world == 1)");
+}
+
+extern "C" climber_status climber_stream_status(climber_ctx_t c, climber_stream_t stream) {
+  if (!c) return fail(CLIMBER_E_INVALID_ARG, "null ctx");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CU(cudaStreamSynchronize(s));
+  int err = 0;
+  CU(cudaMemcpy(&err, c->err, 4, cudaMemcpyDeviceToHost));
+  CU(cudaMemset(c->err, 0, 4));
+  if (err & ERR_RANGE) return fail(CLIMBER_E_OUT_OF_RANGE, "an item/action/scenario id was out of range");
+  if (err & ERR_UNSORTED) return fail(CLIMBER_E_UNSORTED, "a lifecycle sequence had decreasing timestamps");
+  return CLIMBER_OK;
+}
+
+// ---------------------------------------------------------------------------
+// end-to-end call with host buffers
+// ---------------------------------------------------------------------------
+extern "C" climber_status climber_rank_host(climber_ctx_t c, int32_t B, const int64_t* ev_offsets,
+                                            const int32_t* item, const uint8_t* action, const uint8_t* scenario,
+                                            const int64_t* ts, const int32_t* scenario_r,
+                                            const int64_t* cand_offsets, const int32_t* items, float* scores,
+                                            climber_stream_t stream) {
+  if (!c || !ev_offsets || !scenario_r || !cand_offsets || !items || !scores)
+    return fail(CLIMBER_E_INVALID_ARG, "null argument");
+  if (B < 1 || B > c->cfg.max_batch_users) return fail(CLIMBER_E_INVALID_ARG, "B out of range");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t E = ev_offsets[B] - ev_offsets[0], P = cand_offsets[B] - cand_offsets[0];
+  if (E > 0 && (!item || !action || !scenario || !ts)) return fail(CLIMBER_E_INVALID_ARG, "null event array");
+  size_t need = (size_t)E * (4 + 1 + 1 + 8) + (size_t)P * (4 + 4) + 4096;
+  if (need > c->io_bytes) {
+    if (c->io) cudaFree(c->io);
+    c->io = nullptr;
+    c->io_bytes = 0;
+    CU(cudaMalloc(&c->io, need));
+    c->io_bytes = need;
+  }
+  char* p = (char*)c->io;
+  auto carve = [&](size_t bytes) { char* q = p; p += (bytes + 255) & ~size_t(255); return q; };
+  int64_t* d_ts = (int64_t*)carve((size_t)E * 8);
+  int32_t* d_item = (int32_t*)carve((size_t)E * 4);
+  int32_t* d_items = (int32_t*)carve((size_t)P * 4);
+  float* d_scores = (float*)carve((size_t)P * 4);
+  uint8_t* d_act = (uint8_t*)carve((size_t)E);
+  uint8_t* d_scn = (uint8_t*)carve((size_t)E);
+  const int64_t e0 = ev_offsets[0], c0 = cand_offsets[0];
+  if (E > 0) {
+    CU(cudaMemcpyAsync(d_item, item + e0, E * 4, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(d_act, action + e0, E, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(d_scn, scenario + e0, E, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(d_ts, ts + e0, E * 8, cudaMemcpyHostToDevice, s));
+  }
+  CU(cudaMemcpyAsync(d_items, items + c0, P * 4, cudaMemcpyHostToDevice, s));
+  std::vector<int64_t> eo(B + 1), co(B + 1);
+  for (int b = 0; b <= B; ++b) {
+    eo[b] = ev_offsets[b] - e0;
+    co[b] = cand_offsets[b] - c0;
+  }
+  climber_events ev{d_item, d_act, d_scn, d_ts};
+  std::vector<climber_kv_t> kvs(B);
+  climber_status st = climber_encode_users(c, B, eo.data(), &ev, scenario_r, stream, kvs.data());
+  if (st != CLIMBER_OK) return st;
+  st = climber_score_items_batched(c, B, kvs.data(), co.data(), d_items, d_scores, stream);
+  if (st == CLIMBER_OK) {
+    cudaError_t e = cudaMemcpyAsync(scores + c0, d_scores, P * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) st = fail(CLIMBER_E_CUDA, "rank_host: %s", cudaGetErrorString(e));
+  } else {
+    cudaStreamSynchronize(s);
+  }
+  for (int b = 0; b < B; ++b) climber_kv_release(c, kvs[b]);
+  return st;
+}
+
+// ---------------------------------------------------------------------------
+// debug exports
+// ---------------------------------------------------------------------------
+extern "C" climber_status climber_debug_extract(climber_ctx_t c, climber_kv_t kv, int32_t* idx, int32_t* vlen) {
+  if (!c || !idx || !vlen) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+  int slot;
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    climber_status rs = resolve(c, kv, &slot);
+    if (rs != CLIMBER_OK) return rs;
+  }
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(idx, c->idx_all + (size_t)slot * c->D.Nb * c->D.nk, (size_t)c->D.Nb * c->D.nk * 4,
+                cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(vlen, c->vlen_all + (size_t)slot * c->D.Nb, (size_t)c->D.Nb * 4, cudaMemcpyDeviceToHost));
+  return CLIMBER_OK;
+}
+
+extern "C" climber_status climber_debug_mask(climber_ctx_t c, climber_kv_t kv, int32_t M, uint8_t* mask) {
+  if (!c || !mask || M < 1) return fail(CLIMBER_E_INVALID_ARG, "bad argument");
+  int slot;
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    climber_status rs = resolve(c, kv, &slot);
+    if (rs != CLIMBER_OK) return rs;
+  }
+  size_t T = (size_t)c->D.nk + M, n = (size_t)c->D.Nb * T * T;
+  uint8_t* d = nullptr;
+  CU(cudaMalloc(&d, n));
+  launch_debug_mask(c->vlen_all, slot, M, d, c->D, 0);
+  c->launches++;
+  cudaError_t e = cudaMemcpy(mask, d, n, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(CLIMBER_E_CUDA, "debug_mask: %s", cudaGetErrorString(e));
+  return CLIMBER_OK;
+}
+
+extern "C" climber_status climber_debug_kv(climber_ctx_t c, climber_kv_t kv, int32_t layer, int32_t block, void* K,
+                                           void* V) {
+  if (!c || !K || !V) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+  if (layer < 0 || layer >= c->D.L || block < 0 || block >= c->D.Nb) return fail(CLIMBER_E_INVALID_ARG, "layer/block");
+  int slot;
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    climber_status rs = resolve(c, kv, &slot);
+    if (rs != CLIMBER_OK) return rs;
+  }
+  CU(cudaDeviceSynchronize());
+  int v = 0;
+  CU(cudaMemcpy(&v, c->vlen_all + (size_t)slot * c->D.Nb + block, 4, cudaMemcpyDeviceToHost));
+  size_t bytes = (size_t)v * c->D.d * c->esz;
+  if (bytes == 0) return CLIMBER_OK;
+  void *dk = nullptr, *dv = nullptr;
+  CU(cudaMalloc(&dk, bytes));
+  CU(cudaMalloc(&dv, bytes));
+  if (c->cfg.dtype == CLIMBER_BF16)
+    launch_debug_kv<bf16>((const bf16*)c->pool, c->ptab, c->vlen_all, slot, block, layer, (bf16*)dk, (bf16*)dv, c->D, 0);
+  else
+    launch_debug_kv<float>((const float*)c->pool, c->ptab, c->vlen_all, slot, block, layer, (float*)dk, (float*)dv,
+                           c->D, 0);
+  c->launches++;
+  cudaError_t e1 = cudaMemcpy(K, dk, bytes, cudaMemcpyDeviceToHost);
+  cudaError_t e2 = cudaMemcpy(V, dv, bytes, cudaMemcpyDeviceToHost);
+  cudaFree(dk);
+  cudaFree(dv);
+  if (e1 != cudaSuccess || e2 != cudaSuccess) return fail(CLIMBER_E_CUDA, "debug_kv copy failed");
+  return CLIMBER_OK;
+}
+
+extern "C" climber_status climber_debug_gemm(const void* A, const void* B, float* D, int64_t M, int32_t N, int32_t K,
+                                             int32_t use_tc, climber_stream_t stream) {
+  if (!A || !B || !D || M < 1 || N < 1 || K < 1) return fail(CLIMBER_E_INVALID_ARG, "bad argument");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Epilogue e{};
+  e.kind = EPI_RESID; e.out = D; e.ldo = N;
+  if (use_tc) {
+    if (!gemm_tc_supported(M, N, K, K, K)) return fail(CLIMBER_E_UNSUPPORTED, "shape not supported by tcgen05 GEMM");
+    launch_gemm_tc((const bf16*)A, K, (const bf16*)B, K, M, N, K, e, s);
+  } else {
+    if (K % 16 || N % 4) return fail(CLIMBER_E_UNSUPPORTED, "shape not supported by SIMT GEMM");
+    launch_gemm_simt<bf16>((const bf16*)A, K, (const bf16*)B, K, M, N, K, e, s);
+  }
+  CU(cudaGetLastError());
+  return CLIMBER_OK;
+}
+
+extern "C" int64_t climber_launch_count(climber_ctx_t c) { return c ? c->launches : -1; }
+
+extern "C" const char* climber_last_error(void) { return g_last_error.c_str(); }

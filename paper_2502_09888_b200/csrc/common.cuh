@@ -1,0 +1,159 @@
+// Internal definitions shared by the libclimber kernels and the C-ABI layer.
+// Not part of the public ABI (see include/climber.h).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+
+namespace climber {
+
+typedef __nv_bfloat16 bf16;
+
+// Model dimensions, passed by value to kernels.
+struct Dims {
+  int d, h, dh, L, Nb, nk, F, Dse, Hse, V, A, R, Mmax, causal, ppb;
+  float eps;
+};
+
+// Device error word bits (climber_stream_status maps them to statuses).
+enum : int { ERR_RANGE = 1, ERR_UNSORTED = 2 };
+
+constexpr int PAGE = 64;  // tokens per K/V page
+
+// ---- element conversion helpers -------------------------------------------
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ float to_f(bf16 x) { return __bfloat162float(x); }
+template <typename T> __device__ __forceinline__ T from_f(float x);
+template <> __device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ bf16 from_f<bf16>(float x) { return __float2bfloat16_rn(x); }
+
+// Load / store 8 consecutive elements (16 B for bf16, 32 B for fp32).
+__device__ __forceinline__ void load8(const bf16* p, float* v) {
+  uint4 u = *reinterpret_cast<const uint4*>(p);
+  const bf16* b = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __bfloat162float(b[i]);
+}
+__device__ __forceinline__ void load8(const float* p, float* v) {
+  float4 a = *reinterpret_cast<const float4*>(p);
+  float4 b = *reinterpret_cast<const float4*>(p + 4);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void store8(bf16* p, const float* v) {
+  uint4 u;
+  bf16* b = reinterpret_cast<bf16*>(&u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) b[i] = __float2bfloat16_rn(v[i]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+__device__ __forceinline__ void store8(float* p, const float* v) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
+__device__ __forceinline__ float sigmoid_f(float x) { return 1.0f / (1.0f + __expf(-x)); }
+
+// SUMI visibility rule in canonical coordinates (G1,
+// G12, G14): slots 0..nk-1 are history (left-padded, valid iff >= nk - v),
+// slots nk.. are candidates.  The attention kernels implement exactly these
+// key ranges: history row t sees keys j <= t (causal) or j < v; candidate
+// rows see keys 0..v-1 plus themselves.
+__host__ __device__ __forceinline__ bool sumi_visible(int i, int j, int nk, int v, int causal) {
+  const int first = nk - v;
+  if (i < nk && i < first) return false;
+  if (j < nk && j < first) return false;
+  if (i < nk && j < nk) return causal ? (j <= i) : true;
+  if (i < nk) return false;
+  if (j < nk) return true;
+  return i == j;
+}
+
+// ---- GEMM epilogues ---------------------------------------------------------
+// D[m][n] = sum_k A[m][k] * B[n][k]  (both operands K-contiguous), fp32 accum.
+enum EpiKind : int {
+  EPI_STORE = 0,   // out_T[m*ldo + n] = act(acc + bias[n])
+  EPI_RESID = 1,   // out_f32[m*ldo + n] += acc
+  EPI_QKV_PAGES = 2, // columns (n + col_off) in [0,d): Q -> out_T[m*ldo + n]; [d,3d): K/V -> pages
+  EPI_GATE = 3,    // out_f32[m*ldo + n] *= sigmoid(acc + bias[n])   (Eq. 4 bit-wise gate)
+};
+enum ActKind : int { ACT_NONE = 0, ACT_SILU = 1, ACT_RELU = 2 };
+
+struct Epilogue {
+  int kind;
+  int act;
+  void* out;            // T* (STORE, QKV Q part) or float* (RESID, GATE)
+  long long ldo;        // row stride of out, elements
+  const float* bias;    // [N] or nullptr
+  // EPI_QKV_PAGES: history row m = u * nk + t of wave user u
+  void* pool;           // page pool base (T*)
+  const int* ptab;      // [slots][Nb][L][ppb]
+  const int* wave_slot; // [U] slot of wave user u
+  int col_off;          // 0 (full QKV) or d (last layer: K/V only)
+  int blk, layer;       // (k, l)
+  int d, h, dh, nk, Nb, L, ppb;
+};
+
+// Page addressing: page = [2 (K,V)][h][PAGE][dh] elements.
+__device__ __forceinline__ long long page_elem_offset(int page, int kv, int head, int slot_t, int dim,
+                                                      int h, int dh) {
+  return (((long long)page * 2 + kv) * h + head) * (long long)(PAGE * dh) + (long long)slot_t * dh + dim;
+}
+
+// Apply the epilogue to NC consecutive columns [n0, n0+NC) of row m.
+template <typename T, int NC>
+__device__ __forceinline__ void epilogue_chunk(const Epilogue& e, long long m, int n0, const float* v) {
+  if (e.kind == EPI_STORE) {
+    float x[NC];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      float a = v[i] + (e.bias ? e.bias[n0 + i] : 0.0f);
+      if (e.act == ACT_SILU) a = silu_f(a);
+      else if (e.act == ACT_RELU) a = fmaxf(a, 0.0f);
+      x[i] = a;
+    }
+    T* o = reinterpret_cast<T*>(e.out) + m * e.ldo + n0;
+    if constexpr (NC % 8 == 0) {
+#pragma unroll
+      for (int i = 0; i < NC; i += 8) store8(o + i, x + i);
+    } else {
+#pragma unroll
+      for (int i = 0; i < NC; ++i) o[i] = from_f<T>(x[i]);
+    }
+  } else if (e.kind == EPI_RESID) {
+    float* o = reinterpret_cast<float*>(e.out) + m * e.ldo + n0;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) o[i] += v[i];
+  } else if (e.kind == EPI_GATE) {
+    float* o = reinterpret_cast<float*>(e.out) + m * e.ldo + n0;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) o[i] = o[i] * sigmoid_f(v[i] + e.bias[n0 + i]);
+  } else {  // EPI_QKV_PAGES
+    int c = n0 + e.col_off;
+    if (c < e.d) {
+      T* o = reinterpret_cast<T*>(e.out) + m * e.ldo + c;
+#pragma unroll
+      for (int i = 0; i < NC; ++i) o[i] = from_f<T>(v[i]);
+    } else {
+      int u = (int)(m / e.nk), t = (int)(m % e.nk);
+      int slot = e.wave_slot[u];
+      int page = e.ptab[(((long long)slot * e.Nb + e.blk) * e.L + e.layer) * e.ppb + t / PAGE];
+      int kv = (c >= 2 * e.d) ? 1 : 0;
+      int cc = c - e.d * (1 + kv);
+      int head = cc / e.dh, dim = cc % e.dh;   // NC divides dh: chunk stays in one head
+      T* o = reinterpret_cast<T*>(e.pool) + page_elem_offset(page, kv, head, t % PAGE, dim, e.h, e.dh);
+#pragma unroll
+      for (int i = 0; i < NC; ++i) o[i] = from_f<T>(v[i]);
+    }
+  }
+}
+
+}  // namespace climber

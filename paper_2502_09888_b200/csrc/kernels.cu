@@ -1,0 +1,662 @@
+// Non-GEMM kernels of the SUMI hot path (SURVEY §8(a) rows a1, a2, a4/a5
+// attention, a6 head) and the SIMT GEMM used by the fp32 verification build.
+//
+// Every kernel is templated on the storage type T of activations / K/V pages
+// (bf16 production path, fp32 verification build); statistics,
+// softmax and residuals are fp32 in both.
+#include "kernels.cuh"
+
+namespace climber {
+
+// ===========================================================================
+// a1: validation + multi-scale sequence extraction (Eq. 2)
+// One CTA per user.  All threads validate the events (coalesced sweep), then
+// warp k extracts strategy k by a reverse ballot scan: lanes test 32 events
+// newest-first, the rank of a match among newer matches in the chunk is a
+// popcount, so the most recent n_k matches land in canonical left-padded
+// slots n_k-1, n_k-2, ... (G11, G12).
+// ===========================================================================
+__global__ void k_extract(const int32_t* __restrict__ item, const uint8_t* __restrict__ action,
+                          const uint8_t* __restrict__ scenario, const int64_t* __restrict__ ts,
+                          const int64_t* __restrict__ ev_off, const int* __restrict__ wave_slot,
+                          const unsigned long long* __restrict__ amask,
+                          const unsigned long long* __restrict__ smask, int* __restrict__ idx_all,
+                          int* __restrict__ vlen_all, int* __restrict__ bad_all, int* __restrict__ err,
+                          Dims D) {
+  const int u = blockIdx.x;
+  const long long s = ev_off[u], e = ev_off[u + 1];
+  const int slot = wave_slot[u];
+  int flags = 0;
+  for (long long i = s + threadIdx.x; i < e; i += blockDim.x) {
+    int it = item[i];
+    if (it < 0 || it >= D.V || action[i] >= D.A || scenario[i] >= D.R) flags |= ERR_RANGE;
+    if (i > s && ts[i] < ts[i - 1]) flags |= ERR_UNSORTED;
+  }
+  int any = __syncthreads_or(flags);
+  if (flags) atomicOr(err, flags);
+  if (threadIdx.x == 0) bad_all[slot] = any ? 1 : 0;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = warp; k < D.Nb; k += blockDim.x >> 5) {
+    const unsigned long long am = amask[k], sm = smask[k];
+    int* idx = idx_all + ((long long)slot * D.Nb + k) * D.nk;
+    int cnt = 0;
+    for (long long base = e - 1; base >= s && cnt < D.nk; base -= 32) {
+      long long i = base - lane;
+      bool ok = false;
+      if (i >= s) {
+        unsigned a = action[i], sc = scenario[i];
+        ok = a < 64 && sc < 64 && ((am >> a) & 1ull) && ((sm >> sc) & 1ull);
+      }
+      unsigned bal = __ballot_sync(0xffffffffu, ok);
+      if (ok) {
+        int pos = D.nk - 1 - (cnt + __popc(bal & ((1u << lane) - 1u)));
+        if (pos >= 0) idx[pos] = (int)(i - s);
+      }
+      cnt += __popc(bal);
+    }
+    int v = min(cnt, D.nk);
+    for (int p = lane; p < D.nk - v; p += 32) idx[p] = -1;
+    if (lane == 0) vlen_all[(long long)slot * D.Nb + k] = v;
+  }
+}
+
+// ===========================================================================
+// a2: embedding gather-sum (G10).  Warp per row, 8 elems/lane.
+// History row (u, t) of block k: E_item + E_act + E_scn of the t-th extracted
+// event, zero for pad rows (t >= v).  Right-padded internal layout.
+// ===========================================================================
+template <typename T>
+__global__ void k_embed_hist(const int32_t* __restrict__ item, const uint8_t* __restrict__ action,
+                             const uint8_t* __restrict__ scenario, const int64_t* __restrict__ ev_off,
+                             const int* __restrict__ wave_slot, const int* __restrict__ idx_all,
+                             const int* __restrict__ vlen_all, const int* __restrict__ bad_all,
+                             const T* __restrict__ e_item, const T* __restrict__ e_act,
+                             const T* __restrict__ e_scn, float* __restrict__ X, long long rows, int k,
+                             Dims D) {
+  long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  int u = (int)(row / D.nk), t = (int)(row % D.nk);
+  int slot = wave_slot[u];
+  int v = vlen_all[(long long)slot * D.Nb + k];
+  float* out = X + row * D.d;
+  if (t >= v) {
+    float z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int c = lane * 8; c < D.d; c += 256) store8(out + c, z);
+    return;
+  }
+  long long ev = ev_off[u] + idx_all[((long long)slot * D.Nb + k) * D.nk + (D.nk - v + t)];
+  int it = item[ev], a = action[ev], sc = scenario[ev];
+  bool bad = bad_all[slot] != 0;
+  if (it < 0 || it >= D.V) it = 0;
+  if (a >= D.A) a = 0;
+  if (sc >= D.R) sc = 0;
+  for (int c = lane * 8; c < D.d; c += 256) {
+    float x[8], y[8], z[8];
+    load8(e_item + (long long)it * D.d + c, x);
+    load8(e_act + (long long)a * D.d + c, y);
+    load8(e_scn + (long long)sc * D.d + c, z);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = bad ? __int_as_float(0x7fc00000) : x[i] + y[i] + z[i];
+    store8(out + c, x);
+  }
+}
+
+// Binary search: wave user owning pair p, given cand_off[0..U] (wave-relative).
+__device__ __forceinline__ int pair_user(const int64_t* cand_off, int U, long long p) {
+  int lo = 0, hi = U - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (cand_off[mid] <= p) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Candidate rows: c0 = E_item[item] + E_scn[r] (G10), replicated into the
+// N_b block slots of the residual buffer C[p][k][d] (all blocks start from c0).
+template <typename T>
+__global__ void k_embed_cand(const int32_t* __restrict__ items, const int64_t* __restrict__ cand_off,
+                             const int* __restrict__ wave_r, int U, long long P,
+                             const T* __restrict__ e_item, const T* __restrict__ e_scn,
+                             float* __restrict__ C, int* __restrict__ err, Dims D) {
+  long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (p >= P) return;
+  int u = pair_user(cand_off, U, p);
+  int r = wave_r[u];
+  int it = items[p];
+  bool bad = it < 0 || it >= D.V;
+  if (bad) {
+    it = 0;
+    if (lane == 0) atomicOr(err, ERR_RANGE);
+  }
+  for (int c = lane * 8; c < D.d; c += 256) {
+    float x[8], z[8];
+    load8(e_item + (long long)it * D.d + c, x);
+    load8(e_scn + (long long)r * D.d + c, z);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = bad ? __int_as_float(0x7fc00000) : x[i] + z[i];
+    for (int k = 0; k < D.Nb; ++k) store8(C + (p * D.Nb + k) * D.d + c, x);
+  }
+}
+
+// ===========================================================================
+// RMSNorm (G7): out[row] = X[row] / sqrt(mean(X^2) + eps) * g.  Warp per row.
+// ===========================================================================
+template <typename T>
+__global__ void k_rmsnorm(const float* __restrict__ X, long long ldx, const float* __restrict__ g,
+                          T* __restrict__ out, long long ldo, long long rows, int d, float eps) {
+  long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float* x = X + row * ldx;
+  float buf[4][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    int c = (lane + 32 * j) * 8;
+    if (c < d) {
+      load8(x + c, buf[j]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ss += buf[j][i] * buf[j][i];
+    }
+  }
+  ss = warp_sum(ss);
+  float rs = rsqrtf(ss / (float)d + eps);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    int c = (lane + 32 * j) * 8;
+    if (c < d) {
+      float gg[8], y[8];
+      load8(g + c, gg);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) y[i] = buf[j][i] * rs * gg[i];
+      store8(out + row * ldo + c, y);
+    }
+  }
+}
+
+// fp32 -> T copy (vec(G) for the squeeze-and-excitation GEMM).
+template <typename T>
+__global__ void k_convert(const float* __restrict__ X, T* __restrict__ out, long long n8) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n8) return;
+  float v[8];
+  load8(X + i * 8, v);
+  store8(out + i * 8, v);
+}
+
+// a6 head (G18): score[p] = w_head . Y[p] + b_head.  Warp per row, fixed order.
+__global__ void k_head(const float* __restrict__ Y, const float* __restrict__ w, float b,
+                       float* __restrict__ scores, long long P, int D) {
+  long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (p >= P) return;
+  float acc = 0.f;
+  for (int c = lane * 8; c < D; c += 256) {
+    float y[8], ww[8];
+    load8(Y + p * D + c, y);
+    load8(w + c, ww);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc = fmaf(y[i], ww[i], acc);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) scores[p] = acc + b;
+}
+
+// ===========================================================================
+// Attention (Eq. 3 with f_b = 0, G2/G3): softmax(q.k / (sqrt(d_h) tau)).
+// SIMT flash form: one thread owns one query row (q, o in registers), K/V
+// chunks of KC keys are staged in shared memory (broadcast reads), online
+// softmax in base 2 with fp32 statistics.
+// ===========================================================================
+constexpr int KC = 32;
+constexpr float LOG2E = 1.4426950408889634f;
+
+template <typename T, int DH>
+__device__ __forceinline__ void load_kv_chunk(float (*Ks)[DH + 1], float (*Vs)[DH + 1], const T* pool,
+                                              const int* pages, int t0, int nkeys, int head, int h) {
+  // nkeys <= KC tokens starting at t0; a chunk never crosses a page (PAGE % KC == 0)
+  const int page = pages[t0 / PAGE];
+  const T* kb = pool + page_elem_offset(page, 0, head, t0 % PAGE, 0, h, DH);
+  const T* vb = pool + page_elem_offset(page, 1, head, t0 % PAGE, 0, h, DH);
+  for (int i = threadIdx.x; i < KC * DH; i += blockDim.x) {
+    int j = i / DH, c = i % DH;
+    float kv = 0.f, vv = 0.f;
+    if (j < nkeys) {
+      kv = to_f(kb[i]);
+      vv = to_f(vb[i]);
+    }
+    Ks[j][c] = kv;
+    Vs[j][c] = vv;
+  }
+}
+
+template <int DH>
+__device__ __forceinline__ void online_chunk(const float (*Ks)[DH + 1], const float (*Vs)[DH + 1],
+                                             const float* q, float* o, float& m, float& l, int jmax) {
+  // keys j < jmax of the staged chunk are visible to this thread
+  if (jmax <= 0) return;
+  float s[KC];
+  float cmax = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < KC; ++j) {
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < DH; ++c) acc = fmaf(q[c], Ks[j][c], acc);
+    s[j] = (j < jmax) ? acc : -INFINITY;
+    cmax = fmaxf(cmax, s[j]);
+  }
+  float mn = fmaxf(m, cmax);
+  float alpha = exp2f(m - mn);  // m = -inf -> 0
+  l *= alpha;
+#pragma unroll
+  for (int c = 0; c < DH; ++c) o[c] *= alpha;
+#pragma unroll
+  for (int j = 0; j < KC; ++j) {
+    float p = exp2f(s[j] - mn);
+    l += p;
+#pragma unroll
+    for (int c = 0; c < DH; ++c) o[c] = fmaf(p, Vs[j][c], o[c]);
+  }
+  m = mn;
+}
+
+// SUMI candidate attention: candidate (u, m) of block k,
+// layer l attends to the v cached history keys of its user/block/layer and to
+// itself (k_self, v_self) only.  grid (U, h, ceil(Mmax/128)), block 128.
+template <typename T, int DH>
+__global__ void __launch_bounds__(128) k_attn_sumi(const T* __restrict__ QKV, const int64_t* __restrict__ cand_off,
+                                                   const int* __restrict__ wave_slot, const int* __restrict__ wave_r,
+                                                   const T* __restrict__ pool, const int* __restrict__ ptab,
+                                                   const int* __restrict__ vlen_all, const float* __restrict__ tau,
+                                                   T* __restrict__ O, int k, int l, Dims D) {
+  __shared__ float Ks[KC][DH + 1];
+  __shared__ float Vs[KC][DH + 1];
+  const int u = blockIdx.x, head = blockIdx.y;
+  const long long p0 = cand_off[u], p1 = cand_off[u + 1];
+  const long long p = p0 + (long long)blockIdx.z * blockDim.x + threadIdx.x;
+  if (p0 + (long long)blockIdx.z * blockDim.x >= p1) return;  // whole CTA idle (uniform)
+  const bool active = p < p1;
+  const int slot = wave_slot[u];
+  const int r = wave_r[u];
+  const int v = vlen_all[(long long)slot * D.Nb + k];
+  const int* pages = ptab + (((long long)slot * D.Nb + k) * D.L + l) * D.ppb;
+  const float sc = LOG2E / (sqrtf((float)DH) * tau[((l * D.Nb + k) * D.R + r) * D.h + head]);
+
+  float q[DH], o[DH];
+  float m = -INFINITY, lsum = 0.f;
+  if (active) {
+    const T* row = QKV + p * (3LL * D.d);
+    float ks[DH];
+#pragma unroll
+    for (int c = 0; c < DH; c += 8) {
+      load8(row + head * DH + c, q + c);
+      load8(row + D.d + head * DH + c, ks + c);
+      load8(row + 2 * D.d + head * DH + c, o + c);
+    }
+    float ss = 0.f;
+#pragma unroll
+    for (int c = 0; c < DH; ++c) {
+      q[c] *= sc;
+      ss = fmaf(q[c], ks[c], ss);
+    }
+    m = ss;      // self term first: weight exp2(0) = 1 on v_self
+    lsum = 1.f;
+  } else {
+#pragma unroll
+    for (int c = 0; c < DH; ++c) q[c] = o[c] = 0.f;
+  }
+  for (int t0 = 0; t0 < v; t0 += KC) {
+    int nkeys = min(KC, v - t0);
+    __syncthreads();
+    load_kv_chunk<T, DH>(Ks, Vs, pool, pages, t0, nkeys, head, D.h);
+    __syncthreads();
+    if (active) online_chunk<DH>(Ks, Vs, q, o, m, lsum, nkeys);
+  }
+  if (active) {
+    float inv = 1.f / lsum;
+    T* out = O + p * D.d + head * DH;
+#pragma unroll
+    for (int c = 0; c < DH; c += 8) {
+      float y[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) y[i] = o[c + i] * inv;
+      store8(out + c, y);
+    }
+  }
+}
+
+// History self-attention inside block k (Eq. 3 over S_k; causal G1 or
+// bidirectional).  Query row t of user u attends keys j <= t (causal) or
+// j < v.  Pad rows (t >= v) output zeros.  grid (U, h, nk/128), block 128.
+template <typename T, int DH>
+__global__ void __launch_bounds__(128) k_attn_hist(const T* __restrict__ Q, const int* __restrict__ wave_slot,
+                                                   const int* __restrict__ wave_r, const T* __restrict__ pool,
+                                                   const int* __restrict__ ptab, const int* __restrict__ vlen_all,
+                                                   const float* __restrict__ tau, T* __restrict__ O, int k, int l,
+                                                   Dims D) {
+  __shared__ float Ks[KC][DH + 1];
+  __shared__ float Vs[KC][DH + 1];
+  const int u = blockIdx.x, head = blockIdx.y;
+  const int t = blockIdx.z * blockDim.x + threadIdx.x;
+  const int slot = wave_slot[u];
+  const int r = wave_r[u];
+  const int v = vlen_all[(long long)slot * D.Nb + k];
+  const long long row = (long long)u * D.nk + t;
+  const bool active = t < v;
+  const int* pages = ptab + (((long long)slot * D.Nb + k) * D.L + l) * D.ppb;
+  const float sc = LOG2E / (sqrtf((float)DH) * tau[((l * D.Nb + k) * D.R + r) * D.h + head]);
+  float q[DH], o[DH];
+  float m = -INFINITY, lsum = 0.f;
+#pragma unroll
+  for (int c = 0; c < DH; ++c) o[c] = 0.f;
+  if (active) {
+#pragma unroll
+    for (int c = 0; c < DH; c += 8) load8(Q + row * D.d + head * DH + c, q + c);
+#pragma unroll
+    for (int c = 0; c < DH; ++c) q[c] *= sc;
+  } else {
+#pragma unroll
+    for (int c = 0; c < DH; ++c) q[c] = 0.f;
+  }
+  const int tile_last = min(v, (int)(blockIdx.z + 1) * (int)blockDim.x) - 1;
+  const int kend = D.causal ? tile_last + 1 : v;
+  for (int t0 = 0; t0 < kend; t0 += KC) {
+    int nkeys = min(KC, v - t0);
+    __syncthreads();
+    load_kv_chunk<T, DH>(Ks, Vs, pool, pages, t0, nkeys, head, D.h);
+    __syncthreads();
+    if (active) {
+      int jmax = D.causal ? min(nkeys, t - t0 + 1) : nkeys;
+      online_chunk<DH>(Ks, Vs, q, o, m, lsum, jmax);
+    }
+  }
+  T* out = O + row * D.d + head * DH;
+  if (t < D.nk) {
+    float inv = active ? 1.f / lsum : 0.f;
+#pragma unroll
+    for (int c = 0; c < DH; c += 8) {
+      float y[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) y[i] = o[c + i] * inv;
+      store8(out + c, y);
+    }
+  }
+}
+
+// a5 fusion ATL attention (G16): the N_b tokens of one pair
+// attend to each other (full visibility), temperature tau_f[r][head].
+// Thread per (pair, token, head).
+template <typename T, int DH>
+__global__ void k_attn_fusion(const T* __restrict__ QKV, const int64_t* __restrict__ cand_off,
+                              const int* __restrict__ wave_r, int U, long long P,
+                              const float* __restrict__ tau_f, T* __restrict__ O, Dims D) {
+  long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long total = P * D.Nb * D.h;
+  if (g >= total) return;
+  int head = (int)(g % D.h);
+  long long tok = g / D.h;          // = p * Nb + i
+  long long p = tok / D.Nb;
+  int u = pair_user(cand_off, U, p);
+  int r = wave_r[u];
+  const float sc = LOG2E / (sqrtf((float)DH) * tau_f[r * D.h + head]);
+  const long long ld = 3LL * D.d;
+  float q[DH], o[DH];
+#pragma unroll
+  for (int c = 0; c < DH; c += 8) load8(QKV + tok * ld + head * DH + c, q + c);
+  float s[8];
+  float mx = -INFINITY;
+  for (int j = 0; j < D.Nb; ++j) {
+    float kk[DH];
+    const T* kr = QKV + (p * D.Nb + j) * ld + D.d + head * DH;
+#pragma unroll
+    for (int c = 0; c < DH; c += 8) load8(kr + c, kk + c);
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < DH; ++c) acc = fmaf(q[c], kk[c], acc);
+    s[j] = acc * sc;
+    mx = fmaxf(mx, s[j]);
+  }
+#pragma unroll
+  for (int c = 0; c < DH; ++c) o[c] = 0.f;
+  float lsum = 0.f;
+  for (int j = 0; j < D.Nb; ++j) {
+    float pj = exp2f(s[j] - mx);
+    lsum += pj;
+    float vv[DH];
+    const T* vr = QKV + (p * D.Nb + j) * ld + 2 * D.d + head * DH;
+#pragma unroll
+    for (int c = 0; c < DH; c += 8) load8(vr + c, vv + c);
+#pragma unroll
+    for (int c = 0; c < DH; ++c) o[c] = fmaf(pj, vv[c], o[c]);
+  }
+  float inv = 1.f / lsum;
+  T* out = O + tok * D.d + head * DH;
+#pragma unroll
+  for (int c = 0; c < DH; c += 8) {
+    float y[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) y[i] = o[c + i] * inv;
+    store8(out + c, y);
+  }
+}
+
+// ===========================================================================
+// Debug exports
+// ===========================================================================
+// Canonical SUMI mask of one handle: evaluated with
+// sumi_visible(), the same key-range rule the attention kernels implement.
+__global__ void k_debug_mask(const int* __restrict__ vlen_all, int slot, int M, uint8_t* __restrict__ mask,
+                             Dims D) {
+  const int T = D.nk + M;
+  long long n = (long long)D.Nb * T * T;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (long long)gridDim.x * blockDim.x) {
+    int k = (int)(g / ((long long)T * T));
+    long long ij = g % ((long long)T * T);
+    int i = (int)(ij / T), j = (int)(ij % T);
+    int v = vlen_all[(long long)slot * D.Nb + k];
+    mask[g] = sumi_visible(i, j, D.nk, v, D.causal) ? 1 : 0;
+  }
+}
+
+template <typename T>
+__global__ void k_debug_kv(const T* __restrict__ pool, const int* __restrict__ ptab,
+                           const int* __restrict__ vlen_all, int slot, int k, int l, T* __restrict__ Kout,
+                           T* __restrict__ Vout, Dims D) {
+  int v = vlen_all[(long long)slot * D.Nb + k];
+  const int* pages = ptab + (((long long)slot * D.Nb + k) * D.L + l) * D.ppb;
+  long long n = (long long)v * D.d;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (long long)gridDim.x * blockDim.x) {
+    int t = (int)(g / D.d), c = (int)(g % D.d);
+    int head = c / D.dh, dim = c % D.dh;
+    int page = pages[t / PAGE];
+    Kout[g] = pool[page_elem_offset(page, 0, head, t % PAGE, dim, D.h, D.dh)];
+    Vout[g] = pool[page_elem_offset(page, 1, head, t % PAGE, dim, D.h, D.dh)];
+  }
+}
+
+// Scatter the staged page-table rows of a call into the per-slot table.
+__global__ void k_scatter_ptab(const int* __restrict__ staged, const int* __restrict__ slots, int B, int per,
+                               int* __restrict__ ptab) {
+  long long n = (long long)B * per;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (long long)gridDim.x * blockDim.x) {
+    int b = (int)(g / per), i = (int)(g % per);
+    ptab[(long long)slots[b] * per + i] = staged[g];
+  }
+}
+
+// ===========================================================================
+// SIMT GEMM (fp32 verification build; also a debug path for bf16):
+// D[m][n] = sum_k A[m][k] B[n][k], 64x64 tile, BK = 16, 256 threads, 4x4 each.
+// ===========================================================================
+template <typename T>
+__global__ void __launch_bounds__(256) k_gemm_simt(const T* __restrict__ A, long long lda, const T* __restrict__ B,
+                                                   long long ldb, long long M, int N, int K, Epilogue e) {
+  __shared__ float As[16][68];
+  __shared__ float Bs[16][68];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const long long m0 = (long long)blockIdx.y * 64;
+  const int n0 = blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+      int r = i / 16, c = i % 16;
+      long long gm = m0 + r;
+      int gn = n0 + r;
+      As[c][r] = (gm < M) ? to_f(A[gm * lda + k0 + c]) : 0.f;
+      Bs[c][r] = (gn < N) ? to_f(B[(long long)gn * ldb + k0 + c]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = As[kk][ty * 4 + i];
+        b[i] = Bs[kk][tx * 4 + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  const int n = n0 + tx * 4;
+  if (n >= N) return;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    long long m = m0 + ty * 4 + i;
+    if (m < M) epilogue_chunk<T, 4>(e, m, n, acc[i]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static inline unsigned blocks_for(long long threads, int bs) { return (unsigned)((threads + bs - 1) / bs); }
+
+void launch_extract(const EventsDev& ev, const int64_t* ev_off, const int* wave_slot, int U,
+                    const unsigned long long* amask, const unsigned long long* smask, int* idx_all,
+                    int* vlen_all, int* bad_all, int* err, const Dims& D, cudaStream_t s) {
+  k_extract<<<U, 256, 0, s>>>(ev.item, ev.action, ev.scenario, ev.ts, ev_off, wave_slot, amask, smask, idx_all,
+                              vlen_all, bad_all, err, D);
+}
+
+template <typename T>
+void launch_embed_hist(const EventsDev& ev, const int64_t* ev_off, const int* wave_slot, int U, const int* idx_all,
+                       const int* vlen_all, const int* bad_all, const T* e_item, const T* e_act, const T* e_scn,
+                       float* X, int k, const Dims& D, cudaStream_t s) {
+  long long rows = (long long)U * D.nk;
+  k_embed_hist<T><<<blocks_for(rows * 32, 256), 256, 0, s>>>(ev.item, ev.action, ev.scenario, ev_off, wave_slot,
+                                                           idx_all, vlen_all, bad_all, e_item, e_act, e_scn, X,
+                                                           rows, k, D);
+}
+
+template <typename T>
+void launch_embed_cand(const int32_t* items, const int64_t* cand_off, const int* wave_r, int U, long long P,
+                       const T* e_item, const T* e_scn, float* C, int* err, const Dims& D, cudaStream_t s) {
+  k_embed_cand<T><<<blocks_for(P * 32, 256), 256, 0, s>>>(items, cand_off, wave_r, U, P, e_item, e_scn, C, err, D);
+}
+
+template <typename T>
+void launch_rmsnorm(const float* X, long long ldx, const float* g, T* out, long long ldo, long long rows, int d,
+                    float eps, cudaStream_t s) {
+  k_rmsnorm<T><<<blocks_for(rows * 32, 256), 256, 0, s>>>(X, ldx, g, out, ldo, rows, d, eps);
+}
+
+template <typename T>
+void launch_convert(const float* X, T* out, long long n, cudaStream_t s) {
+  k_convert<T><<<blocks_for(n / 8, 256), 256, 0, s>>>(X, out, n / 8);
+}
+
+void launch_head(const float* Y, const float* w, float b, float* scores, long long P, int Dse, cudaStream_t s) {
+  k_head<<<blocks_for(P * 32, 256), 256, 0, s>>>(Y, w, b, scores, P, Dse);
+}
+
+template <typename T>
+void launch_attn_sumi(const T* QKV, const int64_t* cand_off, const int* wave_slot, const int* wave_r, int U,
+                      int Mmax, const T* pool, const int* ptab, const int* vlen_all, const float* tau, T* O, int k,
+                      int l, const Dims& D, cudaStream_t s) {
+  dim3 grid(U, D.h, (Mmax + 127) / 128);
+#define CL_SUMI(DH) k_attn_sumi<T, DH><<<grid, 128, 0, s>>>(QKV, cand_off, wave_slot, wave_r, pool, ptab, vlen_all, tau, O, k, l, D)
+  if (D.dh == 16) CL_SUMI(16);
+  else if (D.dh == 32) CL_SUMI(32);
+  else CL_SUMI(64);
+#undef CL_SUMI
+}
+
+template <typename T>
+void launch_attn_hist(const T* Q, const int* wave_slot, const int* wave_r, int U, const T* pool, const int* ptab,
+                      const int* vlen_all, const float* tau, T* O, int k, int l, const Dims& D, cudaStream_t s) {
+  dim3 grid(U, D.h, (D.nk + 127) / 128);
+#define CL_HIST(DH) k_attn_hist<T, DH><<<grid, 128, 0, s>>>(Q, wave_slot, wave_r, pool, ptab, vlen_all, tau, O, k, l, D)
+  if (D.dh == 16) CL_HIST(16);
+  else if (D.dh == 32) CL_HIST(32);
+  else CL_HIST(64);
+#undef CL_HIST
+}
+
+template <typename T>
+void launch_attn_fusion(const T* QKV, const int64_t* cand_off, const int* wave_r, int U, long long P,
+                        const float* tau_f, T* O, const Dims& D, cudaStream_t s) {
+  long long n = P * D.Nb * D.h;
+  unsigned g = blocks_for(n, 128);
+#define CL_FUS(DH) k_attn_fusion<T, DH><<<g, 128, 0, s>>>(QKV, cand_off, wave_r, U, P, tau_f, O, D)
+  if (D.dh == 16) CL_FUS(16);
+  else if (D.dh == 32) CL_FUS(32);
+  else CL_FUS(64);
+#undef CL_FUS
+}
+
+void launch_debug_mask(const int* vlen_all, int slot, int M, uint8_t* mask, const Dims& D, cudaStream_t s) {
+  k_debug_mask<<<296, 256, 0, s>>>(vlen_all, slot, M, mask, D);
+}
+
+template <typename T>
+void launch_debug_kv(const T* pool, const int* ptab, const int* vlen_all, int slot, int k, int l, T* K, T* V,
+                     const Dims& D, cudaStream_t s) {
+  k_debug_kv<T><<<296, 256, 0, s>>>(pool, ptab, vlen_all, slot, k, l, K, V, D);
+}
+
+void launch_scatter_ptab(const int* staged, const int* slots, int B, int per, int* ptab, cudaStream_t s) {
+  k_scatter_ptab<<<296, 256, 0, s>>>(staged, slots, B, per, ptab);
+}
+
+template <typename T>
+void launch_gemm_simt(const T* A, long long lda, const T* B, long long ldb, long long M, int N, int K,
+                      const Epilogue& e, cudaStream_t s) {
+  dim3 grid((N + 63) / 64, (unsigned)((M + 63) / 64));
+  k_gemm_simt<T><<<grid, 256, 0, s>>>(A, lda, B, ldb, M, N, K, e);
+}
+
+#define INST(T)                                                                                                  \
+  template void launch_embed_hist<T>(const EventsDev&, const int64_t*, const int*, int, const int*, const int*,  \
+                                     const int*, const T*, const T*, const T*, float*, int, const Dims&,         \
+                                     cudaStream_t);                                                              \
+  template void launch_embed_cand<T>(const int32_t*, const int64_t*, const int*, int, long long, const T*,       \
+                                     const T*, float*, int*, const Dims&, cudaStream_t);                         \
+  template void launch_rmsnorm<T>(const float*, long long, const float*, T*, long long, long long, int, float,   \
+                                  cudaStream_t);                                                                 \
+  template void launch_convert<T>(const float*, T*, long long, cudaStream_t);                                    \
+  template void launch_attn_sumi<T>(const T*, const int64_t*, const int*, const int*, int, int, const T*,        \
+                                    const int*, const int*, const float*, T*, int, int, const Dims&,             \
+                                    cudaStream_t);                                                               \
+  template void launch_attn_hist<T>(const T*, const int*, const int*, int, const T*, const int*, const int*,     \
+                                    const float*, T*, int, int, const Dims&, cudaStream_t);                      \
+  template void launch_attn_fusion<T>(const T*, const int64_t*, const int*, int, long long, const float*, T*,    \
+                                      const Dims&, cudaStream_t);                                                \
+  template void launch_debug_kv<T>(const T*, const int*, const int*, int, int, int, T*, T*, const Dims&,         \
+                                   cudaStream_t);                                                                \
+  template void launch_gemm_simt<T>(const T*, long long, const T*, long long, long long, int, int,               \
+                                    const Epilogue&, cudaStream_t);
+INST(float)
+INST(bf16)
+#undef INST
+
+}  // namespace climber

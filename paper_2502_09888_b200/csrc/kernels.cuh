@@ -1,0 +1,55 @@
+// Launchers for the libclimber kernels (internal).
+#pragma once
+#include "common.cuh"
+
+namespace climber {
+
+struct EventsDev {
+  const int32_t* item;
+  const uint8_t* action;
+  const uint8_t* scenario;
+  const int64_t* ts;
+};
+
+void launch_extract(const EventsDev& ev, const int64_t* ev_off, const int* wave_slot, int U,
+                    const unsigned long long* amask, const unsigned long long* smask, int* idx_all,
+                    int* vlen_all, int* bad_all, int* err, const Dims& D, cudaStream_t s);
+template <typename T>
+void launch_embed_hist(const EventsDev& ev, const int64_t* ev_off, const int* wave_slot, int U, const int* idx_all,
+                       const int* vlen_all, const int* bad_all, const T* e_item, const T* e_act, const T* e_scn,
+                       float* X, int k, const Dims& D, cudaStream_t s);
+template <typename T>
+void launch_embed_cand(const int32_t* items, const int64_t* cand_off, const int* wave_r, int U, long long P,
+                       const T* e_item, const T* e_scn, float* C, int* err, const Dims& D, cudaStream_t s);
+template <typename T>
+void launch_rmsnorm(const float* X, long long ldx, const float* g, T* out, long long ldo, long long rows, int d,
+                    float eps, cudaStream_t s);
+template <typename T>
+void launch_convert(const float* X, T* out, long long n, cudaStream_t s);
+void launch_head(const float* Y, const float* w, float b, float* scores, long long P, int Dse, cudaStream_t s);
+template <typename T>
+void launch_attn_sumi(const T* QKV, const int64_t* cand_off, const int* wave_slot, const int* wave_r, int U,
+                      int Mmax, const T* pool, const int* ptab, const int* vlen_all, const float* tau, T* O, int k,
+                      int l, const Dims& D, cudaStream_t s);
+template <typename T>
+void launch_attn_hist(const T* Q, const int* wave_slot, const int* wave_r, int U, const T* pool, const int* ptab,
+                      const int* vlen_all, const float* tau, T* O, int k, int l, const Dims& D, cudaStream_t s);
+template <typename T>
+void launch_attn_fusion(const T* QKV, const int64_t* cand_off, const int* wave_r, int U, long long P,
+                        const float* tau_f, T* O, const Dims& D, cudaStream_t s);
+void launch_debug_mask(const int* vlen_all, int slot, int M, uint8_t* mask, const Dims& D, cudaStream_t s);
+template <typename T>
+void launch_debug_kv(const T* pool, const int* ptab, const int* vlen_all, int slot, int k, int l, T* K, T* V,
+                     const Dims& D, cudaStream_t s);
+void launch_scatter_ptab(const int* staged, const int* slots, int B, int per, int* ptab, cudaStream_t s);
+template <typename T>
+void launch_gemm_simt(const T* A, long long lda, const T* B, long long ldb, long long M, int N, int K,
+                      const Epilogue& e, cudaStream_t s);
+
+// tcgen05 GEMM (bf16 in, fp32 accumulate in TMEM), gemm_tc.cu.  Returns false
+// if the shape is not supported by the tensor-core kernel.
+bool gemm_tc_supported(long long M, int N, int K, long long lda, long long ldb);
+void launch_gemm_tc(const bf16* A, long long lda, const bf16* B, long long ldb, long long M, int N, int K,
+                    const Epilogue& e, cudaStream_t s);
+
+}  // namespace climber

@@ -119,10 +119,13 @@ def strategies_for(N_b: int, R: int) -> List[tuple]:
 # ---------------------------------------------------------------------------
 def round_bf16(x: np.ndarray) -> np.ndarray:
     """Round fp32 values to the nearest bf16 (ties to even); returns fp32."""
-    x = np.ascontiguousarray(x, dtype=np.float32)
-    u = x.view(np.uint32).astype(np.uint64)
-    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
-    return u.astype(np.uint32).view(np.float32)
+    x = np.array(x, dtype=np.float32, copy=True, order="C")
+    u = x.view(np.uint32)          # finite values: u + 0x8000 cannot overflow 32 bits
+    lsb = (u >> 16) & 1
+    lsb += 0x7FFF
+    u += lsb
+    u &= 0xFFFF0000
+    return x
 
 
 def _normal(rng, shape, std) -> np.ndarray:

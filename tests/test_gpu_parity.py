@@ -1,0 +1,196 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle on the same
+seeded synthetic inputs (north star tolerances; masks/indices bit-exact)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from helpers import gpu_scores, make_gpu, oracle_scores, parity_err, to_dev, tolerance
+
+pytestmark = pytest.mark.gpu
+
+
+def _check_cfg(cfg, B, users, seed_w=0, seed_b=1, **kw):
+    w = synth.make_weights(cfg, seed_w)
+    batch = synth.make_batch(cfg, seed_b, B=B)
+    cl = make_gpu(cfg, w, B, **kw)
+    got = gpu_scores(cl, batch)
+    cl.stream_status()
+    ref = oracle_scores(cfg, w, batch, users)
+    tol = tolerance(cfg)
+    worst = (0.0, 0.0)
+    for b, r in ref.items():
+        s0, s1 = int(batch.cand_offsets[b]), int(batch.cand_offsets[b + 1])
+        ab, rel = parity_err(got[s0:s1], r)
+        worst = (max(worst[0], ab), max(worst[1], rel))
+    assert np.all(np.isfinite(got))
+    assert worst[0] <= tol and worst[1] <= tol, (cfg.name, worst)
+    return worst
+
+
+def test_tiny_fp32():
+    _check_cfg(synth.preset("tiny"), B=1, users=[0])
+
+
+@pytest.mark.parametrize("causal", [1, 0])
+def test_tiny_l2_fp32(causal):
+    cfg = synth.preset("tiny", L=2, B=3, hist_causal=causal)
+    _check_cfg(cfg, B=3, users=[0, 1, 2])
+
+
+def test_tiny_bf16():
+    cfg = synth.preset("tiny", L=2, dtype="bf16")
+    _check_cfg(cfg, B=2, users=[0, 1])
+
+
+def test_small_fp32_verification_build():
+    cfg = synth.preset("small", dtype="fp32")
+    _check_cfg(cfg, B=4, users=[0, 1, 2, 3])
+
+
+def test_small_bf16():
+    _check_cfg(synth.preset("small"), B=32, users=[0, 7, 31])
+
+
+def test_medium_bf16_ragged():
+    _check_cfg(synth.preset("medium"), B=8, users=[0, 3, 7])
+
+
+def test_large_bf16():
+    cfg = synth.preset("large")
+    _check_cfg(cfg, B=2, users=[0, 1], max_wave_pairs=2000)
+
+
+def test_sweep_corner_bf16():
+    cfg = synth.preset("sweep", L=2, n_k=64, M=100, n_s=1536)
+    _check_cfg(cfg, B=2, users=[0, 1])
+
+
+# ---------------------------------------------------------------------------
+# integer parity: extraction indices and canonical masks bit-exact
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["tiny", "small", "medium"])
+def test_extract_and_mask_bit_exact(name):
+    cfg = synth.preset(name)
+    if name == "tiny":
+        cfg = cfg.replace(hist_causal=0)
+    w = synth.make_weights(cfg, 0)
+    B = 3
+    batch = synth.make_batch(cfg, 2, B=B)
+    cl = make_gpu(cfg, w, B)
+    item, action, scenario, ts, cand = to_dev(batch)
+    hs = cl.encode_users(batch.ev_offsets, item, action, scenario, ts, batch.r)
+    strats = synth.strategies_for(cfg.N_b, cfg.R)
+    for b in range(B):
+        _, a, sc, _ = batch.user_events(b)
+        idx, vlen = cl.debug_extract(hs[b])
+        ridx, rvlen = O.extract(a, sc, strats, cfg.n_k)
+        assert np.array_equal(idx, ridx) and np.array_equal(vlen, rvlen)
+        M = 5
+        mask = cl.debug_mask(hs[b], M)
+        for k in range(cfg.N_b):
+            assert np.array_equal(mask[k], O.canonical_mask(int(rvlen[k]), cfg.n_k, M, cfg.hist_causal))
+    cl.release(hs)
+
+
+def test_kv_cache_matches_oracle():
+    cfg = synth.preset("tiny", L=2)
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 1, B=1)
+    cl = make_gpu(cfg, w, 1)
+    item, action, scenario, ts, cand = to_dev(batch)
+    hs = cl.encode_users(batch.ev_offsets, item, action, scenario, ts, batch.r)
+    it, a, sc, _ = batch.user_events(0)
+    cache = O.encode_user(cfg, w, synth.strategies_for(cfg.N_b, cfg.R), it, a, sc, int(batch.r[0]))
+    for k in range(cfg.N_b):
+        for l in range(cfg.L):
+            v = int(cache.vlen[k])
+            K, V = cl.debug_kv(hs[0], l, k, v)
+            np.testing.assert_allclose(K, cache.K[k][l], atol=1e-4, rtol=1e-4)
+            np.testing.assert_allclose(V, cache.V[k][l], atol=1e-4, rtol=1e-4)
+    cl.release(hs)
+
+
+# ---------------------------------------------------------------------------
+# invariants on the GPU: permutation (bitwise), determinism, reuse, isolation
+# ---------------------------------------------------------------------------
+def test_permutation_determinism_and_cache_reuse_bitwise():
+    import torch
+    cfg = synth.preset("small")
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 3, B=4)
+    cl = make_gpu(cfg, w, 4, kv_users=8)
+    s1, hs, (item, action, scenario, ts, cand) = gpu_scores(cl, batch, release=False)
+    s2 = cl.score_batched(hs, batch.cand_offsets, cand).cpu().numpy()
+    assert np.array_equal(s1, s2)                     # reuse + run-to-run determinism
+    M = cfg.M
+    rng = np.random.default_rng(0)
+    perm = np.concatenate([b * M + rng.permutation(M) for b in range(4)])
+    s3 = cl.score_batched(hs, batch.cand_offsets, cand[torch.from_numpy(perm).cuda()]).cpu().numpy()
+    assert np.array_equal(s3, s1[perm])               # permuting candidates permutes scores bitwise
+    # a bystander's score does not depend on the other candidates (isolation)
+    sub = cand.view(4, M)[:, :7].contiguous().view(-1)
+    off = np.arange(5, dtype=np.int64) * 7
+    s4 = cl.score_batched(hs, off, sub).cpu().numpy().reshape(4, 7)
+    assert np.array_equal(s4, s1.reshape(4, M)[:, :7])
+    # re-encoding the same user gives bit-identical scores
+    s5 = gpu_scores(cl, batch)
+    assert np.array_equal(s5, s1)
+    cl.release(hs)
+
+
+def test_empty_history_and_single_candidate():
+    cfg = synth.preset("tiny", L=2)
+    w = synth.make_weights(cfg, 0)
+    rng = np.random.default_rng(1)
+    u = synth.make_user(cfg, rng, n_s=0, M=1)
+    cl = make_gpu(cfg, w, 1)
+    got = gpu_scores(cl, u)
+    ref = oracle_scores(cfg, w, u)[0]
+    assert parity_err(got, ref)[0] < 1e-4
+
+
+def test_device_errors_and_stale_handles():
+    import torch
+    from paper_2502_09888_b200 import ClimberError
+    cfg = synth.preset("tiny")
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 1, B=1)
+    cl = make_gpu(cfg, w, 1)
+    item, action, scenario, ts, cand = to_dev(batch)
+    bad_cand = cand.clone()
+    bad_cand[3] = cfg.V + 5
+    hs = cl.encode_users(batch.ev_offsets, item, action, scenario, ts, batch.r)
+    s = cl.score_batched(hs, batch.cand_offsets, bad_cand).cpu().numpy()
+    with pytest.raises(ClimberError) as ei:
+        cl.stream_status()
+    assert ei.value.name == "E_OUT_OF_RANGE"
+    assert np.isnan(s[3]) and np.all(np.isfinite(np.delete(s, 3)))   # only that candidate
+    cl.release(hs)
+    with pytest.raises(ClimberError) as ei:
+        cl.release(hs)
+    assert ei.value.name == "E_STALE"
+    with pytest.raises(ClimberError) as ei:
+        cl.score_batched(hs, batch.cand_offsets, cand)
+    assert ei.value.name == "E_STALE"
+    ts_bad = ts.clone()
+    ts_bad[10] = ts_bad[9] - 1
+    hs = cl.encode_users(batch.ev_offsets, item, action, scenario, ts_bad, batch.r)
+    with pytest.raises(ClimberError) as ei:
+        cl.stream_status()
+    assert ei.value.name == "E_UNSORTED"
+    cl.release(hs)
+    with pytest.raises(ClimberError) as ei:
+        cl.score_batched(hs, np.array([0, cfg.M + 1]), cand)
+    assert ei.value.name in ("E_INVALID_ARG", "E_STALE")
+
+
+def test_rank_host_end_to_end():
+    cfg = synth.preset("small")
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 1, B=4)
+    cl = make_gpu(cfg, w, 4)
+    s_host = cl.rank_host(batch.ev_offsets, batch.item, batch.action, batch.scenario, batch.ts, batch.r,
+                          batch.cand_offsets, batch.cand)
+    s_dev = gpu_scores(cl, batch)
+    assert np.array_equal(s_host, s_dev)
