@@ -242,6 +242,28 @@ climber_status climber_debug_kv(climber_ctx_t ctx, climber_kv_t kv, int32_t laye
 climber_status climber_debug_gemm(const void* A, const void* B, float* D, int64_t M, int32_t N, int32_t K,
                                   int32_t use_tc, climber_stream_t stream);
 
+/* ---- measurement (bench evidence) ---- */
+
+/* Kernel classes timed by the profiler. */
+typedef enum {
+  CLIMBER_K_EXTRACT = 0, CLIMBER_K_EMBED = 1, CLIMBER_K_RMSNORM = 2, CLIMBER_K_GEMM_QKV = 3,
+  CLIMBER_K_GEMM_O = 4, CLIMBER_K_GEMM_FFN_UP = 5, CLIMBER_K_GEMM_FFN_DOWN = 6, CLIMBER_K_GEMM_SE = 7,
+  CLIMBER_K_ATTN_HIST = 8, CLIMBER_K_ATTN_SUMI = 9, CLIMBER_K_ATTN_FUSION = 10, CLIMBER_K_HEAD = 11,
+  CLIMBER_K_OTHER = 12, CLIMBER_K_NUM = 13
+} climber_kernel_class;
+
+/* enable != 0: every subsequent launch is bracketed by CUDA events recorded on
+ * its own stream, accumulated per kernel class.  enable == 0 stops. */
+climber_status climber_profile(climber_ctx_t ctx, int32_t enable);
+
+/* Synchronise, then for each class c write out[4*c + 0..3] = {launches,
+ * total device ms, algorithmic FLOPs, algorithmic HBM bytes} accumulated since
+ * the previous read, and reset.  out: HOST double[4 * CLIMBER_K_NUM].
+ * FLOPs/bytes are what the operation must compute/move (GEMM 2MNK; attention
+ * 4 * pairs * d with every history row valid; memory-bound kernels one read of
+ * each input and one write of each output). */
+climber_status climber_profile_read(climber_ctx_t ctx, double* out);
+
 /* Number of kernel launches the library has enqueued since the ctx was
  * created (bench evidence for "gpu_launches"). */
 int64_t climber_launch_count(climber_ctx_t ctx);

@@ -83,6 +83,8 @@ def lib() -> C.CDLL:
             "climber_debug_kv": (I32, [VP, VP, I32, I32, P, P]),
             "climber_launch_count": (I64, [VP]),
             "climber_debug_gemm": (I32, [VP, VP, VP, I64, I32, I32, I32, VP]),
+            "climber_profile": (I32, [VP, I32]),
+            "climber_profile_read": (I32, [VP, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -96,7 +98,10 @@ EXPORTED_SYMBOLS = ("climber_arena_bytes", "climber_create", "climber_destroy", 
                     "climber_encode_users", "climber_score_items", "climber_score_items_batched",
                     "climber_rank_host", "climber_kv_release", "climber_kv_broadcast", "climber_stream_status",
                     "climber_last_error", "climber_debug_extract", "climber_debug_mask", "climber_debug_kv",
-                    "climber_launch_count", "climber_debug_gemm")
+                    "climber_launch_count", "climber_debug_gemm", "climber_profile", "climber_profile_read")
+
+KERNEL_CLASSES = ("extract", "embed", "rmsnorm", "gemm_qkv", "gemm_o", "gemm_ffn_up", "gemm_ffn_down", "gemm_se",
+                  "attn_hist", "attn_sumi", "attn_fusion", "head", "other")
 
 
 def _check(st: int):
@@ -209,6 +214,16 @@ class Climber:
     def _stream(self, stream=None):
         s = stream if stream is not None else self.torch.cuda.current_stream()
         return C.c_void_p(s.cuda_stream)
+
+    def profile(self, enable: bool):
+        _check(lib().climber_profile(self.h, int(bool(enable))))
+
+    def profile_read(self) -> dict:
+        """{class: {launches, ms, flops, bytes}} accumulated since the last read."""
+        out = np.zeros(4 * len(KERNEL_CLASSES), np.float64)
+        _check(lib().climber_profile_read(self.h, _ptr(out)))
+        return {n: dict(zip(("launches", "ms", "flops", "bytes"), out[4 * i:4 * i + 4].tolist()))
+                for i, n in enumerate(KERNEL_CLASSES)}
 
     @property
     def launch_count(self) -> int:

@@ -56,6 +56,7 @@ struct SlotState {
   std::vector<int> pages;
 };
 
+struct ProfRec;
 struct climber_ctx_s {
   climber_config cfg;
   Dims D;
@@ -92,6 +93,11 @@ struct climber_ctx_s {
   long long launches = 0;
   bool use_tc = true;
   bool sync_check = false;
+  // profiler
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_next = 0;
+  std::vector<struct ProfRec> recs;
   // rank_host staging (device, lazily allocated)
   void* io = nullptr;
   size_t io_bytes = 0;
@@ -367,6 +373,7 @@ extern "C" climber_status climber_destroy(climber_ctx_t c) {
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->io) cudaFree(c->io);
   cudaEventDestroy(c->stage_evt);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete c;
   return CLIMBER_OK;
 }
@@ -374,10 +381,50 @@ extern "C" climber_status climber_destroy(climber_ctx_t c) {
 // ---------------------------------------------------------------------------
 // GEMM dispatch: tcgen05 tensor cores for bf16, SIMT for the fp32 build
 // ---------------------------------------------------------------------------
+// Profiler: CUDA events on the launching stream around each launch, per class.
+struct ProfRec {
+  int cls;
+  cudaEvent_t e0, e1;
+  double flops, bytes;
+};
+
+static cudaEvent_t prof_event(climber_ctx_s* c) {
+  if (c->ev_next == c->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_next++];
+}
+
+struct Prof {
+  climber_ctx_s* c;
+  int cls;
+  cudaStream_t s;
+  double flops, bytes;
+  cudaEvent_t e0 = nullptr;
+  Prof(climber_ctx_s* c_, int cls_, cudaStream_t s_, double flops_ = 0, double bytes_ = 0)
+      : c(c_), cls(cls_), s(s_), flops(flops_), bytes(bytes_) {
+    c->launches++;
+    if (c->prof) {
+      e0 = prof_event(c);
+      cudaEventRecord(e0, s);
+    }
+  }
+  ~Prof() {
+    if (e0) {
+      cudaEvent_t e1 = prof_event(c);
+      cudaEventRecord(e1, s);
+      c->recs.push_back({cls, e0, e1, flops, bytes});
+    }
+  }
+};
+
+// GEMM dispatch: tcgen05 tensor cores for bf16, SIMT for the fp32 build
 template <typename T>
-static void gemm(climber_ctx_s* c, const T* A, long long lda, const T* B, long long ldb, long long M, int N, int K,
-                 const Epilogue& e, cudaStream_t s) {
-  c->launches++;
+static void gemm(climber_ctx_s* c, int cls, const T* A, long long lda, const T* B, long long ldb, long long M, int N,
+                 int K, const Epilogue& e, cudaStream_t s) {
+  Prof p(c, cls, s, 2.0 * M * N * K);
   if constexpr (std::is_same<T, bf16>::value) {
     if (c->use_tc && gemm_tc_supported(M, N, K, lda, ldb)) {
       launch_gemm_tc(A, lda, B, ldb, M, N, K, e, s);
@@ -402,44 +449,60 @@ static Epilogue epi_resid(float* out, long long ldo) {
 // encode: one wave of U users (SURVEY §3 call stack 1)
 // ---------------------------------------------------------------------------
 template <typename T>
-static void encode_wave(climber_ctx_s* c, const EventsDev& ev, int u0, int U, cudaStream_t s) {
+static void encode_wave(climber_ctx_s* c, const EventsDev& ev, int u0, int U, long long n_events, cudaStream_t s) {
   const Dims& D = c->D;
   const long long rows = (long long)U * D.nk;
   const long long d = D.d, F = D.F;
+  const double es = (double)c->esz;
   const int* wslot = c->d_slots + u0;
   const int* wr = c->d_r + u0;
-  launch_extract(ev, c->d_ev_off + u0, wslot, U, c->amask, c->smask, c->idx_all, c->vlen_all, c->bad_all, c->err, D, s);
-  c->launches++;
+  {
+    Prof p(c, CLIMBER_K_EXTRACT, s, 0, (double)n_events * 14 + (double)U * D.Nb * D.nk * 4);
+    launch_extract(ev, c->d_ev_off + u0, wslot, U, c->amask, c->smask, c->idx_all, c->vlen_all, c->bad_all, c->err,
+                   D, s);
+  }
   T* H = (T*)c->H;
   T* Qb = (T*)c->QKV;
   T* O = (T*)c->O;
   T* Fh = (T*)c->Fh;
+  const double norm_bytes = (double)rows * d * (4 + es);
+  const double causal_pairs = D.causal ? (double)D.nk * (D.nk + 1) / 2 : (double)D.nk * D.nk;
   for (int k = 0; k < D.Nb; ++k) {
-    launch_embed_hist<T>(ev, c->d_ev_off + u0, wslot, U, c->idx_all, c->vlen_all, c->bad_all, (const T*)c->e_item,
-                         (const T*)c->e_act, (const T*)c->e_scn, c->X, k, D, s);
-    c->launches++;
+    {
+      Prof p(c, CLIMBER_K_EMBED, s, 0, (double)rows * d * (3 * es + 4));
+      launch_embed_hist<T>(ev, c->d_ev_off + u0, wslot, U, c->idx_all, c->vlen_all, c->bad_all, (const T*)c->e_item,
+                           (const T*)c->e_act, (const T*)c->e_scn, c->X, k, D, s);
+    }
     for (int l = 0; l < D.L; ++l) {
       const size_t kl = (size_t)k * D.L + l;
-      launch_rmsnorm<T>(c->X, d, c->g1 + kl * d, H, d, rows, D.d, D.eps, s);
-      c->launches++;
+      {
+        Prof p(c, CLIMBER_K_RMSNORM, s, 0, norm_bytes);
+        launch_rmsnorm<T>(c->X, d, c->g1 + kl * d, H, d, rows, D.d, D.eps, s);
+      }
       Epilogue e{};
       e.kind = EPI_QKV_PAGES; e.out = Qb; e.ldo = d; e.pool = c->pool; e.ptab = c->ptab; e.wave_slot = wslot;
       e.blk = k; e.layer = l; e.d = D.d; e.h = D.h; e.dh = D.dh; e.nk = D.nk; e.Nb = D.Nb; e.L = D.L; e.ppb = D.ppb;
       const T* Wqkv = (const T*)c->w_qkv + kl * 3 * d * d;
       if (l < D.L - 1) {
         e.col_off = 0;
-        gemm<T>(c, H, d, Wqkv, d, rows, 3 * D.d, D.d, e, s);
-        launch_attn_hist<T>(Qb, wslot, wr, U, (const T*)c->pool, c->ptab, c->vlen_all, c->tau, O, k, l, D, s);
-        c->launches++;
-        gemm<T>(c, O, d, (const T*)c->w_o + kl * d * d, d, rows, D.d, D.d, epi_resid(c->X, d), s);
-        launch_rmsnorm<T>(c->X, d, c->g2 + kl * d, H, d, rows, D.d, D.eps, s);
-        c->launches++;
-        gemm<T>(c, H, d, (const T*)c->w1 + kl * F * d, d, rows, D.F, D.d, epi_store(Fh, F, ACT_SILU), s);
-        gemm<T>(c, Fh, F, (const T*)c->w2 + kl * d * F, F, rows, D.d, D.F, epi_resid(c->X, d), s);
+        gemm<T>(c, CLIMBER_K_GEMM_QKV, H, d, Wqkv, d, rows, 3 * D.d, D.d, e, s);
+        {
+          Prof p(c, CLIMBER_K_ATTN_HIST, s, 4.0 * U * causal_pairs * d, (double)rows * d * es * 4);
+          launch_attn_hist<T>(Qb, wslot, wr, U, (const T*)c->pool, c->ptab, c->vlen_all, c->tau, O, k, l, D, s);
+        }
+        gemm<T>(c, CLIMBER_K_GEMM_O, O, d, (const T*)c->w_o + kl * d * d, d, rows, D.d, D.d, epi_resid(c->X, d), s);
+        {
+          Prof p(c, CLIMBER_K_RMSNORM, s, 0, norm_bytes);
+          launch_rmsnorm<T>(c->X, d, c->g2 + kl * d, H, d, rows, D.d, D.eps, s);
+        }
+        gemm<T>(c, CLIMBER_K_GEMM_FFN_UP, H, d, (const T*)c->w1 + kl * F * d, d, rows, D.F, D.d,
+                epi_store(Fh, F, ACT_SILU), s);
+        gemm<T>(c, CLIMBER_K_GEMM_FFN_DOWN, Fh, F, (const T*)c->w2 + kl * d * F, F, rows, D.d, D.F,
+                epi_resid(c->X, d), s);
       } else {
         // last layer: only K/V of the history are ever read -> N = 2d
         e.col_off = D.d;
-        gemm<T>(c, H, d, Wqkv + d * d, d, rows, 2 * D.d, D.d, e, s);
+        gemm<T>(c, CLIMBER_K_GEMM_QKV, H, d, Wqkv + d * d, d, rows, 2 * D.d, D.d, e, s);
       }
     }
   }
@@ -453,6 +516,7 @@ static void score_wave(climber_ctx_s* c, const int32_t* items, const int64_t* wc
                        int Mmax_wave, float* scores, cudaStream_t s) {
   const Dims& D = c->D;
   const long long d = D.d, F = D.F, Nb = D.Nb, ldC = Nb * d;
+  const double es = (double)c->esz;
   const int* wslot = c->d_slots + u0;
   const int* wr = c->d_r + u0;
   T* H = (T*)c->H;
@@ -460,54 +524,76 @@ static void score_wave(climber_ctx_s* c, const int32_t* items, const int64_t* wc
   T* O = (T*)c->O;
   T* Fh = (T*)c->Fh;
   float* X = c->X;  // C[p][k][d]
-  launch_embed_cand<T>(items, wcand, wr, U, P, (const T*)c->e_item, (const T*)c->e_scn, X, c->err, D, s);
-  c->launches++;
+  {
+    Prof p(c, CLIMBER_K_EMBED, s, 0, (double)P * d * (2 * es + 4 * Nb));
+    launch_embed_cand<T>(items, wcand, wr, U, P, (const T*)c->e_item, (const T*)c->e_scn, X, c->err, D, s);
+  }
+  const double norm_bytes = (double)P * d * (4 + es);
   for (int k = 0; k < D.Nb; ++k) {
     float* Ck = X + k * d;
     for (int l = 0; l < D.L; ++l) {
       const size_t kl = (size_t)k * D.L + l;
-      launch_rmsnorm<T>(Ck, ldC, c->g1 + kl * d, H, d, P, D.d, D.eps, s);
-      c->launches++;
-      gemm<T>(c, H, d, (const T*)c->w_qkv + kl * 3 * d * d, d, P, 3 * D.d, D.d, epi_store(QKV, 3 * d), s);
-      launch_attn_sumi<T>(QKV, wcand, wslot, wr, U, Mmax_wave, (const T*)c->pool, c->ptab, c->vlen_all, c->tau, O, k,
-                          l, D, s);
-      c->launches++;
-      gemm<T>(c, O, d, (const T*)c->w_o + kl * d * d, d, P, D.d, D.d, epi_resid(Ck, ldC), s);
-      launch_rmsnorm<T>(Ck, ldC, c->g2 + kl * d, H, d, P, D.d, D.eps, s);
-      c->launches++;
-      gemm<T>(c, H, d, (const T*)c->w1 + kl * F * d, d, P, D.F, D.d, epi_store(Fh, F, ACT_SILU), s);
-      gemm<T>(c, Fh, F, (const T*)c->w2 + kl * d * F, F, P, D.d, D.F, epi_resid(Ck, ldC), s);
+      {
+        Prof p(c, CLIMBER_K_RMSNORM, s, 0, norm_bytes);
+        launch_rmsnorm<T>(Ck, ldC, c->g1 + kl * d, H, d, P, D.d, D.eps, s);
+      }
+      gemm<T>(c, CLIMBER_K_GEMM_QKV, H, d, (const T*)c->w_qkv + kl * 3 * d * d, d, P, 3 * D.d, D.d,
+              epi_store(QKV, 3 * d), s);
+      {
+        Prof p(c, CLIMBER_K_ATTN_SUMI, s, 4.0 * P * (D.nk + 1) * d,
+               (double)P * d * es * 4 + (double)U * D.nk * d * 2 * es);
+        launch_attn_sumi<T>(QKV, wcand, wslot, wr, U, Mmax_wave, (const T*)c->pool, c->ptab, c->vlen_all, c->tau, O,
+                            k, l, D, s);
+      }
+      gemm<T>(c, CLIMBER_K_GEMM_O, O, d, (const T*)c->w_o + kl * d * d, d, P, D.d, D.d, epi_resid(Ck, ldC), s);
+      {
+        Prof p(c, CLIMBER_K_RMSNORM, s, 0, norm_bytes);
+        launch_rmsnorm<T>(Ck, ldC, c->g2 + kl * d, H, d, P, D.d, D.eps, s);
+      }
+      gemm<T>(c, CLIMBER_K_GEMM_FFN_UP, H, d, (const T*)c->w1 + kl * F * d, d, P, D.F, D.d,
+              epi_store(Fh, F, ACT_SILU), s);
+      gemm<T>(c, CLIMBER_K_GEMM_FFN_DOWN, Fh, F, (const T*)c->w2 + kl * d * F, F, P, D.d, D.F, epi_resid(Ck, ldC),
+              s);
     }
   }
   // ---- BGF (Eq. 4): fusion ATL over the N_b tokens of every pair, rows = P*N_b
   const long long R = P * Nb;
-  launch_rmsnorm<T>(X, d, c->fg1, H, d, R, D.d, D.eps, s);
-  c->launches++;
-  gemm<T>(c, H, d, (const T*)c->fw_qkv, d, R, 3 * D.d, D.d, epi_store(QKV, 3 * d), s);
-  launch_attn_fusion<T>(QKV, wcand, wr, U, P, c->tau_f, O, D, s);
-  c->launches++;
-  gemm<T>(c, O, d, (const T*)c->fw_o, d, R, D.d, D.d, epi_resid(X, d), s);
-  launch_rmsnorm<T>(X, d, c->fg2, H, d, R, D.d, D.eps, s);
-  c->launches++;
-  gemm<T>(c, H, d, (const T*)c->fw1, d, R, D.F, D.d, epi_store(Fh, F, ACT_SILU), s);
-  gemm<T>(c, Fh, F, (const T*)c->fw2, F, R, D.d, D.F, epi_resid(X, d), s);
+  {
+    Prof p(c, CLIMBER_K_RMSNORM, s, 0, (double)R * d * (4 + es));
+    launch_rmsnorm<T>(X, d, c->fg1, H, d, R, D.d, D.eps, s);
+  }
+  gemm<T>(c, CLIMBER_K_GEMM_QKV, H, d, (const T*)c->fw_qkv, d, R, 3 * D.d, D.d, epi_store(QKV, 3 * d), s);
+  {
+    Prof p(c, CLIMBER_K_ATTN_FUSION, s, 4.0 * P * Nb * Nb * d, (double)R * d * es * 4);
+    launch_attn_fusion<T>(QKV, wcand, wr, U, P, c->tau_f, O, D, s);
+  }
+  gemm<T>(c, CLIMBER_K_GEMM_O, O, d, (const T*)c->fw_o, d, R, D.d, D.d, epi_resid(X, d), s);
+  {
+    Prof p(c, CLIMBER_K_RMSNORM, s, 0, (double)R * d * (4 + es));
+    launch_rmsnorm<T>(X, d, c->fg2, H, d, R, D.d, D.eps, s);
+  }
+  gemm<T>(c, CLIMBER_K_GEMM_FFN_UP, H, d, (const T*)c->fw1, d, R, D.F, D.d, epi_store(Fh, F, ACT_SILU), s);
+  gemm<T>(c, CLIMBER_K_GEMM_FFN_DOWN, Fh, F, (const T*)c->fw2, F, R, D.d, D.F, epi_resid(X, d), s);
   // ---- squeeze-and-excitation gate on vec(G) = X viewed as [P][N_b d]
   const T* G = nullptr;
   if constexpr (std::is_same<T, float>::value) {
     G = X;
   } else {
+    Prof p(c, CLIMBER_K_OTHER, s, 0, (double)P * D.Dse * (4 + es));
     launch_convert<T>(X, H, P * D.Dse, s);
-    c->launches++;
     G = H;
   }
   T* Z1 = O;  // [P][Hse]
-  gemm<T>(c, G, D.Dse, (const T*)c->w_se1, D.Dse, P, D.Hse, D.Dse, epi_store(Z1, D.Hse, ACT_RELU, c->b_se1), s);
+  gemm<T>(c, CLIMBER_K_GEMM_SE, G, D.Dse, (const T*)c->w_se1, D.Dse, P, D.Hse, D.Dse,
+          epi_store(Z1, D.Hse, ACT_RELU, c->b_se1), s);
   Epilogue eg{};
   eg.kind = EPI_GATE; eg.out = X; eg.ldo = D.Dse; eg.bias = c->b_se2;
-  gemm<T>(c, Z1, D.Hse, (const T*)c->w_se2, D.Hse, P, D.Dse, D.Hse, eg, s);
+  gemm<T>(c, CLIMBER_K_GEMM_SE, Z1, D.Hse, (const T*)c->w_se2, D.Hse, P, D.Dse, D.Hse, eg, s);
   // ---- head (G18)
-  launch_head(X, c->w_head, c->b_head, scores, P, D.Dse, s);
-  c->launches++;
+  {
+    Prof p(c, CLIMBER_K_HEAD, s, 2.0 * P * D.Dse, (double)P * D.Dse * 4 + P * 4);
+    launch_head(X, c->w_head, c->b_head, scores, P, D.Dse, s);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -542,8 +628,8 @@ static climber_status stage_upload(climber_ctx_s* c, int B, bool with_ptab, cuda
   CU(cudaMemcpyAsync(c->d_r, h.r, B * 4, cudaMemcpyHostToDevice, s));
   if (with_ptab) {
     CU(cudaMemcpyAsync(c->d_ptab_stage, h.ptab, (size_t)B * c->per_slot * 4, cudaMemcpyHostToDevice, s));
+    Prof p(c, CLIMBER_K_OTHER, s, 0, (double)B * c->per_slot * 8);
     launch_scatter_ptab(c->d_ptab_stage, c->d_slots, B, c->per_slot, c->ptab, s);
-    c->launches++;
   }
   CU(cudaEventRecord(c->stage_evt, s));
   return CLIMBER_OK;
@@ -608,8 +694,9 @@ extern "C" climber_status climber_encode_users(climber_ctx_t c, int32_t B, const
     EventsDev ev{events->item, events->action, events->scenario, events->ts};
     for (int u0 = 0; u0 < B; u0 += c->cfg.max_wave_users) {
       int U = B - u0 < c->cfg.max_wave_users ? B - u0 : c->cfg.max_wave_users;
-      if (c->cfg.dtype == CLIMBER_BF16) encode_wave<bf16>(c, ev, u0, U, s);
-      else encode_wave<float>(c, ev, u0, U, s);
+      long long nev = ev_offsets[u0 + U] - ev_offsets[u0];
+      if (c->cfg.dtype == CLIMBER_BF16) encode_wave<bf16>(c, ev, u0, U, nev, s);
+      else encode_wave<float>(c, ev, u0, U, nev, s);
       climber_status rs = check_launch(c, s);
       if (rs != CLIMBER_OK) return rs;
     }
@@ -873,6 +960,30 @@ extern "C" climber_status climber_debug_gemm(const void* A, const void* B, float
     launch_gemm_simt<bf16>((const bf16*)A, K, (const bf16*)B, K, M, N, K, e, s);
   }
   CU(cudaGetLastError());
+  return CLIMBER_OK;
+}
+
+extern "C" climber_status climber_profile(climber_ctx_t c, int32_t enable) {
+  if (!c) return fail(CLIMBER_E_INVALID_ARG, "null ctx");
+  c->prof = enable != 0;
+  return CLIMBER_OK;
+}
+
+extern "C" climber_status climber_profile_read(climber_ctx_t c, double* out) {
+  if (!c || !out) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+  for (int i = 0; i < 4 * CLIMBER_K_NUM; ++i) out[i] = 0;
+  for (const ProfRec& r : c->recs) {
+    CU(cudaEventSynchronize(r.e1));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, r.e0, r.e1));
+    double* o = out + 4 * r.cls;
+    o[0] += 1;
+    o[1] += ms;
+    o[2] += r.flops;
+    o[3] += r.bytes;
+  }
+  c->recs.clear();
+  c->ev_next = 0;
   return CLIMBER_OK;
 }
 
