@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""Benchmark: scored user-item pairs/s of SUMI ranking inference on B200.
+
+A step = one pass of the whole hot path over one
+batch: encode B users (extraction, embedding, N_b x L ATL stack, paged K/V
+cache) + score B x M candidates (SUMI attention, BGF, head) + release the
+handles.  Inputs are resident in HBM when the timed region starts; the K/V
+cache alone (68.7 GB at `large`) is far larger than the 126 MB L2, so no L2
+flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config large] [--impl climber|reference]
+
+N > 1 (torchrun, one rank per GPU): request sharding — every rank scores its
+own batch of B users (weak scaling), no data-path collective; the timed region
+is bracketed by barriers and the max over ranks is reported.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "scored user-item pairs/sec & p50 request latency at 1/2/4/8 B200 vs roofline"
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, \
+            "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        time.sleep(0.1)
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        load = [s for s in sm if s > 300] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(cfg, w, batch, budget_s=15.0):
+    """The fp64 oracle as it stands, on this host's cores, on a bounded sample
+    (whole users of the same batch, until ~budget_s of CPU work)."""
+    import oracle as O
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    strats = synth.strategies_for(cfg.N_b, cfg.R)
+    t0 = time.perf_counter()
+    pairs = users = 0
+    while users < batch.B and (users == 0 or time.perf_counter() - t0 < budget_s):
+        O.sumi_scores(cfg, w, strats, batch, users)
+        pairs += int(batch.cand_offsets[users + 1] - batch.cand_offsets[users])
+        users += 1
+    dt = time.perf_counter() - t0
+    return {"value": pairs / dt, "unit": "pairs/s", "cores": int(cores), "kind": "oracle",
+            "sample": f"{users} user(s) x {cfg.M} candidates of workload '{cfg.name}' (fp64 NumPy, {dt:.1f} s)"}
+
+
+def run_reference(args, cfg):
+    """--impl reference: the oracle on the host cores, each step a bounded
+    sample (one user with all M candidates) of the same workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 1, B=args.warmup + args.steps)
+    import oracle as O
+    strats = synth.strategies_for(cfg.N_b, cfg.R)
+    for b in range(args.warmup):
+        O.sumi_scores(cfg, w, strats, batch, b)
+    t0 = time.perf_counter()
+    pairs = 0
+    for i in range(args.steps):
+        b = args.warmup + i
+        O.sumi_scores(cfg, w, strats, batch, b)
+        pairs += int(batch.cand_offsets[b + 1] - batch.cand_offsets[b])
+    dt = time.perf_counter() - t0
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    v = pairs / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_cfg(cfg),
+            "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": int(cores), "kind": "oracle",
+                             "sample": f"1 user x {cfg.M} candidates per step of workload '{cfg.name}'"},
+            "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_cfg(cfg):
+    return {"workload": cfg.name, "B": cfg.B, "M": cfg.M, "n": cfg.n, "N_b": cfg.N_b, "n_k": cfg.n_k, "L": cfg.L,
+            "d": cfg.d, "h": cfg.h, "n_s": cfg.n_s if not cfg.n_s_max else [cfg.n_s, cfg.n_s_max],
+            "parallelism": "request-sharded replicas (no data-path collective)",
+            "l2": "no flush: per-step K/V cache + activations far exceed the 126 MB L2"}
+
+
+ROOF_CLASSES_TENSOR = ("gemm_qkv", "gemm_o", "gemm_ffn_up", "gemm_ffn_down", "gemm_se")
+
+
+def roofline(prof, pk, pk_src, bf16=True):
+    """Dominant kernel class by device time; achieved = algorithmic FLOPs (or
+    bytes) per launch / mean launch duration (CUDA events on the launch stream)."""
+    tot_ms = sum(v["ms"] for v in prof.values())
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    p = prof[dom]
+    n = max(p["launches"], 1)
+    ms_per_launch = p["ms"] / n
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom)
+        except Exception:
+            traffic = None
+    if dom.startswith("gemm"):
+        bound, unit = "tensor", "TFLOP/s"
+        ach = p["flops"] / n / (ms_per_launch * 1e-3) / 1e12
+        peak = pk["bf16_tflops_sustained"]
+        peak_note = f"bf16 dense, sustained ({pk_src})"
+    elif dom in ("attn_sumi", "attn_hist") and bf16:
+        # bf16 path: mma.sync tensor-core flash attention
+        bound, unit = "tensor", "TFLOP/s"
+        ach = p["flops"] / n / (ms_per_launch * 1e-3) / 1e12
+        peak = pk["bf16_tflops_sustained"]
+        peak_note = f"bf16 dense, sustained ({pk_src}); kernel uses mma.sync m16n8k16"
+    elif dom in ("attn_sumi", "attn_hist"):
+        # fp32 verification build: SIMT FMA; peak = 148 SM x 128 FP32 lanes x 2 FLOP x max SM clock
+        bound, unit = "alu", "TFLOP/s"
+        ach = p["flops"] / n / (ms_per_launch * 1e-3) / 1e12
+        peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        peak_note = "fp32 FMA: 148 SM x 128 lanes x 2 x sm_max_mhz (DESIGN.md §5)"
+    else:
+        bound, unit = "hbm", "GB/s"
+        ach = p["bytes"] / n / (ms_per_launch * 1e-3) / 1e9
+        peak = pk["hbm_gbs"]
+        peak_note = f"HBM copy ({pk_src})"
+    return {"kernel": dom, "bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+            "traffic": traffic, "launches": int(p["launches"]), "ms_per_launch": ms_per_launch,
+            "share_of_step": p["ms"] / tot_ms if tot_ms else None, "peak_source": peak_note}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="large", choices=sorted(synth.PRESETS))
+    ap.add_argument("--impl", default="climber", choices=["climber", "reference"])
+    ap.add_argument("--users", type=int, default=0, help="override B (users per rank per step)")
+    ap.add_argument("--latency-requests", type=int, default=30)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = synth.preset(args.config)
+    if args.users:
+        cfg = cfg.replace(B=args.users)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2502_09888_b200 import Climber, ModelConfig
+
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 1 + rank)
+    B, M = cfg.B, cfg.M
+    cl = Climber(ModelConfig.from_any(cfg), w, synth.strategies_for(cfg.N_b, cfg.R), max_users=B,
+                 max_wave_users=64, max_wave_pairs=max(M, 65536), kv_users=B)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    item, action, scenario, ts, cand = (dev(batch.item), dev(batch.action), dev(batch.scenario), dev(batch.ts),
+                                        dev(batch.cand))
+    scores = torch.empty(int(batch.cand_offsets[-1]), dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        hs = cl.encode_users(batch.ev_offsets, item, action, scenario, ts, batch.r)
+        cl.score_batched(hs, batch.cand_offsets, cand, scores)
+        cl.release(hs)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    cl.stream_status()
+    assert torch.isfinite(scores).all().item(), "non-finite scores"
+
+    # ---- timed region (device events, barrier + sync on both sides) ----
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    n0 = cl.launch_count
+    cl.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    cl.profile(False)
+    launches = cl.launch_count - n0
+    prof = cl.profile_read()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = t.item()
+    pairs_per_rank = int(batch.cand_offsets[-1]) * args.steps
+    value = pairs_per_rank * world / (ms_max / 1e3)
+
+    # ---- end to end through the public C ABI with HOST buffers ----
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        h = [pin(x) for x in (batch.ev_offsets, batch.item, batch.action, batch.scenario, batch.ts, batch.r,
+                              batch.cand_offsets, batch.cand)]
+        cl.rank_host(*h)  # warm the staging buffers
+        ksteps = max(2, args.steps // 2)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(ksteps):
+            out = cl.rank_host(*h)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device="cuda")
+        if dist:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        h2d = sum(a.nbytes for a in (h[1], h[2], h[3], h[4], h[7]))
+        e2e = {"value": int(batch.cand_offsets[-1]) * ksteps * world / (te.item() / 1e3), "unit": "pairs/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(out.nbytes), "steps": ksteps,
+               "api": "climber_rank_host (pinned host buffers)"}
+
+    # ---- per-request latency: one user, M candidates, host call to host scores ----
+    lat = None
+    if rank == 0 and args.latency_requests > 0:
+        one = [batch.subset([b % B]) for b in range(args.latency_requests + 5)]
+        tl = []
+        for i, u in enumerate(one):
+            t0 = time.perf_counter()
+            cl.rank_host(u.ev_offsets, u.item, u.action, u.scenario, u.ts, u.r, u.cand_offsets, u.cand)
+            if i >= 5:
+                tl.append((time.perf_counter() - t0) * 1e3)
+        lat = {"p50": float(np.percentile(tl, 50)), "p99": float(np.percentile(tl, 99)), "requests": len(tl),
+               "mode": "single GPU per request (B=1, M candidates), climber_rank_host, no CUDA graph"}
+
+    if rank == 0:
+        pk, pk_src = peaks()
+        roof = roofline(prof, pk, pk_src, cfg.dtype == "bf16")
+        tot_flops = sum(v["flops"] for v in prof.values())
+        line = {"metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if cfg.dtype == "bf16" else "f32",
+                "data": "synthetic", "config": workload_cfg(cfg), "roofline": roof,
+                "step_tflops": tot_flops / (ms_max * 1e-3) / 1e12,
+                "e2e": e2e, "latency_ms": lat, "gpu_launches": int(launches), "clocks": clk,
+                "kernel_ms": {k: round(v["ms"], 3) for k, v in prof.items() if v["launches"]}}
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg, w, batch, args.cpu_budget)
+        print(json.dumps(line), flush=True)
+    cl.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -92,6 +92,7 @@ struct climber_ctx_s {
   std::vector<SlotState> slots;
   long long launches = 0;
   bool use_tc = true;
+  bool use_mma_attn = true;
   bool sync_check = false;
   // profiler
   bool prof = false;
@@ -306,6 +307,8 @@ extern "C" climber_status climber_create(const climber_config* cfg, const climbe
     carve(c, cv);
     const char* env = getenv("CLIMBER_GEMM");
     c->use_tc = !(env && strcmp(env, "simt") == 0);
+    const char* ea = getenv("CLIMBER_ATTN");
+    c->use_mma_attn = !(ea && strcmp(ea, "simt") == 0);
     const char* sc = getenv("CLIMBER_SYNC_CHECK");
     c->sync_check = sc && atoi(sc) != 0;
 
@@ -481,6 +484,7 @@ static void encode_wave(climber_ctx_s* c, const EventsDev& ev, int u0, int U, lo
       }
       Epilogue e{};
       e.kind = EPI_QKV_PAGES; e.out = Qb; e.ldo = d; e.pool = c->pool; e.ptab = c->ptab; e.wave_slot = wslot;
+      e.pool_rows = c->n_pages * 2 * PAGE;
       e.blk = k; e.layer = l; e.d = D.d; e.h = D.h; e.dh = D.dh; e.nk = D.nk; e.Nb = D.Nb; e.L = D.L; e.ppb = D.ppb;
       const T* Wqkv = (const T*)c->w_qkv + kl * 3 * d * d;
       if (l < D.L - 1) {
@@ -488,7 +492,15 @@ static void encode_wave(climber_ctx_s* c, const EventsDev& ev, int u0, int U, lo
         gemm<T>(c, CLIMBER_K_GEMM_QKV, H, d, Wqkv, d, rows, 3 * D.d, D.d, e, s);
         {
           Prof p(c, CLIMBER_K_ATTN_HIST, s, 4.0 * U * causal_pairs * d, (double)rows * d * es * 4);
-          launch_attn_hist<T>(Qb, wslot, wr, U, (const T*)c->pool, c->ptab, c->vlen_all, c->tau, O, k, l, D, s);
+          if constexpr (std::is_same<T, bf16>::value) {
+            if (c->use_mma_attn) {
+              launch_attn_hist_mma(Qb, wslot, wr, U, (const T*)c->pool, c->ptab, c->vlen_all, c->tau, O, k, l, D, s);
+            } else {
+              launch_attn_hist<T>(Qb, wslot, wr, U, (const T*)c->pool, c->ptab, c->vlen_all, c->tau, O, k, l, D, s);
+            }
+          } else {
+            launch_attn_hist<T>(Qb, wslot, wr, U, (const T*)c->pool, c->ptab, c->vlen_all, c->tau, O, k, l, D, s);
+          }
         }
         gemm<T>(c, CLIMBER_K_GEMM_O, O, d, (const T*)c->w_o + kl * d * d, d, rows, D.d, D.d, epi_resid(c->X, d), s);
         {
@@ -542,8 +554,18 @@ static void score_wave(climber_ctx_s* c, const int32_t* items, const int64_t* wc
       {
         Prof p(c, CLIMBER_K_ATTN_SUMI, s, 4.0 * P * (D.nk + 1) * d,
                (double)P * d * es * 4 + (double)U * D.nk * d * 2 * es);
-        launch_attn_sumi<T>(QKV, wcand, wslot, wr, U, Mmax_wave, (const T*)c->pool, c->ptab, c->vlen_all, c->tau, O,
-                            k, l, D, s);
+        if constexpr (std::is_same<T, bf16>::value) {
+          if (c->use_mma_attn) {
+            launch_attn_sumi_mma(QKV, wcand, wslot, wr, U, Mmax_wave, (const T*)c->pool, c->ptab, c->vlen_all, c->tau,
+                                 O, k, l, D, s);
+          } else {
+            launch_attn_sumi<T>(QKV, wcand, wslot, wr, U, Mmax_wave, (const T*)c->pool, c->ptab, c->vlen_all, c->tau,
+                                O, k, l, D, s);
+          }
+        } else {
+          launch_attn_sumi<T>(QKV, wcand, wslot, wr, U, Mmax_wave, (const T*)c->pool, c->ptab, c->vlen_all, c->tau, O,
+                              k, l, D, s);
+        }
       }
       gemm<T>(c, CLIMBER_K_GEMM_O, O, d, (const T*)c->w_o + kl * d * d, d, P, D.d, D.d, epi_resid(Ck, ldC), s);
       {
@@ -586,13 +608,14 @@ static void score_wave(climber_ctx_s* c, const int32_t* items, const int64_t* wc
   T* Z1 = O;  // [P][Hse]
   gemm<T>(c, CLIMBER_K_GEMM_SE, G, D.Dse, (const T*)c->w_se1, D.Dse, P, D.Hse, D.Dse,
           epi_store(Z1, D.Hse, ACT_RELU, c->b_se1), s);
+  float* gate = reinterpret_cast<float*>(c->Fh);  // [P][Dse] fp32 (fits: rows_cap * F * esz >= P * Dse * 4)
   Epilogue eg{};
-  eg.kind = EPI_GATE; eg.out = X; eg.ldo = D.Dse; eg.bias = c->b_se2;
+  eg.kind = EPI_STORE_F32; eg.act = ACT_SIGMOID; eg.out = gate; eg.ldo = D.Dse; eg.bias = c->b_se2;
   gemm<T>(c, CLIMBER_K_GEMM_SE, Z1, D.Hse, (const T*)c->w_se2, D.Hse, P, D.Dse, D.Hse, eg, s);
-  // ---- head (G18)
+  // ---- Y = G . gate (Eq. 4) fused with the head (G18)
   {
-    Prof p(c, CLIMBER_K_HEAD, s, 2.0 * P * D.Dse, (double)P * D.Dse * 4 + P * 4);
-    launch_head(X, c->w_head, c->b_head, scores, P, D.Dse, s);
+    Prof p(c, CLIMBER_K_HEAD, s, 3.0 * P * D.Dse, (double)P * D.Dse * 8 + P * 4);
+    launch_head(X, gate, c->w_head, c->b_head, scores, P, D.Dse, s);
   }
 }
 

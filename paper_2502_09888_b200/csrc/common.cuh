@@ -59,8 +59,9 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-__device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
-__device__ __forceinline__ float sigmoid_f(float x) { return 1.0f / (1.0f + __expf(-x)); }
+// fast-math activations (MUFU ex2 + rcp): SiLU (G8), sigmoid (Eq. 4)
+__device__ __forceinline__ float silu_f(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
+__device__ __forceinline__ float sigmoid_f(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 
 // SUMI visibility rule in canonical coordinates (G1,
 // G12, G14): slots 0..nk-1 are history (left-padded, valid iff >= nk - v),
@@ -83,9 +84,16 @@ enum EpiKind : int {
   EPI_STORE = 0,   // out_T[m*ldo + n] = act(acc + bias[n])
   EPI_RESID = 1,   // out_f32[m*ldo + n] += acc
   EPI_QKV_PAGES = 2, // columns (n + col_off) in [0,d): Q -> out_T[m*ldo + n]; [d,3d): K/V -> pages
-  EPI_GATE = 3,    // out_f32[m*ldo + n] *= sigmoid(acc + bias[n])   (Eq. 4 bit-wise gate)
+  EPI_STORE_F32 = 3, // out_f32[m*ldo + n] = act(acc + bias[n])  (the sigmoid gate of Eq. 4)
 };
-enum ActKind : int { ACT_NONE = 0, ACT_SILU = 1, ACT_RELU = 2 };
+enum ActKind : int { ACT_NONE = 0, ACT_SILU = 1, ACT_RELU = 2, ACT_SIGMOID = 3 };
+
+__device__ __forceinline__ float apply_act(int act, float a) {
+  if (act == ACT_SILU) return silu_f(a);
+  if (act == ACT_RELU) return fmaxf(a, 0.0f);
+  if (act == ACT_SIGMOID) return sigmoid_f(a);
+  return a;
+}
 
 struct Epilogue {
   int kind;
@@ -95,6 +103,7 @@ struct Epilogue {
   const float* bias;    // [N] or nullptr
   // EPI_QKV_PAGES: history row m = u * nk + t of wave user u
   void* pool;           // page pool base (T*)
+  long long pool_rows;  // n_pages * 2 * PAGE
   const int* ptab;      // [slots][Nb][L][ppb]
   const int* wave_slot; // [U] slot of wave user u
   int col_off;          // 0 (full QKV) or d (last layer: K/V only)
@@ -102,10 +111,16 @@ struct Epilogue {
   int d, h, dh, nk, Nb, L, ppb;
 };
 
-// Page addressing: page = [2 (K,V)][h][PAGE][dh] elements.
+// Page addressing: page = [2 (K,V)][PAGE tokens][d] elements (heads contiguous
+// d_h column groups inside a token row).  Viewed as a 2-D [n_pages*2*PAGE][d]
+// matrix, the K (or V) rows of 32 consecutive tokens of one page are one TMA
+// box, which is how the QKV GEMM epilogue writes them.
+__host__ __device__ __forceinline__ long long page_row(int page, int kv, int slot_t) {
+  return ((long long)page * 2 + kv) * PAGE + slot_t;
+}
 __device__ __forceinline__ long long page_elem_offset(int page, int kv, int head, int slot_t, int dim,
-                                                      int h, int dh) {
-  return (((long long)page * 2 + kv) * h + head) * (long long)(PAGE * dh) + (long long)slot_t * dh + dim;
+                                                      int d, int dh) {
+  return page_row(page, kv, slot_t) * d + (long long)head * dh + dim;
 }
 
 // Apply the epilogue to NC consecutive columns [n0, n0+NC) of row m.
@@ -114,12 +129,7 @@ __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, long long m, i
   if (e.kind == EPI_STORE) {
     float x[NC];
 #pragma unroll
-    for (int i = 0; i < NC; ++i) {
-      float a = v[i] + (e.bias ? e.bias[n0 + i] : 0.0f);
-      if (e.act == ACT_SILU) a = silu_f(a);
-      else if (e.act == ACT_RELU) a = fmaxf(a, 0.0f);
-      x[i] = a;
-    }
+    for (int i = 0; i < NC; ++i) x[i] = apply_act(e.act, v[i] + (e.bias ? e.bias[n0 + i] : 0.0f));
     T* o = reinterpret_cast<T*>(e.out) + m * e.ldo + n0;
     if constexpr (NC % 8 == 0) {
 #pragma unroll
@@ -132,10 +142,10 @@ __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, long long m, i
     float* o = reinterpret_cast<float*>(e.out) + m * e.ldo + n0;
 #pragma unroll
     for (int i = 0; i < NC; ++i) o[i] += v[i];
-  } else if (e.kind == EPI_GATE) {
+  } else if (e.kind == EPI_STORE_F32) {
     float* o = reinterpret_cast<float*>(e.out) + m * e.ldo + n0;
 #pragma unroll
-    for (int i = 0; i < NC; ++i) o[i] = o[i] * sigmoid_f(v[i] + e.bias[n0 + i]);
+    for (int i = 0; i < NC; ++i) o[i] = apply_act(e.act, v[i] + (e.bias ? e.bias[n0 + i] : 0.0f));
   } else {  // EPI_QKV_PAGES
     int c = n0 + e.col_off;
     if (c < e.d) {
@@ -149,9 +159,38 @@ __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, long long m, i
       int kv = (c >= 2 * e.d) ? 1 : 0;
       int cc = c - e.d * (1 + kv);
       int head = cc / e.dh, dim = cc % e.dh;   // NC divides dh: chunk stays in one head
-      T* o = reinterpret_cast<T*>(e.pool) + page_elem_offset(page, kv, head, t % PAGE, dim, e.h, e.dh);
+      T* o = reinterpret_cast<T*>(e.pool) + page_elem_offset(page, kv, head, t % PAGE, dim, e.d, e.dh);
 #pragma unroll
       for (int i = 0; i < NC; ++i) o[i] = from_f<T>(v[i]);
+    }
+  }
+}
+
+// Element-wise form of the same epilogues: one value of row m, column n.  The
+// tensor-core GEMM transposes each 32x32 accumulator block through shared
+// memory so that lane j handles column n0 + j of one row: every warp-level
+// access is then a contiguous row segment (coalesced) instead of 32 rows.
+template <typename T>
+__device__ __forceinline__ void epilogue_elem(const Epilogue& e, long long m, int n, float v) {
+  if (e.kind == EPI_STORE) {
+    reinterpret_cast<T*>(e.out)[m * e.ldo + n] = from_f<T>(apply_act(e.act, v + (e.bias ? e.bias[n] : 0.0f)));
+  } else if (e.kind == EPI_RESID) {
+    float* o = reinterpret_cast<float*>(e.out) + m * e.ldo + n;
+    *o += v;
+  } else if (e.kind == EPI_STORE_F32) {
+    reinterpret_cast<float*>(e.out)[m * e.ldo + n] = apply_act(e.act, v + (e.bias ? e.bias[n] : 0.0f));
+  } else {  // EPI_QKV_PAGES
+    int c = n + e.col_off;
+    if (c < e.d) {
+      reinterpret_cast<T*>(e.out)[m * e.ldo + c] = from_f<T>(v);
+    } else {
+      int u = (int)(m / e.nk), t = (int)(m % e.nk);
+      int slot = e.wave_slot[u];
+      int page = e.ptab[(((long long)slot * e.Nb + e.blk) * e.L + e.layer) * e.ppb + t / PAGE];
+      int kv = (c >= 2 * e.d) ? 1 : 0;
+      int cc = c - e.d * (1 + kv);
+      reinterpret_cast<T*>(e.pool)[page_elem_offset(page, kv, cc / e.dh, t % PAGE, cc % e.dh, e.d, e.dh)] =
+          from_f<T>(v);
     }
   }
 }

@@ -103,6 +103,23 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// TMA tile store / reduce-add from shared memory (bulk-group completion)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void st_shared_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -111,13 +128,16 @@ struct Smem {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int STG_OFF = STAGES * STAGE_BYTES;  // epilogue staging: 4 warps x 2 x (32 rows x 128 B)
+  static constexpr int STG_WARP = 2 * 32 * 128;
+  static constexpr int BAR_OFF = STG_OFF + 4 * STG_WARP;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + tmem addr, + alignment slack
 };
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, long long M, int N,
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmP, long long M, int N,
               int K, Epilogue e) {
   using S = Smem<BN, STAGES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -137,6 +157,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmD) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmP) : "memory");
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -205,29 +227,105 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue ----------------
+    // STORE / STORE_F32 / RESID: TMEM -> registers -> (bias, activation) ->
+    // 128B-swizzled smem (32 rows x 128 B per warp, double buffered) -> one TMA
+    // tile store (or TMA reduce-add into the fp32 residual) per 32-row chunk.
+    // QKV_PAGES (d % 64 == 0): Q columns -> TMA store into Q, K/V columns ->
+    // TMA store of 32 token rows straight into the user's K/V page (the 32-row
+    // group lies in one user and one page since n_k % 32 == 0).
+    // Otherwise: transpose through smem, lane = column, coalesced page stores.
     const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31
+    uint8_t* stg = smem + S::STG_OFF + ew * S::STG_WARP;
+    const bool tma_epi = e.kind != EPI_QKV_PAGES || (e.d % 64 == 0);
+    const bool f32_out = e.kind == EPI_RESID || e.kind == EPI_STORE_F32;
+    const int CW = f32_out ? 32 : 64;  // columns per 128-byte staged row
+    int sbuf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const int m_blk = (int)(t / n_tiles), n_blk = (int)(t % n_tiles);
       mbar_wait(&tfull[acc], acc_phase);
       fence_after();
-      const long long row = (long long)m_blk * BM + ew * 32 + lane;
+      const long long row0 = (long long)m_blk * BM + ew * 32;
       const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+      if (tma_epi) {
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        float v[32];
-        tmem_ld32(taddr + c, v);
-        if (row < M) {
+        for (int c = 0; c < BN; c += CW) {
+          float v[64];
+          tmem_ld32(taddr + c, v);  // lane = row row0 + lane
+          if (!f32_out) tmem_ld32(taddr + c + 32, v + 32);
           const int n0 = n_blk * BN + c;
-          epilogue_chunk<bf16, 16>(e, row, n0, v);
-          epilogue_chunk<bf16, 16>(e, row, n0 + 16, v + 16);
+          if (e.kind != EPI_RESID && e.kind != EPI_QKV_PAGES) {
+#pragma unroll
+            for (int i = 0; i < 64; ++i)
+              if (i < CW) v[i] = apply_act(e.act, v[i] + (e.bias ? e.bias[n0 + i] : 0.0f));
+          }
+          uint8_t* buf = stg + sbuf * 4096;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+          uint8_t* rowp = buf + lane * 128;
+          if (f32_out) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              st_shared_v4(rowp + ((j ^ (lane & 7)) << 4), __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                           __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              __nv_bfloat162 p0 = __floats2bfloat162_rn(v[8 * j], v[8 * j + 1]);
+              __nv_bfloat162 p1 = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
+              __nv_bfloat162 p2 = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
+              __nv_bfloat162 p3 = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
+              st_shared_v4(rowp + ((j ^ (lane & 7)) << 4), *reinterpret_cast<uint32_t*>(&p0),
+                           *reinterpret_cast<uint32_t*>(&p1), *reinterpret_cast<uint32_t*>(&p2),
+                           *reinterpret_cast<uint32_t*>(&p3));
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0 && row0 < M) {
+            if (e.kind == EPI_RESID) {
+              tma_reduce_add_2d(&tmD, buf, n0, (int)row0);
+            } else if (e.kind == EPI_QKV_PAGES) {
+              const int cg = n0 + e.col_off;
+              if (cg < e.d) {
+                tma_store_2d(&tmD, buf, cg, (int)row0);
+              } else {
+                const int kv = cg >= 2 * e.d ? 1 : 0;
+                const int cc = cg - e.d * (1 + kv);
+                const int u = (int)(row0 / e.nk), tt = (int)(row0 % e.nk);
+                const int slot = e.wave_slot[u];
+                const int page = e.ptab[(((long long)slot * e.Nb + e.blk) * e.L + e.layer) * e.ppb + tt / PAGE];
+                tma_store_2d(&tmP, buf, cc, (int)page_row(page, kv, tt % PAGE));
+              }
+            } else {
+              tma_store_2d(&tmD, buf, n0, (int)row0);
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          sbuf ^= 1;
+        }
+      } else {
+        float (*tr)[33] = reinterpret_cast<float (*)[33]>(stg);
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tmem_ld32(taddr + c, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) tr[lane][i] = v[i];
+          __syncwarp();
+          const int n = n_blk * BN + c + lane;
+#pragma unroll 4
+          for (int i = 0; i < 32; ++i)  // row row0 + i, lane = column: coalesced
+            if (row0 + i < M) epilogue_elem<bf16>(e, row0 + i, n, tr[i][lane]);
+          __syncwarp();
         }
       }
       fence_before();
       mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   fence_before();
   __syncthreads();
@@ -253,14 +351,17 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-static bool make_map(CUtensorMap* map, const bf16* ptr, long long rows, int K, long long ld, int box_rows) {
+static bool make_map(CUtensorMap* map, const void* ptr, long long rows, int cols, long long ld, int box_rows,
+                     int box_cols = BK, bool f32 = false) {
   auto enc = get_encode();
   if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  const int es = f32 ? 4 : 2;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * es};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<bf16*>(ptr), dims, strides, box, estr,
+  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -280,9 +381,22 @@ static int num_sms() {
 template <int BN, int STAGES>
 static void launch(const bf16* A, long long lda, const bf16* B, long long ldb, long long M, int N, int K,
                    const Epilogue& e, cudaStream_t s) {
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, md, mp;
   make_map(&ma, A, M, K, lda, BM);
   make_map(&mb, B, N, K, ldb, BN);
+  mp = ma;  // unused unless QKV_PAGES
+  if (e.kind == EPI_QKV_PAGES) {
+    if (e.d % 64 == 0) {
+      make_map(&md, e.out, M, e.d, e.ldo, 32, 64, false);          // Q buffer [M][d]
+      make_map(&mp, e.pool, e.pool_rows, e.d, e.d, 32, 64, false);  // pages as [n_pages*2*64][d]
+    } else {
+      md = ma;
+    }
+  } else if (e.kind == EPI_STORE) {
+    make_map(&md, e.out, M, N, e.ldo, 32, 64, false);
+  } else {
+    make_map(&md, e.out, M, N, e.ldo, 32, 32, true);
+  }
   constexpr int smem = Smem<BN, STAGES>::TOTAL;
   static bool attr = false;
   if (!attr) {
@@ -291,13 +405,13 @@ static void launch(const bf16* A, long long lda, const bf16* B, long long ldb, l
   }
   long long tiles = ((M + BM - 1) / BM) * (N / BN);
   int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  k_gemm_tc<BN, STAGES><<<grid, NUM_THREADS, smem, s>>>(ma, mb, M, N, K, e);
+  k_gemm_tc<BN, STAGES><<<grid, NUM_THREADS, smem, s>>>(ma, mb, md, mp, M, N, K, e);
 }
 
 }  // namespace tc
 
 bool gemm_tc_supported(long long M, int N, int K, long long lda, long long ldb) {
-  if (M < 1 || K < tc::BK || K % tc::BK || N % 128) return false;
+  if (M < 1 || M >= (1LL << 31) || K < tc::BK || K % tc::BK || N % 128) return false;
   if ((lda * 2) % 16 || (ldb * 2) % 16) return false;
   return tc::get_encode() != nullptr;
 }

@@ -187,19 +187,22 @@ __global__ void k_convert(const float* __restrict__ X, T* __restrict__ out, long
   store8(out + i * 8, v);
 }
 
-// a6 head (G18): score[p] = w_head . Y[p] + b_head.  Warp per row, fixed order.
-__global__ void k_head(const float* __restrict__ Y, const float* __restrict__ w, float b,
-                       float* __restrict__ scores, long long P, int D) {
+// Eq. 4 gate product fused with the a6 head (G18):
+//   score[p] = sum_c (G[p][c] * gate[p][c]) * w_head[c] + b_head,
+// gate = sigmoid(f_gate(G)) from the SE GEMM epilogue.  Warp per row, fixed order.
+__global__ void k_head(const float* __restrict__ Y, const float* __restrict__ gate, const float* __restrict__ w,
+                       float b, float* __restrict__ scores, long long P, int D) {
   long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (p >= P) return;
   float acc = 0.f;
   for (int c = lane * 8; c < D; c += 256) {
-    float y[8], ww[8];
+    float y[8], gg[8], ww[8];
     load8(Y + p * D + c, y);
+    load8(gate + p * D + c, gg);
     load8(w + c, ww);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc = fmaf(y[i], ww[i], acc);
+    for (int i = 0; i < 8; ++i) acc = fmaf(y[i] * gg[i], ww[i], acc);
   }
   acc = warp_sum(acc);
   if (lane == 0) scores[p] = acc + b;
@@ -216,17 +219,17 @@ constexpr float LOG2E = 1.4426950408889634f;
 
 template <typename T, int DH>
 __device__ __forceinline__ void load_kv_chunk(float (*Ks)[DH + 1], float (*Vs)[DH + 1], const T* pool,
-                                              const int* pages, int t0, int nkeys, int head, int h) {
+                                              const int* pages, int t0, int nkeys, int head, int d) {
   // nkeys <= KC tokens starting at t0; a chunk never crosses a page (PAGE % KC == 0)
   const int page = pages[t0 / PAGE];
-  const T* kb = pool + page_elem_offset(page, 0, head, t0 % PAGE, 0, h, DH);
-  const T* vb = pool + page_elem_offset(page, 1, head, t0 % PAGE, 0, h, DH);
+  const T* kb = pool + page_elem_offset(page, 0, head, t0 % PAGE, 0, d, DH);
+  const T* vb = pool + page_elem_offset(page, 1, head, t0 % PAGE, 0, d, DH);
   for (int i = threadIdx.x; i < KC * DH; i += blockDim.x) {
     int j = i / DH, c = i % DH;
     float kv = 0.f, vv = 0.f;
     if (j < nkeys) {
-      kv = to_f(kb[i]);
-      vv = to_f(vb[i]);
+      kv = to_f(kb[(long long)j * d + c]);
+      vv = to_f(vb[(long long)j * d + c]);
     }
     Ks[j][c] = kv;
     Vs[j][c] = vv;
@@ -311,7 +314,7 @@ __global__ void __launch_bounds__(128) k_attn_sumi(const T* __restrict__ QKV, co
   for (int t0 = 0; t0 < v; t0 += KC) {
     int nkeys = min(KC, v - t0);
     __syncthreads();
-    load_kv_chunk<T, DH>(Ks, Vs, pool, pages, t0, nkeys, head, D.h);
+    load_kv_chunk<T, DH>(Ks, Vs, pool, pages, t0, nkeys, head, D.d);
     __syncthreads();
     if (active) online_chunk<DH>(Ks, Vs, q, o, m, lsum, nkeys);
   }
@@ -366,7 +369,7 @@ __global__ void __launch_bounds__(128) k_attn_hist(const T* __restrict__ Q, cons
   for (int t0 = 0; t0 < kend; t0 += KC) {
     int nkeys = min(KC, v - t0);
     __syncthreads();
-    load_kv_chunk<T, DH>(Ks, Vs, pool, pages, t0, nkeys, head, D.h);
+    load_kv_chunk<T, DH>(Ks, Vs, pool, pages, t0, nkeys, head, D.d);
     __syncthreads();
     if (active) {
       int jmax = D.causal ? min(nkeys, t - t0 + 1) : nkeys;
@@ -474,8 +477,8 @@ __global__ void k_debug_kv(const T* __restrict__ pool, const int* __restrict__ p
     int t = (int)(g / D.d), c = (int)(g % D.d);
     int head = c / D.dh, dim = c % D.dh;
     int page = pages[t / PAGE];
-    Kout[g] = pool[page_elem_offset(page, 0, head, t % PAGE, dim, D.h, D.dh)];
-    Vout[g] = pool[page_elem_offset(page, 1, head, t % PAGE, dim, D.h, D.dh)];
+    Kout[g] = pool[page_elem_offset(page, 0, head, t % PAGE, dim, D.d, D.dh)];
+    Vout[g] = pool[page_elem_offset(page, 1, head, t % PAGE, dim, D.d, D.dh)];
   }
 }
 
@@ -575,8 +578,9 @@ void launch_convert(const float* X, T* out, long long n, cudaStream_t s) {
   k_convert<T><<<blocks_for(n / 8, 256), 256, 0, s>>>(X, out, n / 8);
 }
 
-void launch_head(const float* Y, const float* w, float b, float* scores, long long P, int Dse, cudaStream_t s) {
-  k_head<<<blocks_for(P * 32, 256), 256, 0, s>>>(Y, w, b, scores, P, Dse);
+void launch_head(const float* Y, const float* gate, const float* w, float b, float* scores, long long P, int Dse,
+                 cudaStream_t s) {
+  k_head<<<blocks_for(P * 32, 256), 256, 0, s>>>(Y, gate, w, b, scores, P, Dse);
 }
 
 template <typename T>

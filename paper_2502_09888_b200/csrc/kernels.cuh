@@ -26,7 +26,8 @@ void launch_rmsnorm(const float* X, long long ldx, const float* g, T* out, long 
                     float eps, cudaStream_t s);
 template <typename T>
 void launch_convert(const float* X, T* out, long long n, cudaStream_t s);
-void launch_head(const float* Y, const float* w, float b, float* scores, long long P, int Dse, cudaStream_t s);
+void launch_head(const float* Y, const float* gate, const float* w, float b, float* scores, long long P, int Dse,
+                 cudaStream_t s);
 template <typename T>
 void launch_attn_sumi(const T* QKV, const int64_t* cand_off, const int* wave_slot, const int* wave_r, int U,
                       int Mmax, const T* pool, const int* ptab, const int* vlen_all, const float* tau, T* O, int k,
@@ -45,6 +46,15 @@ void launch_scatter_ptab(const int* staged, const int* slots, int B, int per, in
 template <typename T>
 void launch_gemm_simt(const T* A, long long lda, const T* B, long long ldb, long long M, int N, int K,
                       const Epilogue& e, cudaStream_t s);
+
+// Tensor-core (mma.sync) attention for the bf16 path, attn_mma.cu.
+bool attn_mma_supported(int dh);
+void launch_attn_sumi_mma(const bf16* QKV, const int64_t* cand_off, const int* wave_slot, const int* wave_r, int U,
+                          int Mmax, const bf16* pool, const int* ptab, const int* vlen_all, const float* tau, bf16* O,
+                          int k, int l, const Dims& D, cudaStream_t s);
+void launch_attn_hist_mma(const bf16* Q, const int* wave_slot, const int* wave_r, int U, const bf16* pool,
+                          const int* ptab, const int* vlen_all, const float* tau, bf16* O, int k, int l, const Dims& D,
+                          cudaStream_t s);
 
 // tcgen05 GEMM (bf16 in, fp32 accumulate in TMEM), gemm_tc.cu.  Returns false
 // if the shape is not supported by the tensor-core kernel.
