@@ -59,9 +59,20 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// fast-math activations (MUFU ex2 + rcp): SiLU (G8), sigmoid (Eq. 4)
-__device__ __forceinline__ float silu_f(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
-__device__ __forceinline__ float sigmoid_f(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+// Activations with one MUFU op each: sigma(x) = 1/2 tanh(x/2) + 1/2, so
+// SiLU (G8) = x sigma(x) and the Eq. 4 gate use a single tanh.approx.f32
+// (max rel. error ~2^-11, below the bf16 rounding of the GEMM outputs).
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// bf16 path: one MUFU op; fp32 verification build: accurate expf.
+template <typename T> __device__ __forceinline__ float sigmoid_t(float x) {
+  return fmaf(0.5f, tanh_approx(0.5f * x), 0.5f);
+}
+template <> __device__ __forceinline__ float sigmoid_t<float>(float x) { return 1.0f / (1.0f + expf(-x)); }
+template <typename T> __device__ __forceinline__ float silu_t(float x) { return x * sigmoid_t<T>(x); }
 
 // SUMI visibility rule in canonical coordinates (G1,
 // G12, G14): slots 0..nk-1 are history (left-padded, valid iff >= nk - v),
@@ -88,10 +99,11 @@ enum EpiKind : int {
 };
 enum ActKind : int { ACT_NONE = 0, ACT_SILU = 1, ACT_RELU = 2, ACT_SIGMOID = 3 };
 
+template <typename T>
 __device__ __forceinline__ float apply_act(int act, float a) {
-  if (act == ACT_SILU) return silu_f(a);
+  if (act == ACT_SILU) return silu_t<T>(a);
   if (act == ACT_RELU) return fmaxf(a, 0.0f);
-  if (act == ACT_SIGMOID) return sigmoid_f(a);
+  if (act == ACT_SIGMOID) return sigmoid_t<T>(a);
   return a;
 }
 
@@ -129,7 +141,7 @@ __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, long long m, i
   if (e.kind == EPI_STORE) {
     float x[NC];
 #pragma unroll
-    for (int i = 0; i < NC; ++i) x[i] = apply_act(e.act, v[i] + (e.bias ? e.bias[n0 + i] : 0.0f));
+    for (int i = 0; i < NC; ++i) x[i] = apply_act<T>(e.act, v[i] + (e.bias ? e.bias[n0 + i] : 0.0f));
     T* o = reinterpret_cast<T*>(e.out) + m * e.ldo + n0;
     if constexpr (NC % 8 == 0) {
 #pragma unroll
@@ -145,7 +157,7 @@ __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, long long m, i
   } else if (e.kind == EPI_STORE_F32) {
     float* o = reinterpret_cast<float*>(e.out) + m * e.ldo + n0;
 #pragma unroll
-    for (int i = 0; i < NC; ++i) o[i] = apply_act(e.act, v[i] + (e.bias ? e.bias[n0 + i] : 0.0f));
+    for (int i = 0; i < NC; ++i) o[i] = apply_act<T>(e.act, v[i] + (e.bias ? e.bias[n0 + i] : 0.0f));
   } else {  // EPI_QKV_PAGES
     int c = n0 + e.col_off;
     if (c < e.d) {
@@ -173,12 +185,12 @@ __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, long long m, i
 template <typename T>
 __device__ __forceinline__ void epilogue_elem(const Epilogue& e, long long m, int n, float v) {
   if (e.kind == EPI_STORE) {
-    reinterpret_cast<T*>(e.out)[m * e.ldo + n] = from_f<T>(apply_act(e.act, v + (e.bias ? e.bias[n] : 0.0f)));
+    reinterpret_cast<T*>(e.out)[m * e.ldo + n] = from_f<T>(apply_act<T>(e.act, v + (e.bias ? e.bias[n] : 0.0f)));
   } else if (e.kind == EPI_RESID) {
     float* o = reinterpret_cast<float*>(e.out) + m * e.ldo + n;
     *o += v;
   } else if (e.kind == EPI_STORE_F32) {
-    reinterpret_cast<float*>(e.out)[m * e.ldo + n] = apply_act(e.act, v + (e.bias ? e.bias[n] : 0.0f));
+    reinterpret_cast<float*>(e.out)[m * e.ldo + n] = apply_act<T>(e.act, v + (e.bias ? e.bias[n] : 0.0f));
   } else {  // EPI_QKV_PAGES
     int c = n + e.col_off;
     if (c < e.d) {
