@@ -92,7 +92,7 @@ struct climber_ctx_s {
   std::vector<SlotState> slots;
   long long launches = 0;
   bool use_tc = true;
-  bool use_mma_attn = true;
+  int attn_mode = 2;  // bf16 attention: 2 tcgen05 (where supported), 1 mma.sync, 0 SIMT
   bool sync_check = false;
   // profiler
   bool prof = false;
@@ -308,7 +308,7 @@ extern "C" climber_status climber_create(const climber_config* cfg, const climbe
     const char* env = getenv("CLIMBER_GEMM");
     c->use_tc = !(env && strcmp(env, "simt") == 0);
     const char* ea = getenv("CLIMBER_ATTN");
-    c->use_mma_attn = !(ea && strcmp(ea, "simt") == 0);
+    c->attn_mode = (ea && strcmp(ea, "simt") == 0) ? 0 : (ea && strcmp(ea, "mma") == 0) ? 1 : 2;
     const char* sc = getenv("CLIMBER_SYNC_CHECK");
     c->sync_check = sc && atoi(sc) != 0;
 
@@ -493,7 +493,10 @@ static void encode_wave(climber_ctx_s* c, const EventsDev& ev, int u0, int U, lo
         {
           Prof p(c, CLIMBER_K_ATTN_HIST, s, 4.0 * U * causal_pairs * d, (double)rows * d * es * 4);
           if constexpr (std::is_same<T, bf16>::value) {
-            if (c->use_mma_attn) {
+            if (c->attn_mode == 2 && attn_tc_supported(D.dh, D.nk, true)) {
+              launch_attn_hist_tc(Qb, wslot, wr, U, (const T*)c->pool, c->n_pages * 2 * PAGE, c->ptab, c->vlen_all,
+                                  c->tau, O, k, l, D, s);
+            } else if (c->attn_mode >= 1) {
               launch_attn_hist_mma(Qb, wslot, wr, U, (const T*)c->pool, c->ptab, c->vlen_all, c->tau, O, k, l, D, s);
             } else {
               launch_attn_hist<T>(Qb, wslot, wr, U, (const T*)c->pool, c->ptab, c->vlen_all, c->tau, O, k, l, D, s);
@@ -555,7 +558,10 @@ static void score_wave(climber_ctx_s* c, const int32_t* items, const int64_t* wc
         Prof p(c, CLIMBER_K_ATTN_SUMI, s, 4.0 * P * (D.nk + 1) * d,
                (double)P * d * es * 4 + (double)U * D.nk * d * 2 * es);
         if constexpr (std::is_same<T, bf16>::value) {
-          if (c->use_mma_attn) {
+          if (c->attn_mode == 2 && attn_tc_supported(D.dh, D.nk, false)) {
+            launch_attn_sumi_tc(QKV, P, wcand, wslot, wr, U, Mmax_wave, (const T*)c->pool, c->n_pages * 2 * PAGE,
+                                c->ptab, c->vlen_all, c->tau, O, k, l, D, s);
+          } else if (c->attn_mode >= 1) {
             launch_attn_sumi_mma(QKV, wcand, wslot, wr, U, Mmax_wave, (const T*)c->pool, c->ptab, c->vlen_all, c->tau,
                                  O, k, l, D, s);
           } else {

@@ -1,0 +1,442 @@
+// tcgen05/TMEM attention for the bf16 path (Eq. 3 with f_b = 0;
+// SUMI masks P:L255): softmax(q.k / (sqrt(d_h) tau)) v.
+//
+//   MODE_SUMI: a tile of 128 candidates of one (user, head) attends to the v
+//              cached history keys of its (block, layer) plus itself.
+//   MODE_HIST: 128 history rows of one (user, head) attend keys j <= t
+//              (causal) or j < v (requires n_k % 128 == 0).
+//
+// CTA = 8 warps, one 128-row query tile (TMEM lane = query row); 2 CTAs/SM:
+//   warp 0   TMA: Q tile once; K and V of one 64-token page per chunk into a
+//            4-stage ring
+//   warp 1   MMA (one thread): S_j = Q K_j^T (M=128, N=64, K=d_h) into one of
+//            two TMEM score buffers, so QK^T of chunk j+1 overlaps the softmax
+//            of chunk j; O += P_j V_j (M=128, N=d_h, K=64) with P_j read from
+//            TMEM (it overwrites S_j in place as packed bf16), V MN-major
+//   warp 2   TMEM allocator (2 x 64 score columns + d_h output columns)
+//   warps 4-7 softmax, one thread per query row, two passes over its S row in
+//            TMEM (max, then exp2 -> packed bf16 P); lazy online max (O in TMEM
+//            is rescaled only when the row max grows by more than 2^8);
+//            epilogue O / l -> bf16 -> global.
+// The SUMI self term initialises the row state: m = s_self, l = 1, O = v_self
+// (tcgen05.st), so no candidate ever reads another candidate's K/V.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "kernels.cuh"
+#include "tc_util.cuh"
+
+namespace climber {
+namespace at {
+using namespace tcu;
+
+constexpr int ROWS = 128;
+constexpr int KEYS = PAGE;  // 64 keys per chunk = one K/V page
+constexpr int STAGES = 4;
+constexpr int THREADS = 256;
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float RESCALE_LOG2 = 8.0f;
+
+// 2^x on the MUFU (ex2.approx.ftz: -inf -> +0, no range fix-up instructions)
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+enum { MODE_SUMI = 0, MODE_HIST = 1 };
+
+template <int DH>
+struct Lay {
+  static constexpr int RB = DH * 2;                      // bytes per Q/K/V row (128 or 64)
+  static constexpr uint32_t SWZ = (DH == 64) ? 2u : 4u;  // descriptor swizzle: 128B / 64B
+  static constexpr int Q_OFF = 0;
+  static constexpr int Q_BYTES = ROWS * RB;
+  static constexpr int KVB = KEYS * RB;                  // one K (or V) page slice of one head
+  static constexpr int KV_OFF = Q_OFF + Q_BYTES;         // stage s: K at KV_OFF + 2 s KVB, V at + KVB
+  static constexpr int BAR_OFF = KV_OFF + 2 * STAGES * KVB;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+  static constexpr int STG_OFF = KV_OFF;                 // epilogue staging reuses the K/V ring
+};
+
+struct Args {
+  const bf16* Q;  // SUMI: QKV [P][3d] (q | k_self | v_self); HIST: Q [U*nk][d]
+  const int64_t* cand_off;
+  const int* wave_slot;
+  const int* wave_r;
+  const int* ptab;
+  const int* vlen_all;
+  const float* tau;
+  bf16* O;        // [rows][d]
+  int k, l;
+  Dims D;
+};
+
+template <int DH, int MODE>
+__global__ void __launch_bounds__(THREADS, 2)
+    k_attn_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, Args a) {
+  using Ly = Lay<DH>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Ly::BAR_OFF);
+  uint64_t* bar_q = bars + 0;
+  uint64_t* kv_full = bars + 1;                // [STAGES]
+  uint64_t* kv_empty = bars + 1 + STAGES;      // [STAGES]
+  // s_full / p_full are per score buffer: the softmax may run one chunk ahead
+  // of the MMA thread's p_full check, so a single barrier could advance two
+  // phases past a parity wait (ABA); one barrier per buffer cannot.
+  uint64_t* s_full = bars + 1 + 2 * STAGES;    // [2]
+  uint64_t* p_full = bars + 3 + 2 * STAGES;    // [2]
+  uint64_t* o_done = bars + 5 + 2 * STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 2 * STAGES);
+
+  const Dims& D = a.D;
+  const int u = blockIdx.z, head = blockIdx.y, tile0 = blockIdx.x * ROWS;  // tiles of one (u, h) adjacent
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = a.wave_slot[u];
+  const int r = a.wave_r[u];
+  const int v = a.vlen_all[(long long)slot * D.Nb + a.k];
+  const int* pages = a.ptab + (((long long)slot * D.Nb + a.k) * D.L + a.l) * D.ppb;
+  const float sc = LOG2E / (sqrtf((float)DH) * a.tau[((a.l * D.Nb + a.k) * D.R + r) * D.h + head]);
+
+  long long row_base;
+  int n_rows, key_end;
+  long long ldq;
+  if (MODE == MODE_SUMI) {
+    const long long p0 = a.cand_off[u], p1 = a.cand_off[u + 1];
+    if (p0 + tile0 >= p1) return;  // CTA-uniform
+    row_base = p0 + tile0;
+    n_rows = (int)((p1 - row_base) < ROWS ? (p1 - row_base) : ROWS);
+    key_end = v;
+    ldq = 3LL * D.d;
+  } else {
+    if (tile0 >= D.nk) return;
+    row_base = (long long)u * D.nk + tile0;
+    n_rows = max(0, min(ROWS, v - tile0));
+    key_end = D.causal ? min(v, tile0 + ROWS) : v;
+    ldq = D.d;
+  }
+  const int n_chunks = (key_end + KEYS - 1) / KEYS;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmQ) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmKV) : "memory");
+    mbar_init(bar_q, 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    mbar_init(&s_full[0], 1);
+    mbar_init(&s_full[1], 1);
+    mbar_init(&p_full[0], 128);
+    mbar_init(&p_full[1], 128);
+    mbar_init(o_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tO = tmem_base + 2 * KEYS;  // S/P buffers at tmem_base + b * KEYS
+
+  if (warp == 0) {
+    if (lane == 0 && n_chunks > 0) {
+      // ---------------- TMA producer ----------------
+      mbar_expect_tx(bar_q, Ly::Q_BYTES);
+      tma_load_2d(smem + Ly::Q_OFF, &tmQ, bar_q, head * DH, (int)row_base);
+      for (int j = 0; j < n_chunks; ++j) {
+        const int st = j % STAGES;
+        mbar_wait(&kv_empty[st], ((j / STAGES) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], 2 * Ly::KVB);
+        uint8_t* kd = smem + Ly::KV_OFF + 2 * st * Ly::KVB;
+        const int page = pages[j];
+        tma_load_2d(kd, &tmKV, &kv_full[st], head * DH, (int)page_row(page, 0, 0));
+        tma_load_2d(kd + Ly::KVB, &tmKV, &kv_full[st], head * DH, (int)page_row(page, 1, 0));
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && n_chunks > 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t idesc_qk = idesc_bf16_major(ROWS, KEYS, 0, 0);
+      constexpr uint32_t idesc_pv = idesc_bf16_major(ROWS, DH, 0, 1);
+      const uint64_t qd = make_sdesc(smem_u32(smem + Ly::Q_OFF), 16, 8 * Ly::RB, Ly::SWZ);
+      mbar_wait(bar_q, 0);
+      auto issue_qk = [&](int j) {
+        const int st = j % STAGES;
+        mbar_wait(&kv_full[st], (j / STAGES) & 1);
+        fence_after();
+        const uint64_t kd = make_sdesc(smem_u32(smem + Ly::KV_OFF + 2 * st * Ly::KVB), 16, 8 * Ly::RB, Ly::SWZ);
+        const uint32_t tSj = tmem_base + (j & 1) * KEYS;
+#pragma unroll
+        for (int s = 0; s < DH / 16; ++s) mma_bf16(tSj, qd + 2 * s, kd + 2 * s, idesc_qk, s > 0 ? 1u : 0u);
+        mma_commit(&s_full[j & 1]);
+      };
+      issue_qk(0);
+      for (int j = 0; j < n_chunks; ++j) {
+        const int st = j % STAGES;
+        if (j + 1 < n_chunks) {
+          if (j >= 1) mbar_wait(o_done, (j - 1) & 1);  // PV(j-1) consumed P_{j-1} = buffer (j+1) & 1
+          issue_qk(j + 1);
+        }
+        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+        fence_after();
+        const uint64_t vd = make_sdesc(smem_u32(smem + Ly::KV_OFF + 2 * st * Ly::KVB + Ly::KVB), 16, 8 * Ly::RB,
+                                       Ly::SWZ);
+        const uint32_t tPj = tmem_base + (j & 1) * KEYS;
+#pragma unroll
+        for (int s = 0; s < KEYS / 16; ++s) {
+          const uint64_t vds = vd + (uint64_t)((16 * Ly::RB) >> 4) * s;  // 16 keys = 2 groups of 8 rows
+          const uint32_t acc = (MODE == MODE_SUMI || j > 0 || s > 0) ? 1u : 0u;
+          mma_bf16_ts(tO, tPj + 8 * s, vds, idesc_pv, acc);  // 16 keys of P = 8 packed columns
+        }
+        mma_commit(o_done);
+        mma_commit(&kv_empty[st]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- softmax + epilogue ----------------
+    const int ew = warp - 4;
+    const int row = ew * 32 + lane;  // query row = TMEM lane
+    const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
+    const bool valid = row < n_rows;
+    const long long grow = row_base + row;
+    const int t_row = tile0 + row;
+    float m_used, l;
+    if (MODE == MODE_SUMI) {
+      const bf16* qp = a.Q + grow * ldq + head * DH;
+      float ss = 0.f;
+      if (valid) {
+#pragma unroll
+        for (int c = 0; c < DH; c += 8) {
+          float q[8], kk[8];
+          load8(qp + c, q);
+          load8(qp + D.d + c, kk);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) ss = fmaf(q[i], kk[i], ss);
+        }
+      }
+      m_used = ss * sc;
+      l = 1.f;
+#pragma unroll
+      for (int c = 0; c < DH; c += 32) {  // O = v_self
+        float vs[32];
+#pragma unroll
+        for (int cc = 0; cc < 32; cc += 8) {
+          if (valid) {
+            load8(qp + 2 * D.d + c + cc, vs + cc);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) vs[cc + i] = 0.f;
+          }
+        }
+        tmem_st32(tO + lane_off + c, vs);
+      }
+    } else {
+      m_used = -INFINITY;
+      l = 0.f;
+    }
+    const bool causal_hist = (MODE == MODE_HIST) && D.causal;
+    for (int j = 0; j < n_chunks; ++j) {
+      const uint32_t tSj = tmem_base + (j & 1) * KEYS + lane_off;
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      fence_after();
+      const int key0 = j * KEYS;
+      int lim = key_end - key0;  // keys [0, lim) of the chunk are visible to this row
+      if (causal_hist) lim = min(lim, t_row - key0 + 1);
+      // pass 1: row max of the raw scores (8 independent partials)
+      uint32_t sr[KEYS];
+      tmem_ld32_nw(tSj, sr);
+      tmem_ld32_nw(tSj + 32, sr + 32);
+      tmem_ld_wait();
+      float mx8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
+      const bool full = lim >= KEYS;  // no masking in full chunks (the common case)
+      if (full) {
+#pragma unroll
+        for (int i = 0; i < KEYS; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(sr[i]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < KEYS; ++i)
+          if (i < lim) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(sr[i]));
+      }
+      const float mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      const float mx = mraw * sc;  // sc > 0
+      // lazy rescale: per row, only when its max grew by > 2^8; the TMEM
+      // ld/st are warp-collective (.sync.aligned), so the warp decides together
+      const bool mine = mx > m_used + RESCALE_LOG2;
+      const float alpha = mine ? exp2f(m_used - mx) : 1.f;  // m_used = -inf -> 0
+      if (mine) {
+        l *= alpha;
+        m_used = mx;
+      }
+      if ((MODE == MODE_SUMI || j > 0) && __any_sync(0xffffffffu, mine)) {
+        if (j > 0) mbar_wait(o_done, (j - 1) & 1);  // PV(j-1) finished writing O
+        fence_after();
+#pragma unroll
+        for (int c = 0; c < DH; c += 32) {
+          float o[32];
+          tmem_ld32(tO + lane_off + c, o);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] *= alpha;
+          tmem_st32(tO + lane_off + c, o);
+        }
+      }
+      // pass 2: P = exp2(s sc - m) as packed bf16, written over S_j in TMEM
+      const float nb = (m_used == -INFINITY) ? 0.f : -m_used;
+      float ls8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      uint32_t pk[KEYS / 2];
+      if (full) {
+#pragma unroll
+        for (int i = 0; i < KEYS; i += 2) {
+          const float e0 = ex2_approx(fmaf(__uint_as_float(sr[i]), sc, nb));
+          const float e1 = ex2_approx(fmaf(__uint_as_float(sr[i + 1]), sc, nb));
+          ls8[i & 7] += e0;
+          ls8[(i + 1) & 7] += e1;
+          __nv_bfloat162 pp = __floats2bfloat162_rn(e0, e1);
+          pk[i >> 1] = *reinterpret_cast<uint32_t*>(&pp);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < KEYS; i += 2) {
+          const float e0 = (i < lim) ? ex2_approx(fmaf(__uint_as_float(sr[i]), sc, nb)) : 0.f;
+          const float e1 = (i + 1 < lim) ? ex2_approx(fmaf(__uint_as_float(sr[i + 1]), sc, nb)) : 0.f;
+          ls8[i & 7] += e0;
+          ls8[(i + 1) & 7] += e1;
+          __nv_bfloat162 pp = __floats2bfloat162_rn(e0, e1);
+          pk[i >> 1] = *reinterpret_cast<uint32_t*>(&pp);
+        }
+      }
+      tmem_st16u(tSj, pk);
+      tmem_st16u(tSj + 16, pk + 16);
+      tmem_st_wait();
+      l += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
+      fence_before();
+      mbar_arrive(&p_full[j & 1]);
+    }
+    // ---- epilogue: O / l -> bf16, staged in smem for coalesced stores
+    if (n_chunks > 0) {
+      mbar_wait(o_done, (n_chunks - 1) & 1);
+      fence_after();
+    }
+    const float inv = (valid && l > 0.f) ? 1.f / l : 0.f;
+    constexpr int LDS = DH + 8;
+    bf16* stg = reinterpret_cast<bf16*>(smem + Ly::STG_OFF);  // K/V ring fully consumed (last PV done)
+#pragma unroll
+    for (int c = 0; c < DH; c += 32) {
+      float o[32];
+      if (MODE == MODE_SUMI || n_chunks > 0) {
+        tmem_ld32(tO + lane_off + c, o);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] = 0.f;
+      }
+#pragma unroll
+      for (int cc = 0; cc < 32; cc += 8) {
+        float y[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[i] = o[cc + i] * inv;
+        store8(stg + row * LDS + c + cc, y);
+      }
+    }
+    __syncwarp();
+    const int rows_out = (MODE == MODE_SUMI) ? n_rows : min(ROWS, D.nk - tile0);
+    constexpr int LPR = DH / 2;  // lanes per row, 2 bf16 each
+#pragma unroll 4
+    for (int i = 0; i < 32; i += 32 / LPR) {
+      const int rr = ew * 32 + i + lane / LPR;
+      const int cc = (lane % LPR) * 2;
+      if (rr < rows_out) {
+        const uint32_t val = *reinterpret_cast<const uint32_t*>(stg + rr * LDS + cc);
+        *reinterpret_cast<uint32_t*>(a.O + (row_base + rr) * D.d + head * DH + cc) = val;
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 map: [rows][cols] with row stride ld, box {box_cols, box_rows}, swizzle = box row bytes
+static bool map2d(CUtensorMap* m, const void* base, long long rows, int cols, long long ld, int box_cols,
+                  int box_rows) {
+  auto enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMapSwizzle sw = box_cols * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int DH, int MODE>
+static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s) {
+  constexpr int smem = Lay<DH>::TOTAL;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_attn_tc<DH, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  k_attn_tc<DH, MODE><<<grid, THREADS, smem, s>>>(mq, mkv, a);
+}
+
+}  // namespace at
+
+bool attn_tc_supported(int dh, int nk, bool hist) {
+  if (dh != 32 && dh != 64) return false;
+  if (hist && nk % at::ROWS) return false;
+  return at::encoder() != nullptr;
+}
+
+void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, const int* wave_slot,
+                         const int* wave_r, int U, int Mmax, const bf16* pool, long long pool_rows, const int* ptab,
+                         const int* vlen_all, const float* tau, bf16* O, int k, int l, const Dims& D, cudaStream_t s) {
+  CUtensorMap mq, mkv;
+  at::map2d(&mq, QKV, P, 3 * D.d, 3LL * D.d, D.dh, at::ROWS);
+  at::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, at::KEYS);
+  at::Args a{QKV, cand_off, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, D};
+  dim3 grid((Mmax + at::ROWS - 1) / at::ROWS, D.h, U);
+  if (D.dh == 64) at::launch<64, at::MODE_SUMI>(mq, mkv, a, grid, s);
+  else at::launch<32, at::MODE_SUMI>(mq, mkv, a, grid, s);
+}
+
+void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r, int U, const bf16* pool,
+                         long long pool_rows, const int* ptab, const int* vlen_all, const float* tau, bf16* O, int k,
+                         int l, const Dims& D, cudaStream_t s) {
+  CUtensorMap mq, mkv;
+  at::map2d(&mq, Q, (long long)U * D.nk, D.d, D.d, D.dh, at::ROWS);
+  at::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, at::KEYS);
+  at::Args a{Q, nullptr, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, D};
+  dim3 grid(D.nk / at::ROWS, D.h, U);
+  if (D.dh == 64) at::launch<64, at::MODE_HIST>(mq, mkv, a, grid, s);
+  else at::launch<32, at::MODE_HIST>(mq, mkv, a, grid, s);
+}
+
+}  // namespace climber
