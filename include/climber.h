@@ -234,13 +234,15 @@ climber_status climber_debug_mask(climber_ctx_t ctx, climber_kv_t kv, int32_t M,
 climber_status climber_debug_kv(climber_ctx_t ctx, climber_kv_t kv, int32_t layer, int32_t block,
                                 void* K, void* V);
 
-/* The bf16 tensor-core GEMM of the path in isolation: D[m][n] += sum_k
- * A[m][k] * B[n][k] (fp32 accumulate, fp32 residual-add epilogue).  DEVICE
- * pointers: A bf16 [M][K], B bf16 [N][K], D float [M][N]; K % 64 == 0,
- * N % 128 == 0 (else E_UNSUPPORTED).  use_tc = 0 runs the SIMT kernel.
- * Asynchronous on `stream`. */
-climber_status climber_debug_gemm(const void* A, const void* B, float* D, int64_t M, int32_t N, int32_t K,
-                                  int32_t use_tc, climber_stream_t stream);
+/* The bf16 tensor-core GEMM of the path in isolation, C = sum_k A[m][k] B[n][k]
+ * (fp32 accumulate) with one of the path's epilogues:
+ *   epi 0: D float [M][N]  += C        (residual add)
+ *   epi 1: D bf16  [M][N]   = C        (plain store)
+ *   epi 2: D bf16  [M][N]   = SiLU(C)  (FFN up)
+ * DEVICE pointers: A bf16 [M][K], B bf16 [N][K]; K % 64 == 0, N % 128 == 0
+ * (else E_UNSUPPORTED).  use_tc = 0 runs the SIMT kernel.  Asynchronous. */
+climber_status climber_debug_gemm(const void* A, const void* B, void* D, int64_t M, int32_t N, int32_t K,
+                                  int32_t use_tc, int32_t epi, climber_stream_t stream);
 
 /* ---- measurement (bench evidence) ---- */
 

@@ -82,7 +82,7 @@ def lib() -> C.CDLL:
             "climber_debug_mask": (I32, [VP, VP, I32, P]),
             "climber_debug_kv": (I32, [VP, VP, I32, I32, P, P]),
             "climber_launch_count": (I64, [VP]),
-            "climber_debug_gemm": (I32, [VP, VP, VP, I64, I32, I32, I32, VP]),
+            "climber_debug_gemm": (I32, [VP, VP, VP, I64, I32, I32, I32, I32, VP]),
             "climber_profile": (I32, [VP, I32]),
             "climber_profile_read": (I32, [VP, P]),
         }
@@ -109,14 +109,15 @@ def _check(st: int):
         raise ClimberError(st, lib().climber_last_error().decode())
 
 
-def debug_gemm(A, B, D, use_tc: bool = True, stream=None):
-    """D += A @ B^T with the library's bf16 GEMM (A [M][K], B [N][K] bf16, D fp32; CUDA tensors)."""
+def debug_gemm(A, B, D, use_tc: bool = True, stream=None, epi: int = 0):
+    """The library's bf16 GEMM C = A @ B^T (A [M][K], B [N][K] bf16; CUDA tensors):
+    epi 0: D(fp32) += C; epi 1: D(bf16) = C; epi 2: D(bf16) = SiLU(C)."""
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     M, K = A.shape
     N = B.shape[0]
     _check(lib().climber_debug_gemm(C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), C.c_void_p(D.data_ptr()),
-                                    M, N, K, int(use_tc), C.c_void_p(s.cuda_stream)))
+                                    M, N, K, int(use_tc), int(epi), C.c_void_p(s.cuda_stream)))
 
 
 def _ptr(a: np.ndarray):

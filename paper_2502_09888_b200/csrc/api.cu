@@ -975,12 +975,13 @@ extern "C" climber_status climber_debug_kv(climber_ctx_t c, climber_kv_t kv, int
   return CLIMBER_OK;
 }
 
-extern "C" climber_status climber_debug_gemm(const void* A, const void* B, float* D, int64_t M, int32_t N, int32_t K,
-                                             int32_t use_tc, climber_stream_t stream) {
-  if (!A || !B || !D || M < 1 || N < 1 || K < 1) return fail(CLIMBER_E_INVALID_ARG, "bad argument");
+extern "C" climber_status climber_debug_gemm(const void* A, const void* B, void* D, int64_t M, int32_t N, int32_t K,
+                                             int32_t use_tc, int32_t epi, climber_stream_t stream) {
+  if (!A || !B || !D || M < 1 || N < 1 || K < 1 || epi < 0 || epi > 2)
+    return fail(CLIMBER_E_INVALID_ARG, "bad argument");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  Epilogue e{};
-  e.kind = EPI_RESID; e.out = D; e.ldo = N;
+  Epilogue e = epi == 0 ? epi_resid(reinterpret_cast<float*>(D), N)
+                        : epi_store(D, N, epi == 2 ? ACT_SILU : ACT_NONE);
   if (use_tc) {
     if (!gemm_tc_supported(M, N, K, K, K)) return fail(CLIMBER_E_UNSUPPORTED, "shape not supported by tcgen05 GEMM");
     launch_gemm_tc((const bf16*)A, K, (const bf16*)B, K, M, N, K, e, s);

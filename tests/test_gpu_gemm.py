@@ -23,3 +23,22 @@ def test_gemm_vs_fp64(M, N, K, use_tc):
     err = (D.cpu().double() - ref).abs().max().item()
     bound = K * 2.0 ** -22 * 16  # |a|,|b| ~ N(0,1): generous fp32-accumulation bound
     assert err < bound, (err, bound)
+
+
+@pytest.mark.parametrize("epi", [1, 2])
+@pytest.mark.parametrize("M,N,K", [(300, 256, 512), (4096, 2048, 512), (77, 384, 128)])
+def test_gemm_store_epilogues(M, N, K, epi):
+    import torch
+    import torch.nn.functional as F
+    from paper_2502_09888_b200.climber import debug_gemm
+    g = torch.Generator().manual_seed(M + N + K + epi)
+    A = torch.randn(M, K, generator=g).bfloat16()
+    B = (torch.randn(N, K, generator=g) / K ** 0.5).bfloat16()
+    D = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    debug_gemm(A.cuda(), B.cuda(), D, epi=epi)
+    torch.cuda.synchronize()
+    ref = A.double() @ B.double().T
+    if epi == 2:
+        ref = F.silu(ref)
+    err = (D.cpu().double() - ref).abs().max().item()
+    assert err < 2e-2 * max(1.0, ref.abs().max().item()), err

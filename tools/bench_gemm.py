@@ -10,17 +10,18 @@ shapes = [(65536, 1536, 512), (65536, 512, 512), (65536, 2048, 512), (65536, 512
 if len(sys.argv) > 1:
     shapes = [tuple(int(x) for x in sys.argv[1].split(","))]
 reps = int(os.environ.get("REPS", "20"))
+EPI = int(os.environ.get("EPI", "0"))
 for M, N, K in shapes:
     A = torch.randn(M, K, device="cuda").bfloat16()
     B = torch.randn(N, K, device="cuda").bfloat16()
-    D = torch.zeros(M, N, device="cuda")
+    D = torch.zeros(M, N, device="cuda") if EPI == 0 else torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
     for _ in range(3):
-        debug_gemm(A, B, D)
+        debug_gemm(A, B, D, epi=EPI)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
-        debug_gemm(A, B, D)
+        debug_gemm(A, B, D, epi=EPI)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
@@ -31,5 +32,5 @@ for M, N, K in shapes:
     t1.record()
     torch.cuda.synchronize()
     ms_t = t0.elapsed_time(t1) / reps
-    print(json.dumps({"M": M, "N": N, "K": K, "ms": ms, "tflops": 2 * M * N * K / ms / 1e9,
+    print(json.dumps({"epi": EPI, "M": M, "N": N, "K": K, "ms": ms, "tflops": 2 * M * N * K / ms / 1e9,
                       "torch_bf16_out_tflops": 2 * M * N * K / ms_t / 1e9}), flush=True)
