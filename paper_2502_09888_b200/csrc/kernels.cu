@@ -391,58 +391,113 @@ __global__ void __launch_bounds__(128) k_attn_hist(const T* __restrict__ Q, cons
 
 // a5 fusion ATL attention (G16): the N_b tokens of one pair
 // attend to each other (full visibility), temperature tau_f[r][head].
-// Thread per (pair, token, head).
+// One warp per (pair, head): 4 lanes per token (N_b <= 8), each lane owns
+// d_h/4 dimensions of its token's q, k, v; K and V of the pair are staged in
+// shared memory, scores are reduced over the 4 lanes with two shuffles.
+// Memory: one read of the pair's Q, K, V head slices, one write of O.
 template <typename T, int DH>
-__global__ void k_attn_fusion(const T* __restrict__ QKV, const int64_t* __restrict__ cand_off,
-                              const int* __restrict__ wave_r, int U, long long P,
-                              const float* __restrict__ tau_f, T* __restrict__ O, Dims D) {
-  long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long total = P * D.Nb * D.h;
-  if (g >= total) return;
-  int head = (int)(g % D.h);
-  long long tok = g / D.h;          // = p * Nb + i
-  long long p = tok / D.Nb;
-  int u = pair_user(cand_off, U, p);
-  int r = wave_r[u];
+__global__ void __launch_bounds__(256) k_attn_fusion(const T* __restrict__ QKV, const int64_t* __restrict__ cand_off,
+                                                     const int* __restrict__ wave_r, int U, long long P,
+                                                     const float* __restrict__ tau_f, T* __restrict__ O, Dims D) {
+  constexpr int PD = DH / 4;      // dims per lane (4, 8 or 16)
+  constexpr int SEG = PD + 4;     // smem segment stride: the 4 parts land in distinct banks
+  __shared__ __align__(16) float Ks[8][8][4 * SEG];
+  __shared__ __align__(16) float Vs[8][8][4 * SEG];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long gw = (long long)blockIdx.x * 8 + wib;  // (pair, head)
+  if (gw >= P * D.h) return;
+  const int head = (int)(gw % D.h);
+  const long long p = gw / D.h;
+  const int tok = lane >> 2, part = lane & 3;
+  const bool act = tok < D.Nb;
+  const int u = pair_user(cand_off, U, p);
+  const int r = wave_r[u];
   const float sc = LOG2E / (sqrtf((float)DH) * tau_f[r * D.h + head]);
   const long long ld = 3LL * D.d;
-  float q[DH], o[DH];
+  const T* row = QKV + (p * D.Nb + (act ? tok : 0)) * ld + head * DH + part * PD;
+  float q[PD];
+  float* ks = &Ks[wib][tok][part * SEG];
+  float* vs = &Vs[wib][tok][part * SEG];
 #pragma unroll
-  for (int c = 0; c < DH; c += 8) load8(QKV + tok * ld + head * DH + c, q + c);
+  for (int c = 0; c < PD; c += 4) {
+    float x[8], y[8], z[8];
+    if (PD >= 8 && c % 8 == 0) {
+      if (act) {
+        load8(row + c, x);
+        load8(row + D.d + c, y);
+        load8(row + 2 * D.d + c, z);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = y[i] = z[i] = 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) q[c + i] = x[i] * sc;
+      *reinterpret_cast<float4*>(ks + c) = make_float4(y[0], y[1], y[2], y[3]);
+      *reinterpret_cast<float4*>(ks + c + 4) = make_float4(y[4], y[5], y[6], y[7]);
+      *reinterpret_cast<float4*>(vs + c) = make_float4(z[0], z[1], z[2], z[3]);
+      *reinterpret_cast<float4*>(vs + c + 4) = make_float4(z[4], z[5], z[6], z[7]);
+    } else if (PD < 8) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        q[c + i] = act ? to_f(row[c + i]) * sc : 0.f;
+        ks[c + i] = act ? to_f(row[D.d + c + i]) : 0.f;
+        vs[c + i] = act ? to_f(row[2 * D.d + c + i]) : 0.f;
+      }
+    }
+  }
+  __syncwarp();
   float s[8];
   float mx = -INFINITY;
-  for (int j = 0; j < D.Nb; ++j) {
-    float kk[DH];
-    const T* kr = QKV + (p * D.Nb + j) * ld + D.d + head * DH;
 #pragma unroll
-    for (int c = 0; c < DH; c += 8) load8(kr + c, kk + c);
+  for (int j = 0; j < 8; ++j) {
+    const float* kj = &Ks[wib][j][part * SEG];
     float acc = 0.f;
 #pragma unroll
-    for (int c = 0; c < DH; ++c) acc = fmaf(q[c], kk[c], acc);
-    s[j] = acc * sc;
+    for (int c = 0; c < PD; c += 4) {
+      const float4 k4 = *reinterpret_cast<const float4*>(kj + c);
+      acc = fmaf(q[c], k4.x, fmaf(q[c + 1], k4.y, fmaf(q[c + 2], k4.z, fmaf(q[c + 3], k4.w, acc))));
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    s[j] = (j < D.Nb) ? acc : -INFINITY;
     mx = fmaxf(mx, s[j]);
   }
+  float l = 0.f;
 #pragma unroll
-  for (int c = 0; c < DH; ++c) o[c] = 0.f;
-  float lsum = 0.f;
-  for (int j = 0; j < D.Nb; ++j) {
-    float pj = exp2f(s[j] - mx);
-    lsum += pj;
-    float vv[DH];
-    const T* vr = QKV + (p * D.Nb + j) * ld + 2 * D.d + head * DH;
-#pragma unroll
-    for (int c = 0; c < DH; c += 8) load8(vr + c, vv + c);
-#pragma unroll
-    for (int c = 0; c < DH; ++c) o[c] = fmaf(pj, vv[c], o[c]);
+  for (int j = 0; j < 8; ++j) {
+    s[j] = (j < D.Nb) ? exp2f(s[j] - mx) : 0.f;
+    l += s[j];
   }
-  float inv = 1.f / lsum;
-  T* out = O + tok * D.d + head * DH;
+  const float inv = 1.f / l;
+  float o[PD];
 #pragma unroll
-  for (int c = 0; c < DH; c += 8) {
-    float y[8];
+  for (int c = 0; c < PD; ++c) o[c] = 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) y[i] = o[c + i] * inv;
-    store8(out + c, y);
+  for (int j = 0; j < 8; ++j) {
+    const float* vj = &Vs[wib][j][part * SEG];
+#pragma unroll
+    for (int c = 0; c < PD; c += 4) {
+      const float4 v4 = *reinterpret_cast<const float4*>(vj + c);
+      o[c] = fmaf(s[j], v4.x, o[c]);
+      o[c + 1] = fmaf(s[j], v4.y, o[c + 1]);
+      o[c + 2] = fmaf(s[j], v4.z, o[c + 2]);
+      o[c + 3] = fmaf(s[j], v4.w, o[c + 3]);
+    }
+  }
+  if (act) {
+    T* out = O + (p * D.Nb + tok) * D.d + head * DH + part * PD;
+    if constexpr (PD % 8 == 0) {
+#pragma unroll
+      for (int c = 0; c < PD; c += 8) {
+        float y[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[i] = o[c + i] * inv;
+        store8(out + c, y);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < PD; ++c) out[c] = from_f<T>(o[c] * inv);
+    }
   }
 }
 
@@ -609,9 +664,9 @@ void launch_attn_hist(const T* Q, const int* wave_slot, const int* wave_r, int U
 template <typename T>
 void launch_attn_fusion(const T* QKV, const int64_t* cand_off, const int* wave_r, int U, long long P,
                         const float* tau_f, T* O, const Dims& D, cudaStream_t s) {
-  long long n = P * D.Nb * D.h;
-  unsigned g = blocks_for(n, 128);
-#define CL_FUS(DH) k_attn_fusion<T, DH><<<g, 128, 0, s>>>(QKV, cand_off, wave_r, U, P, tau_f, O, D)
+  long long n = P * D.h;  // warps
+  unsigned g = blocks_for(n, 8);
+#define CL_FUS(DH) k_attn_fusion<T, DH><<<g, 256, 0, s>>>(QKV, cand_off, wave_r, U, P, tau_f, O, D)
   if (D.dh == 16) CL_FUS(16);
   else if (D.dh == 32) CL_FUS(32);
   else CL_FUS(64);
