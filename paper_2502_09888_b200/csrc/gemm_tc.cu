@@ -16,6 +16,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.cuh"
@@ -27,25 +28,26 @@ using namespace tcu;
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B rows = one SWIZZLE_128B atom width
-constexpr int NUM_THREADS = 256;
 
-template <int BN, int STAGES>
+
+template <int BN, int STAGES, int EPIW, int SBUF>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STG_OFF = STAGES * STAGE_BYTES;  // epilogue staging: 4 warps x 2 x (32 rows x 128 B)
-  static constexpr int STG_WARP = 2 * 32 * 128;
-  static constexpr int BAR_OFF = STG_OFF + 4 * STG_WARP;
+  static constexpr int STG_WARP = SBUF * 32 * 128;
+  static constexpr int BAR_OFF = STG_OFF + EPIW * STG_WARP;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + tmem addr, + alignment slack
 };
 
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+// EPIW epilogue warps (4 or 8), SBUF staging buffers per epilogue warp (1 or 2)
+template <int BN, int STAGES, int EPIW, int SBUF>
+__global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmP, long long M, int N,
               int K, Epilogue e) {
-  using S = Smem<BN, STAGES>;
+  using S = Smem<BN, STAGES, EPIW, SBUF>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
@@ -71,7 +73,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 32 * EPIW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -140,8 +142,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // TMA store of 32 token rows straight into the user's K/V page (the 32-row
     // group lies in one user and one page since n_k % 32 == 0).
     // Otherwise: transpose through smem, lane = column, coalesced page stores.
-    const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31
-    uint8_t* stg = smem + S::STG_OFF + ew * S::STG_WARP;
+    // 8 warps: warp w reads TMEM lane quadrant w % 4 (hardware rule), the two
+    // warps of a quadrant split the tile's columns in halves
+    const int ew = warp & 3;             // TMEM lanes 32*ew .. 32*ew+31
+    constexpr int NCG = EPIW / 4;        // column groups
+    const int cg = (warp - 4) >> 2;      // this warp's column group
+    uint8_t* stg = smem + S::STG_OFF + (warp - 4) * S::STG_WARP;
     const bool tma_epi = e.kind != EPI_QKV_PAGES || (e.d % 64 == 0);
     const bool f32_out = e.kind == EPI_RESID || e.kind == EPI_STORE_F32;
     const int CW = f32_out ? 32 : 64;  // columns per 128-byte staged row
@@ -156,7 +162,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
       if (tma_epi) {
 #pragma unroll 1
-        for (int c = 0; c < BN; c += CW) {
+        for (int c = cg * (BN / NCG); c < (cg + 1) * (BN / NCG); c += CW) {
           float v[64];
           tmem_ld32(taddr + c, v);  // lane = row row0 + lane
           if (!f32_out) tmem_ld32(taddr + c + 32, v + 32);
@@ -167,7 +173,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if (i < CW) v[i] = apply_act<bf16>(e.act, v[i] + (e.bias ? e.bias[n0 + i] : 0.0f));
           }
           uint8_t* buf = stg + sbuf * 4096;
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          if (lane == 0) {
+            if (SBUF == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
           __syncwarp();
           uint8_t* rowp = buf + lane * 128;
           if (f32_out) {
@@ -209,12 +218,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
-          sbuf ^= 1;
+          sbuf = (SBUF == 2) ? (sbuf ^ 1) : 0;
         }
       } else {
         float (*tr)[33] = reinterpret_cast<float (*)[33]>(stg);
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = cg * (BN / NCG); c < (cg + 1) * (BN / NCG); c += 32) {
           float v[32];
           tmem_ld32(taddr + c, v);
 #pragma unroll
@@ -284,7 +293,7 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int EPIW, int SBUF>
 static void launch(const bf16* A, long long lda, const bf16* B, long long ldb, long long M, int N, int K,
                    const Epilogue& e, cudaStream_t s) {
   CUtensorMap ma, mb, md, mp;
@@ -303,15 +312,16 @@ static void launch(const bf16* A, long long lda, const bf16* B, long long ldb, l
   } else {
     make_map(&md, e.out, M, N, e.ldo, 32, 32, true);
   }
-  constexpr int smem = Smem<BN, STAGES>::TOTAL;
+  constexpr int smem = Smem<BN, STAGES, EPIW, SBUF>::TOTAL;
+  static_assert(smem <= 232448, "smem");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm_tc<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, EPIW, SBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
   long long tiles = ((M + BM - 1) / BM) * (N / BN);
   int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  k_gemm_tc<BN, STAGES><<<grid, NUM_THREADS, smem, s>>>(ma, mb, md, mp, M, N, K, e);
+  k_gemm_tc<BN, STAGES, EPIW, SBUF><<<grid, 128 + 32 * EPIW, smem, s>>>(ma, mb, md, mp, M, N, K, e);
 }
 
 }  // namespace tc
@@ -324,8 +334,26 @@ bool gemm_tc_supported(long long M, int N, int K, long long lda, long long ldb) 
 
 void launch_gemm_tc(const bf16* A, long long lda, const bf16* B, long long ldb, long long M, int N, int K,
                     const Epilogue& e, cudaStream_t s) {
-  if (N % 256 == 0) tc::launch<256, 4>(A, lda, B, ldb, M, N, K, e, s);
-  else tc::launch<128, 6>(A, lda, B, ldb, M, N, K, e, s);
+  // Variant per epilogue cost (measured with tools/bench_gemm.py on B200):
+  //   1: 4 epilogue warps, 4 stages, double-buffered staging (plain store, residual)
+  //   2: 8 epilogue warps, 3 stages, double-buffered staging
+  //   3: 8 epilogue warps, 4 stages, single staging buffer (SiLU / sigmoid:
+  //      MUFU-heavy epilogues need 8 warps to keep up with the MMA)
+  static int forced = -1;
+  if (forced < 0) {
+    const char* v = getenv("CLIMBER_GEMM_VARIANT");
+    forced = v ? atoi(v) : 0;
+  }
+  const bool heavy = (e.kind == EPI_STORE || e.kind == EPI_STORE_F32) && e.act != ACT_NONE;
+  int var = forced ? forced : (heavy ? 3 : 1);
+  if (N % 256 == 0) {
+    if (var == 1) tc::launch<256, 4, 4, 2>(A, lda, B, ldb, M, N, K, e, s);
+    else if (var == 2) tc::launch<256, 3, 8, 2>(A, lda, B, ldb, M, N, K, e, s);
+    else tc::launch<256, 4, 8, 1>(A, lda, B, ldb, M, N, K, e, s);
+  } else {
+    if (var == 1) tc::launch<128, 6, 4, 2>(A, lda, B, ldb, M, N, K, e, s);
+    else tc::launch<128, 5, 8, 2>(A, lda, B, ldb, M, N, K, e, s);
+  }
 }
 
 }  // namespace climber
