@@ -10,10 +10,11 @@
 //   warp 0   TMA: Q tile once; K and V of one 64-token page per chunk into a
 //            4-stage ring
 //   warp 1   MMA (one thread): S_j = Q K_j^T (M=128, N=64, K=d_h) into one of
-//            two TMEM score buffers, so QK^T of chunk j+1 overlaps the softmax
-//            of chunk j; O += P_j V_j (M=128, N=d_h, K=64) with P_j read from
-//            TMEM (it overwrites S_j in place as packed bf16), V MN-major
-//   warp 2   TMEM allocator (2 x 64 score columns + d_h output columns)
+//            three TMEM score buffers, so QK^T of chunk j+1 only waits for
+//            PV of chunk j-2 and overlaps the softmax of chunk j; O += P_j V_j
+//            (M=128, N=d_h, K=64) with P_j read from TMEM (it overwrites S_j in
+//            place as packed bf16), V MN-major
+//   warp 2   TMEM allocator (3 x 64 score columns + d_h output columns = 256)
 //   warps 4-7 softmax, one thread per query row, two passes over its S row in
 //            TMEM (max, then exp2 -> packed bf16 P); lazy online max (O in TMEM
 //            is rescaled only when the row max grows by more than 2^8);
@@ -35,6 +36,7 @@ using namespace tcu;
 constexpr int ROWS = 128;
 constexpr int KEYS = PAGE;  // 64 keys per chunk = one K/V page
 constexpr int STAGES = 4;
+constexpr int NSB = 3;      // TMEM score/P buffers
 constexpr int THREADS = 256;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float RESCALE_LOG2 = 8.0f;
@@ -57,7 +59,7 @@ struct Lay {
   static constexpr int KVB = KEYS * RB;                  // one K (or V) page slice of one head
   static constexpr int KV_OFF = Q_OFF + Q_BYTES;         // stage s: K at KV_OFF + 2 s KVB, V at + KVB
   static constexpr int BAR_OFF = KV_OFF + 2 * STAGES * KVB;
-  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+  static constexpr int TOTAL = BAR_OFF + 512 + 1024;
   static constexpr int STG_OFF = KV_OFF;                 // epilogue staging reuses the K/V ring
 };
 
@@ -84,13 +86,13 @@ __global__ void __launch_bounds__(THREADS, 2)
   uint64_t* bar_q = bars + 0;
   uint64_t* kv_full = bars + 1;                // [STAGES]
   uint64_t* kv_empty = bars + 1 + STAGES;      // [STAGES]
-  // s_full / p_full are per score buffer: the softmax may run one chunk ahead
-  // of the MMA thread's p_full check, so a single barrier could advance two
-  // phases past a parity wait (ABA); one barrier per buffer cannot.
-  uint64_t* s_full = bars + 1 + 2 * STAGES;    // [2]
-  uint64_t* p_full = bars + 3 + 2 * STAGES;    // [2]
-  uint64_t* o_done = bars + 5 + 2 * STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 2 * STAGES);
+  // s_full / p_full / o_done are per score buffer (chunk j uses buffer j % 3):
+  // every waiter is then at most one phase behind its barrier, so a parity
+  // wait can never be overtaken by two completions (ABA).
+  uint64_t* s_full = bars + 1 + 2 * STAGES;    // [NSB]
+  uint64_t* p_full = s_full + NSB;             // [NSB]
+  uint64_t* o_done = p_full + NSB;             // [NSB]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NSB);
 
   const Dims& D = a.D;
   const int u = blockIdx.z, head = blockIdx.y, tile0 = blockIdx.x * ROWS;  // tiles of one (u, h) adjacent
@@ -120,6 +122,26 @@ __global__ void __launch_bounds__(THREADS, 2)
   }
   const int n_chunks = (key_end + KEYS - 1) / KEYS;
 
+  // SUMI self term, issued before the prologue barrier so the row-strided
+  // global loads overlap barrier init / TMEM allocation: s_self = q . k_self,
+  // and v_self is prefetched into L2 for the O initialisation below.
+  float ss_pre = 0.f;
+  if (MODE == MODE_SUMI && warp >= 4) {
+    const int row = (warp - 4) * 32 + lane;
+    if (row < n_rows) {
+      const bf16* qp = a.Q + (row_base + row) * ldq + head * DH;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(qp + 2 * D.d));
+#pragma unroll
+      for (int c = 0; c < DH; c += 8) {
+        float q[8], kk[8];
+        load8(qp + c, q);
+        load8(qp + D.d + c, kk);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ss_pre = fmaf(q[i], kk[i], ss_pre);
+      }
+    }
+  }
+
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmQ) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmKV) : "memory");
@@ -128,11 +150,11 @@ __global__ void __launch_bounds__(THREADS, 2)
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    mbar_init(&s_full[0], 1);
-    mbar_init(&s_full[1], 1);
-    mbar_init(&p_full[0], 128);
-    mbar_init(&p_full[1], 128);
-    mbar_init(o_done, 1);
+    for (int b = 0; b < NSB; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 128);
+      mbar_init(&o_done[b], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -144,7 +166,7 @@ __global__ void __launch_bounds__(THREADS, 2)
   __syncthreads();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const uint32_t tO = tmem_base + 2 * KEYS;  // S/P buffers at tmem_base + b * KEYS
+  const uint32_t tO = tmem_base + NSB * KEYS;  // S/P buffers at tmem_base + b * KEYS
 
   if (warp == 0) {
     if (lane == 0 && n_chunks > 0) {
@@ -173,30 +195,31 @@ __global__ void __launch_bounds__(THREADS, 2)
         mbar_wait(&kv_full[st], (j / STAGES) & 1);
         fence_after();
         const uint64_t kd = make_sdesc(smem_u32(smem + Ly::KV_OFF + 2 * st * Ly::KVB), 16, 8 * Ly::RB, Ly::SWZ);
-        const uint32_t tSj = tmem_base + (j & 1) * KEYS;
+        const uint32_t tSj = tmem_base + (j % NSB) * KEYS;
 #pragma unroll
         for (int s = 0; s < DH / 16; ++s) mma_bf16(tSj, qd + 2 * s, kd + 2 * s, idesc_qk, s > 0 ? 1u : 0u);
-        mma_commit(&s_full[j & 1]);
+        mma_commit(&s_full[j % NSB]);
       };
       issue_qk(0);
       for (int j = 0; j < n_chunks; ++j) {
         const int st = j % STAGES;
         if (j + 1 < n_chunks) {
-          if (j >= 1) mbar_wait(o_done, (j - 1) & 1);  // PV(j-1) consumed P_{j-1} = buffer (j+1) & 1
+          const int jp = j + 1 - NSB;  // previous user of buffer (j+1) % NSB
+          if (jp >= 0) mbar_wait(&o_done[jp % NSB], (jp / NSB) & 1);
           issue_qk(j + 1);
         }
-        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+        mbar_wait(&p_full[j % NSB], (j / NSB) & 1);
         fence_after();
         const uint64_t vd = make_sdesc(smem_u32(smem + Ly::KV_OFF + 2 * st * Ly::KVB + Ly::KVB), 16, 8 * Ly::RB,
                                        Ly::SWZ);
-        const uint32_t tPj = tmem_base + (j & 1) * KEYS;
+        const uint32_t tPj = tmem_base + (j % NSB) * KEYS;
 #pragma unroll
         for (int s = 0; s < KEYS / 16; ++s) {
           const uint64_t vds = vd + (uint64_t)((16 * Ly::RB) >> 4) * s;  // 16 keys = 2 groups of 8 rows
           const uint32_t acc = (MODE == MODE_SUMI || j > 0 || s > 0) ? 1u : 0u;
           mma_bf16_ts(tO, tPj + 8 * s, vds, idesc_pv, acc);  // 16 keys of P = 8 packed columns
         }
-        mma_commit(o_done);
+        mma_commit(&o_done[j % NSB]);
         mma_commit(&kv_empty[st]);
       }
     }
@@ -211,18 +234,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     float m_used, l;
     if (MODE == MODE_SUMI) {
       const bf16* qp = a.Q + grow * ldq + head * DH;
-      float ss = 0.f;
-      if (valid) {
-#pragma unroll
-        for (int c = 0; c < DH; c += 8) {
-          float q[8], kk[8];
-          load8(qp + c, q);
-          load8(qp + D.d + c, kk);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) ss = fmaf(q[i], kk[i], ss);
-        }
-      }
-      m_used = ss * sc;
+      m_used = ss_pre * sc;
       l = 1.f;
 #pragma unroll
       for (int c = 0; c < DH; c += 32) {  // O = v_self
@@ -244,8 +256,8 @@ __global__ void __launch_bounds__(THREADS, 2)
     }
     const bool causal_hist = (MODE == MODE_HIST) && D.causal;
     for (int j = 0; j < n_chunks; ++j) {
-      const uint32_t tSj = tmem_base + (j & 1) * KEYS + lane_off;
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      const uint32_t tSj = tmem_base + (j % NSB) * KEYS + lane_off;
+      mbar_wait(&s_full[j % NSB], (j / NSB) & 1);
       fence_after();
       const int key0 = j * KEYS;
       int lim = key_end - key0;  // keys [0, lim) of the chunk are visible to this row
@@ -279,7 +291,7 @@ __global__ void __launch_bounds__(THREADS, 2)
         m_used = mx;
       }
       if ((MODE == MODE_SUMI || j > 0) && __any_sync(0xffffffffu, mine)) {
-        if (j > 0) mbar_wait(o_done, (j - 1) & 1);  // PV(j-1) finished writing O
+        if (j > 0) mbar_wait(&o_done[(j - 1) % NSB], ((j - 1) / NSB) & 1);  // PV(j-1) finished writing O
         fence_after();
 #pragma unroll
         for (int c = 0; c < DH; c += 32) {
@@ -320,11 +332,11 @@ __global__ void __launch_bounds__(THREADS, 2)
       tmem_st_wait();
       l += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
       fence_before();
-      mbar_arrive(&p_full[j & 1]);
+      mbar_arrive(&p_full[j % NSB]);
     }
     // ---- epilogue: O / l -> bf16, staged in smem for coalesced stores
     if (n_chunks > 0) {
-      mbar_wait(o_done, (n_chunks - 1) & 1);
+      mbar_wait(&o_done[(n_chunks - 1) % NSB], ((n_chunks - 1) / NSB) & 1);
       fence_after();
     }
     const float inv = (valid && l > 0.f) ? 1.f / l : 0.f;
