@@ -85,6 +85,12 @@ struct climber_ctx_s {
   long long rows_cap;
   float* X;
   void *H, *QKV, *O, *Fh;
+  // fused-norm bf16 path: bf16 copy of the residual stream and per-row partial
+  // sums of squares (pld = d / 128 partials per row, one per GEMM column tile)
+  bool fused = false;
+  int pld = 1;
+  void* Xb;
+  float* part;
   // host bookkeeping
   std::mutex mu;
   std::vector<int> free_pages;
@@ -206,6 +212,9 @@ static void carve(climber_ctx_s* c, Carver& cv) {
   cv.take(c->QKV, R * 3 * d * e);
   cv.take(c->O, R * d * e);
   cv.take(c->Fh, R * F * e);
+  c->pld = D.d % 256 == 0 ? D.d / 256 : (D.d >= 128 ? D.d / 128 : 1);  // = N / BN of the RESID_NORM GEMMs
+  cv.take(c->Xb, R * d * 2);
+  cv.take(c->part, R * c->pld * 4);
 }
 
 // ---------------------------------------------------------------------------
@@ -313,22 +322,48 @@ extern "C" climber_status climber_create(const climber_config* cfg, const climbe
     c->sync_check = sc && atoi(sc) != 0;
 
     const size_t d = D.d, L = D.L, Nb = D.Nb, F = D.F;
+    // Fused-norm bf16 path: every RMSNorm gain is folded into the rows (input
+    // dimension) of the weight matrix that consumes the normalised activations,
+    // W' = diag(g) W (rounded to bf16 once), and 1/rms is applied per row in
+    // that GEMM's epilogue from the producer's partial sums of squares.
+    const char* en = getenv("CLIMBER_FUSED_NORM");
+    c->fused = cfg->dtype == CLIMBER_BF16 && c->use_tc && gemm_tc_available() && D.d % 128 == 0 &&
+               (D.dh == 32 || D.dh == 64) && D.Hse % 128 == 0 && !(en && atoi(en) == 0);
+    std::vector<float> wqkv_f, w1_f, fwqkv_f, fw1_f;
+    const float *w_qkv = w->w_qkv, *w1 = w->w1, *f_w_qkv = w->f_w_qkv, *f_w1 = w->f_w1;
+    if (c->fused) {
+      auto fold = [](std::vector<float>& dst, const float* W, const float* g, size_t batch, size_t rows, size_t cols) {
+        dst.resize(batch * rows * cols);
+        for (size_t b = 0; b < batch; ++b)
+          for (size_t i = 0; i < rows; ++i)
+            for (size_t j = 0; j < cols; ++j)
+              dst[(b * rows + i) * cols + j] = g[b * rows + i] * W[(b * rows + i) * cols + j];
+      };
+      fold(wqkv_f, w->w_qkv, w->g1, Nb * L, d, 3 * d);
+      fold(w1_f, w->w1, w->g2, Nb * L, d, F);
+      fold(fwqkv_f, w->f_w_qkv, w->f_g1, 1, d, 3 * d);
+      fold(fw1_f, w->f_w1, w->f_g2, 1, d, F);
+      w_qkv = wqkv_f.data();
+      w1 = w1_f.data();
+      f_w_qkv = fwqkv_f.data();
+      f_w1 = fw1_f.data();
+    }
     Uploader up{c};
     up.put(c->e_item, w->emb_item, 1, D.V, d, false, true);
     up.put(c->e_act, w->emb_act, 1, D.A, d, false, true);
     up.put(c->e_scn, w->emb_scn, 1, D.R, d, false, true);
     up.put(c->g1, w->g1, 1, Nb * L, d, false, false);
     up.put(c->g2, w->g2, 1, Nb * L, d, false, false);
-    up.put(c->w_qkv, w->w_qkv, Nb * L, d, 3 * d, true, true);
+    up.put(c->w_qkv, w_qkv, Nb * L, d, 3 * d, true, true);
     up.put(c->w_o, w->w_o, Nb * L, d, d, true, true);
-    up.put(c->w1, w->w1, Nb * L, d, F, true, true);
+    up.put(c->w1, w1, Nb * L, d, F, true, true);
     up.put(c->w2, w->w2, Nb * L, F, d, true, true);
     up.put(c->tau, w->tau, 1, 1, ntau, false, false);
     up.put(c->fg1, w->f_g1, 1, 1, d, false, false);
     up.put(c->fg2, w->f_g2, 1, 1, d, false, false);
-    up.put(c->fw_qkv, w->f_w_qkv, 1, d, 3 * d, true, true);
+    up.put(c->fw_qkv, f_w_qkv, 1, d, 3 * d, true, true);
     up.put(c->fw_o, w->f_w_o, 1, d, d, true, true);
-    up.put(c->fw1, w->f_w1, 1, d, F, true, true);
+    up.put(c->fw1, f_w1, 1, d, F, true, true);
     up.put(c->fw2, w->f_w2, 1, F, d, true, true);
     up.put(c->tau_f, w->tau_f, 1, 1, (size_t)D.R * D.h, false, false);
     up.put(c->w_se1, w->w_se1, 1, D.Dse, D.Hse, true, true);
@@ -474,7 +509,7 @@ static void encode_wave(climber_ctx_s* c, const EventsDev& ev, int u0, int U, lo
     {
       Prof p(c, CLIMBER_K_EMBED, s, 0, (double)rows * d * (3 * es + 4));
       launch_embed_hist<T>(ev, c->d_ev_off + u0, wslot, U, c->idx_all, c->vlen_all, c->bad_all, (const T*)c->e_item,
-                           (const T*)c->e_act, (const T*)c->e_scn, c->X, k, D, s);
+                           (const T*)c->e_act, (const T*)c->e_scn, c->X, (T*)nullptr, nullptr, 0, k, D, s);
     }
     for (int l = 0; l < D.L; ++l) {
       const size_t kl = (size_t)k * D.L + l;
@@ -541,7 +576,8 @@ static void score_wave(climber_ctx_s* c, const int32_t* items, const int64_t* wc
   float* X = c->X;  // C[p][k][d]
   {
     Prof p(c, CLIMBER_K_EMBED, s, 0, (double)P * d * (2 * es + 4 * Nb));
-    launch_embed_cand<T>(items, wcand, wr, U, P, (const T*)c->e_item, (const T*)c->e_scn, X, c->err, D, s);
+    launch_embed_cand<T>(items, wcand, wr, U, P, (const T*)c->e_item, (const T*)c->e_scn, X, (T*)nullptr, nullptr, 0,
+                         c->err, D, s);
   }
   const double norm_bytes = (double)P * d * (4 + es);
   for (int k = 0; k < D.Nb; ++k) {
@@ -622,6 +658,167 @@ static void score_wave(climber_ctx_s* c, const int32_t* items, const int64_t* wc
   {
     Prof p(c, CLIMBER_K_HEAD, s, 3.0 * P * D.Dse, (double)P * D.Dse * 8 + P * 4);
     launch_head(X, gate, c->w_head, c->b_head, scores, P, D.Dse, s);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fused-norm bf16 path (tcgen05 GEMMs): no RMSNorm kernels.  Residual-add GEMMs
+// (EPI_RESID_NORM) write the fp32 residual, its bf16 copy and per-row partial
+// sums of squares; the GEMM that consumes the normalised rows reads the bf16
+// copy with the gain folded into its weights and scales each row by 1/rms.
+// ---------------------------------------------------------------------------
+static Epilogue epi_resid_norm(float* X, long long ldo, void* Xb, float* part, long long part_rs) {
+  Epilogue e{};
+  e.kind = EPI_RESID_NORM; e.out = X; e.ldo = ldo; e.out_b16 = Xb; e.part = part; e.part_rs = part_rs;
+  return e;
+}
+static Epilogue with_rs(Epilogue e, const climber_ctx_s* c, const float* part, long long rs_rs) {
+  e.rs_part = part; e.rs_rs = rs_rs; e.rs_n = c->pld; e.rs_inv_d = 1.0f / (float)c->D.d; e.rs_eps = c->D.eps;
+  return e;
+}
+
+static void attn_hist_bf16(climber_ctx_s* c, const bf16* Q, const int* wslot, const int* wr, int U, bf16* O, int k,
+                           int l, cudaStream_t s) {
+  const Dims& D = c->D;
+  if (c->attn_mode == 2 && attn_tc_supported(D.dh, D.nk, true))
+    launch_attn_hist_tc(Q, wslot, wr, U, (const bf16*)c->pool, c->n_pages * 2 * PAGE, c->ptab, c->vlen_all, c->tau,
+                        O, k, l, D, s);
+  else if (c->attn_mode >= 1)
+    launch_attn_hist_mma(Q, wslot, wr, U, (const bf16*)c->pool, c->ptab, c->vlen_all, c->tau, O, k, l, D, s);
+  else
+    launch_attn_hist<bf16>(Q, wslot, wr, U, (const bf16*)c->pool, c->ptab, c->vlen_all, c->tau, O, k, l, D, s);
+}
+
+static void attn_sumi_bf16(climber_ctx_s* c, const bf16* QKV, long long P, const int64_t* wcand, const int* wslot,
+                           const int* wr, int U, int Mmax, bf16* O, int k, int l, cudaStream_t s) {
+  const Dims& D = c->D;
+  if (c->attn_mode == 2 && attn_tc_supported(D.dh, D.nk, false))
+    launch_attn_sumi_tc(QKV, P, wcand, wslot, wr, U, Mmax, (const bf16*)c->pool, c->n_pages * 2 * PAGE, c->ptab,
+                        c->vlen_all, c->tau, O, k, l, D, s);
+  else if (c->attn_mode >= 1)
+    launch_attn_sumi_mma(QKV, wcand, wslot, wr, U, Mmax, (const bf16*)c->pool, c->ptab, c->vlen_all, c->tau, O, k, l,
+                         D, s);
+  else
+    launch_attn_sumi<bf16>(QKV, wcand, wslot, wr, U, Mmax, (const bf16*)c->pool, c->ptab, c->vlen_all, c->tau, O, k,
+                           l, D, s);
+}
+
+static void encode_wave_fused(climber_ctx_s* c, const EventsDev& ev, int u0, int U, long long n_events,
+                              cudaStream_t s) {
+  const Dims& D = c->D;
+  const long long rows = (long long)U * D.nk;
+  const long long d = D.d, F = D.F, pld = c->pld;
+  const int* wslot = c->d_slots + u0;
+  const int* wr = c->d_r + u0;
+  {
+    Prof p(c, CLIMBER_K_EXTRACT, s, 0, (double)n_events * 14 + (double)U * D.Nb * D.nk * 4);
+    launch_extract(ev, c->d_ev_off + u0, wslot, U, c->amask, c->smask, c->idx_all, c->vlen_all, c->bad_all, c->err,
+                   D, s);
+  }
+  bf16* Xb = (bf16*)c->Xb;
+  bf16* Qb = (bf16*)c->QKV;
+  bf16* O = (bf16*)c->O;
+  bf16* Fh = (bf16*)c->Fh;
+  float* X = c->X;
+  const double causal_pairs = D.causal ? (double)D.nk * (D.nk + 1) / 2 : (double)D.nk * D.nk;
+  for (int k = 0; k < D.Nb; ++k) {
+    {
+      Prof p(c, CLIMBER_K_EMBED, s, 0, (double)rows * d * (3 * 2 + 4 + 2));
+      launch_embed_hist<bf16>(ev, c->d_ev_off + u0, wslot, U, c->idx_all, c->vlen_all, c->bad_all,
+                              (const bf16*)c->e_item, (const bf16*)c->e_act, (const bf16*)c->e_scn, X, Xb, c->part,
+                              c->pld, k, D, s);
+    }
+    for (int l = 0; l < D.L; ++l) {
+      const size_t kl = (size_t)k * D.L + l;
+      Epilogue e{};
+      e.kind = EPI_QKV_PAGES; e.out = Qb; e.ldo = d; e.pool = c->pool; e.ptab = c->ptab; e.wave_slot = wslot;
+      e.pool_rows = c->n_pages * 2 * PAGE;
+      e.blk = k; e.layer = l; e.d = D.d; e.h = D.h; e.dh = D.dh; e.nk = D.nk; e.Nb = D.Nb; e.L = D.L; e.ppb = D.ppb;
+      e = with_rs(e, c, c->part, pld);
+      const bf16* Wqkv = (const bf16*)c->w_qkv + kl * 3 * d * d;
+      if (l < D.L - 1) {
+        e.col_off = 0;
+        gemm<bf16>(c, CLIMBER_K_GEMM_QKV, Xb, d, Wqkv, d, rows, 3 * D.d, D.d, e, s);
+        {
+          Prof p(c, CLIMBER_K_ATTN_HIST, s, 4.0 * U * causal_pairs * d, (double)rows * d * 2 * 4);
+          attn_hist_bf16(c, Qb, wslot, wr, U, O, k, l, s);
+        }
+        gemm<bf16>(c, CLIMBER_K_GEMM_O, O, d, (const bf16*)c->w_o + kl * d * d, d, rows, D.d, D.d,
+                   epi_resid_norm(X, d, Xb, c->part, pld), s);
+        gemm<bf16>(c, CLIMBER_K_GEMM_FFN_UP, Xb, d, (const bf16*)c->w1 + kl * F * d, d, rows, D.F, D.d,
+                   with_rs(epi_store(Fh, F, ACT_SILU), c, c->part, pld), s);
+        gemm<bf16>(c, CLIMBER_K_GEMM_FFN_DOWN, Fh, F, (const bf16*)c->w2 + kl * d * F, F, rows, D.d, D.F,
+                   epi_resid_norm(X, d, Xb, c->part, pld), s);
+      } else {
+        e.col_off = D.d;  // last layer: only K/V of the history are ever read
+        gemm<bf16>(c, CLIMBER_K_GEMM_QKV, Xb, d, Wqkv + d * d, d, rows, 2 * D.d, D.d, e, s);
+      }
+    }
+  }
+}
+
+static void score_wave_fused(climber_ctx_s* c, const int32_t* items, const int64_t* wcand, int u0, int U, long long P,
+                             int Mmax_wave, float* scores, cudaStream_t s) {
+  const Dims& D = c->D;
+  const long long d = D.d, F = D.F, Nb = D.Nb, ldC = Nb * d, pld = c->pld;
+  const int* wslot = c->d_slots + u0;
+  const int* wr = c->d_r + u0;
+  bf16* Cb = (bf16*)c->Xb;  // [p][k][d] bf16 copy of the residual
+  bf16* QKV = (bf16*)c->QKV;
+  bf16* O = (bf16*)c->O;
+  bf16* Fh = (bf16*)c->Fh;
+  float* C = c->X;  // [p][k][d]
+  {
+    Prof p(c, CLIMBER_K_EMBED, s, 0, (double)P * d * (2 * 2 + 6 * Nb));
+    launch_embed_cand<bf16>(items, wcand, wr, U, P, (const bf16*)c->e_item, (const bf16*)c->e_scn, C, Cb, c->part,
+                            c->pld, c->err, D, s);
+  }
+  for (int k = 0; k < D.Nb; ++k) {
+    float* Ck = C + k * d;
+    bf16* Cbk = Cb + k * d;
+    float* pk = c->part + k * pld;
+    const long long prs = Nb * pld;
+    for (int l = 0; l < D.L; ++l) {
+      const size_t kl = (size_t)k * D.L + l;
+      gemm<bf16>(c, CLIMBER_K_GEMM_QKV, Cbk, ldC, (const bf16*)c->w_qkv + kl * 3 * d * d, d, P, 3 * D.d, D.d,
+                 with_rs(epi_store(QKV, 3 * d), c, pk, prs), s);
+      {
+        Prof p(c, CLIMBER_K_ATTN_SUMI, s, 4.0 * P * (D.nk + 1) * d, (double)P * d * 2 * 4 + (double)U * D.nk * d * 4);
+        attn_sumi_bf16(c, QKV, P, wcand, wslot, wr, U, Mmax_wave, O, k, l, s);
+      }
+      gemm<bf16>(c, CLIMBER_K_GEMM_O, O, d, (const bf16*)c->w_o + kl * d * d, d, P, D.d, D.d,
+                 epi_resid_norm(Ck, ldC, Cbk, pk, prs), s);
+      gemm<bf16>(c, CLIMBER_K_GEMM_FFN_UP, Cbk, ldC, (const bf16*)c->w1 + kl * F * d, d, P, D.F, D.d,
+                 with_rs(epi_store(Fh, F, ACT_SILU), c, pk, prs), s);
+      gemm<bf16>(c, CLIMBER_K_GEMM_FFN_DOWN, Fh, F, (const bf16*)c->w2 + kl * d * F, F, P, D.d, D.F,
+                 epi_resid_norm(Ck, ldC, Cbk, pk, prs), s);
+    }
+  }
+  // ---- BGF (Eq. 4): the N_b block outputs of a pair are contiguous rows of C
+  const long long R = P * Nb;
+  gemm<bf16>(c, CLIMBER_K_GEMM_QKV, Cb, d, (const bf16*)c->fw_qkv, d, R, 3 * D.d, D.d,
+             with_rs(epi_store(QKV, 3 * d), c, c->part, pld), s);
+  {
+    Prof p(c, CLIMBER_K_ATTN_FUSION, s, 4.0 * P * Nb * Nb * d, (double)R * d * 2 * 4);
+    launch_attn_fusion<bf16>(QKV, wcand, wr, U, P, c->tau_f, O, D, s);
+  }
+  gemm<bf16>(c, CLIMBER_K_GEMM_O, O, d, (const bf16*)c->fw_o, d, R, D.d, D.d,
+             epi_resid_norm(C, d, Cb, c->part, pld), s);
+  gemm<bf16>(c, CLIMBER_K_GEMM_FFN_UP, Cb, d, (const bf16*)c->fw1, d, R, D.F, D.d,
+             with_rs(epi_store(Fh, F, ACT_SILU), c, c->part, pld), s);
+  gemm<bf16>(c, CLIMBER_K_GEMM_FFN_DOWN, Fh, F, (const bf16*)c->fw2, F, R, D.d, D.F,
+             epi_resid_norm(C, d, Cb, c->part, pld), s);
+  // ---- squeeze-and-excitation on vec(G): the bf16 copy Cb viewed as [P][N_b d]
+  bf16* Z1 = O;  // [P][Hse]
+  gemm<bf16>(c, CLIMBER_K_GEMM_SE, Cb, D.Dse, (const bf16*)c->w_se1, D.Dse, P, D.Hse, D.Dse,
+             epi_store(Z1, D.Hse, ACT_RELU, c->b_se1), s);
+  float* gate = reinterpret_cast<float*>(c->Fh);
+  Epilogue eg{};
+  eg.kind = EPI_STORE_F32; eg.act = ACT_SIGMOID; eg.out = gate; eg.ldo = D.Dse; eg.bias = c->b_se2;
+  gemm<bf16>(c, CLIMBER_K_GEMM_SE, Z1, D.Hse, (const bf16*)c->w_se2, D.Hse, P, D.Dse, D.Hse, eg, s);
+  {
+    Prof p(c, CLIMBER_K_HEAD, s, 3.0 * P * D.Dse, (double)P * D.Dse * 8 + P * 4);
+    launch_head(C, gate, c->w_head, c->b_head, scores, P, D.Dse, s);
   }
 }
 
@@ -724,7 +921,8 @@ extern "C" climber_status climber_encode_users(climber_ctx_t c, int32_t B, const
     for (int u0 = 0; u0 < B; u0 += c->cfg.max_wave_users) {
       int U = B - u0 < c->cfg.max_wave_users ? B - u0 : c->cfg.max_wave_users;
       long long nev = ev_offsets[u0 + U] - ev_offsets[u0];
-      if (c->cfg.dtype == CLIMBER_BF16) encode_wave<bf16>(c, ev, u0, U, nev, s);
+      if (c->fused) encode_wave_fused(c, ev, u0, U, nev, s);
+      else if (c->cfg.dtype == CLIMBER_BF16) encode_wave<bf16>(c, ev, u0, U, nev, s);
       else encode_wave<float>(c, ev, u0, U, nev, s);
       climber_status rs = check_launch(c, s);
       if (rs != CLIMBER_OK) return rs;
@@ -796,7 +994,8 @@ extern "C" climber_status climber_score_items_batched(climber_ctx_t c, int32_t B
       const int32_t* it = items + cand_offsets[w.u0];
       float* sc = scores + cand_offsets[w.u0];
       const int64_t* wc = c->d_cand_off + w.coff;
-      if (c->cfg.dtype == CLIMBER_BF16) score_wave<bf16>(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
+      if (c->fused) score_wave_fused(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
+      else if (c->cfg.dtype == CLIMBER_BF16) score_wave<bf16>(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
       else score_wave<float>(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
       climber_status rs = check_launch(c, s);
       if (rs != CLIMBER_OK) return rs;

@@ -96,6 +96,9 @@ enum EpiKind : int {
   EPI_RESID = 1,   // out_f32[m*ldo + n] += acc
   EPI_QKV_PAGES = 2, // columns (n + col_off) in [0,d): Q -> out_T[m*ldo + n]; [d,3d): K/V -> pages
   EPI_STORE_F32 = 3, // out_f32[m*ldo + n] = act(acc + bias[n])  (the sigmoid gate of Eq. 4)
+  EPI_RESID_NORM = 4, // residual add that also prepares the next RMSNorm (tcgen05 GEMM only):
+                      // C = C + acc (fp32, out), Cb = bf16(C) (out_b16), part[m*part_rs + n_tile] =
+                      // sum over the tile's columns of C^2
 };
 enum ActKind : int { ACT_NONE = 0, ACT_SILU = 1, ACT_RELU = 2, ACT_SIGMOID = 3 };
 
@@ -121,6 +124,16 @@ struct Epilogue {
   int col_off;          // 0 (full QKV) or d (last layer: K/V only)
   int blk, layer;       // (k, l)
   int d, h, dh, nk, Nb, L, ppb;
+  // EPI_RESID_NORM outputs
+  void* out_b16;        // bf16 copy of C, same [rows][ldo] layout
+  float* part;          // per-row, per-column-tile sums of squares
+  long long part_rs;    // row stride of part (floats)
+  // RMSNorm folded into a consumer GEMM (gain pre-multiplied into the weights):
+  // acc *= 1 / sqrt(sum_{j < rs_n} rs_part[m * rs_rs + j] * rs_inv_d + rs_eps)
+  const float* rs_part;
+  long long rs_rs;
+  int rs_n;
+  float rs_inv_d, rs_eps;
 };
 
 // Page addressing: page = [2 (K,V)][PAGE tokens][d] elements (heads contiguous

@@ -30,31 +30,34 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B rows = one SWIZZLE_128B atom width
 
 
-template <int BN, int STAGES, int EPIW, int SBUF>
+template <int BN, int STAGES, int EPIW, int SBUF, int NORM = 0>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STG_OFF = STAGES * STAGE_BYTES;  // epilogue staging: 4 warps x 2 x (32 rows x 128 B)
-  static constexpr int STG_WARP = SBUF * 32 * 128;
+  // NORM (EPI_RESID_NORM): per warp 2 sets x (fp32 box 32x32 + bf16 box 32x32) = 12 KB
+  static constexpr int STG_WARP = NORM ? 2 * 6144 : SBUF * 32 * 128;
   static constexpr int BAR_OFF = STG_OFF + EPIW * STG_WARP;
-  static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + tmem addr, + alignment slack
+  static constexpr int TOTAL = BAR_OFF + 512 + 1024;  // barriers + tmem addr, + alignment slack
 };
 
-// EPIW epilogue warps (4 or 8), SBUF staging buffers per epilogue warp (1 or 2)
-template <int BN, int STAGES, int EPIW, int SBUF>
+// EPIW epilogue warps (4 or 8), SBUF staging buffers per epilogue warp (1 or 2),
+// NORM = 1: the EPI_RESID_NORM epilogue (residual add + bf16 copy + row sums of squares)
+template <int BN, int STAGES, int EPIW, int SBUF, int NORM>
 __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmP, long long M, int N,
-              int K, Epilogue e) {
-  using S = Smem<BN, STAGES, EPIW, SBUF>;
+              const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmP,
+              const __grid_constant__ CUtensorMap tmC16, long long M, int N, int K, Epilogue e) {
+  using S = Smem<BN, STAGES, EPIW, SBUF, NORM>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ldbar = tempty + 2;  // NORM: 2 TMA-load barriers per epilogue warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ldbar + 2 * EPIW);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = N / BN;
@@ -67,6 +70,7 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmD) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmP) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmC16) : "memory");
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -75,6 +79,7 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 32 * EPIW);
     }
+    for (int a = 0; a < 2 * EPIW; ++a) mbar_init(&ldbar[a], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -154,11 +159,94 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     int sbuf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    if constexpr (NORM) {
+      // EPI_RESID_NORM, per 32-column chunk: the old residual C (fp32 box 32x32,
+      // 128B-swizzled) is TMA-loaded into one of two staging sets (two chunks in
+      // flight), C += acc in registers (thread = row), the new C is written back
+      // in place and as bf16 into a 32x32 box (64B-swizzled), two TMA stores; the
+      // row's sum of squares over the tile's columns goes to part[m][n_tile].
+      uint64_t* lb = ldbar + (warp - 4) * 2;
+      uint32_t lph[2] = {0u, 0u};
+      constexpr int NCH = BN / 32;
+      auto issue = [&](long long r0, int n0, int set) {
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging no longer read by stores
+          mbar_expect_tx(&lb[set], 4096);
+          tma_load_2d(stg + set * 6144, &tmD, &lb[set], n0, (int)r0);
+        }
+      };
+      for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int m_blk = (int)(t / n_tiles), n_blk = (int)(t % n_tiles);
+        const long long row0 = (long long)m_blk * BM + ew * 32;
+        const bool rows_ok = row0 < M;  // warp-uniform
+        if (rows_ok) {  // the first two chunks of old residual are requested before the accumulator wait
+          issue(row0, n_blk * BN, 0);
+          issue(row0, n_blk * BN + 32, 1);
+        }
+        mbar_wait(&tfull[acc], acc_phase);
+        fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+        float ss = 0.f;
+#pragma unroll 1
+        for (int q = 0; q < NCH; ++q) {
+          const int set = q & 1;
+          const int n0 = n_blk * BN + q * 32;
+          if (rows_ok && q >= 1 && q + 1 < NCH) issue(row0, n0 + 32, set ^ 1);  // set of chunk q-1
+          float v[32];
+          tmem_ld32(taddr + q * 32, v);
+          if (rows_ok) {
+            mbar_wait(&lb[set], lph[set]);
+            lph[set] ^= 1;
+            uint8_t* b = stg + set * 6144;
+            uint8_t* rowp = b + lane * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float4* p4 = reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) << 4));
+              const float4 o = *p4;
+              float* vv = v + 4 * j;
+              vv[0] += o.x; vv[1] += o.y; vv[2] += o.z; vv[3] += o.w;
+              ss = fmaf(vv[0], vv[0], fmaf(vv[1], vv[1], fmaf(vv[2], vv[2], fmaf(vv[3], vv[3], ss))));
+              *p4 = make_float4(vv[0], vv[1], vv[2], vv[3]);
+            }
+            uint8_t* brow = b + 4096 + lane * 64;  // bf16 box: 64 B rows, 64B swizzle
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              __nv_bfloat162 p0 = __floats2bfloat162_rn(v[8 * j], v[8 * j + 1]);
+              __nv_bfloat162 p1 = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
+              __nv_bfloat162 p2 = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
+              __nv_bfloat162 p3 = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
+              st_shared_v4(brow + ((j ^ ((lane >> 1) & 3)) << 4), *reinterpret_cast<uint32_t*>(&p0),
+                           *reinterpret_cast<uint32_t*>(&p1), *reinterpret_cast<uint32_t*>(&p2),
+                           *reinterpret_cast<uint32_t*>(&p3));
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmD, b, n0, (int)row0);
+              tma_store_2d(&tmC16, b + 4096, n0, (int)row0);
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+          }
+        }
+        if (rows_ok && row0 + lane < M) e.part[(row0 + lane) * e.part_rs + n_blk] = ss;
+        fence_before();
+        mbar_arrive(&tempty[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    } else
     for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const int m_blk = (int)(t / n_tiles), n_blk = (int)(t % n_tiles);
+      const long long row0 = (long long)m_blk * BM + ew * 32;
+      // RMSNorm folded into this GEMM: the per-row 1/rms from the producer's
+      // partials, loaded before the accumulator wait so the latency is hidden
+      float rsc = 1.f;
+      if (e.rs_part != nullptr && row0 + lane < M) {
+        float sum = 0.f;
+        for (int j = 0; j < e.rs_n; ++j) sum += e.rs_part[(row0 + lane) * e.rs_rs + j];
+        rsc = rsqrtf(sum * e.rs_inv_d + e.rs_eps);
+      }
       mbar_wait(&tfull[acc], acc_phase);
       fence_after();
-      const long long row0 = (long long)m_blk * BM + ew * 32;
       const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
       if (tma_epi) {
 #pragma unroll 1
@@ -167,10 +255,33 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
           tmem_ld32(taddr + c, v);  // lane = row row0 + lane
           if (!f32_out) tmem_ld32(taddr + c + 32, v + 32);
           const int n0 = n_blk * BN + c;
-          if (e.kind != EPI_RESID && e.kind != EPI_QKV_PAGES) {
+          if (e.rs_part != nullptr) {
 #pragma unroll
-            for (int i = 0; i < 64; ++i)
-              if (i < CW) v[i] = apply_act<bf16>(e.act, v[i] + (e.bias ? e.bias[n0 + i] : 0.0f));
+            for (int i = 0; i < 64; ++i) v[i] *= rsc;
+          }
+          if (e.kind != EPI_RESID && e.kind != EPI_QKV_PAGES) {
+            // bias (vectorised) and activation, each hoisted out of the element loop
+            if (e.bias != nullptr) {
+              const float4* b4 = reinterpret_cast<const float4*>(e.bias + n0);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                if (4 * j < CW) {
+                  const float4 b = b4[j];
+                  v[4 * j] += b.x; v[4 * j + 1] += b.y; v[4 * j + 2] += b.z; v[4 * j + 3] += b.w;
+                }
+              }
+            }
+            const int act = e.act;
+            if (act == ACT_SILU) {
+#pragma unroll
+              for (int i = 0; i < 64; ++i) v[i] = silu_t<bf16>(v[i]);
+            } else if (act == ACT_SIGMOID) {
+#pragma unroll
+              for (int i = 0; i < 64; ++i) v[i] = sigmoid_t<bf16>(v[i]);
+            } else if (act == ACT_RELU) {
+#pragma unroll
+              for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i], 0.f);
+            }
           }
           uint8_t* buf = stg + sbuf * 4096;
           if (lane == 0) {
@@ -267,7 +378,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 static bool make_map(CUtensorMap* map, const void* ptr, long long rows, int cols, long long ld, int box_rows,
-                     int box_cols = BK, bool f32 = false) {
+                     int box_cols = BK, bool f32 = false, bool sw64 = false) {
   auto enc = get_encode();
   if (!enc) return false;
   const int es = f32 ? 4 : 2;
@@ -277,7 +388,8 @@ static bool make_map(CUtensorMap* map, const void* ptr, long long rows, int cols
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                    const_cast<void*>(ptr), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -293,13 +405,15 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int EPIW, int SBUF>
+template <int BN, int STAGES, int EPIW, int SBUF, int NORM = 0>
 static void launch(const bf16* A, long long lda, const bf16* B, long long ldb, long long M, int N, int K,
                    const Epilogue& e, cudaStream_t s) {
-  CUtensorMap ma, mb, md, mp;
+  CUtensorMap ma, mb, md, mp, mc;
   make_map(&ma, A, M, K, lda, BM);
   make_map(&mb, B, N, K, ldb, BN);
   mp = ma;  // unused unless QKV_PAGES
+  mc = ma;  // unused unless RESID_NORM
+  if (e.kind == EPI_RESID_NORM) make_map(&mc, e.out_b16, M, N, e.ldo, 32, 32, false, true);
   if (e.kind == EPI_QKV_PAGES) {
     if (e.d % 64 == 0) {
       make_map(&md, e.out, M, e.d, e.ldo, 32, 64, false);          // Q buffer [M][d]
@@ -312,16 +426,16 @@ static void launch(const bf16* A, long long lda, const bf16* B, long long ldb, l
   } else {
     make_map(&md, e.out, M, N, e.ldo, 32, 32, true);
   }
-  constexpr int smem = Smem<BN, STAGES, EPIW, SBUF>::TOTAL;
+  constexpr int smem = Smem<BN, STAGES, EPIW, SBUF, NORM>::TOTAL;
   static_assert(smem <= 232448, "smem");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, EPIW, SBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, EPIW, SBUF, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
   long long tiles = ((M + BM - 1) / BM) * (N / BN);
   int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  k_gemm_tc<BN, STAGES, EPIW, SBUF><<<grid, 128 + 32 * EPIW, smem, s>>>(ma, mb, md, mp, M, N, K, e);
+  k_gemm_tc<BN, STAGES, EPIW, SBUF, NORM><<<grid, 128 + 32 * EPIW, smem, s>>>(ma, mb, md, mp, mc, M, N, K, e);
 }
 
 }  // namespace tc
@@ -331,6 +445,8 @@ bool gemm_tc_supported(long long M, int N, int K, long long lda, long long ldb) 
   if ((lda * 2) % 16 || (ldb * 2) % 16) return false;
   return tc::get_encode() != nullptr;
 }
+
+bool gemm_tc_available() { return tc::get_encode() != nullptr; }
 
 void launch_gemm_tc(const bf16* A, long long lda, const bf16* B, long long ldb, long long M, int N, int K,
                     const Epilogue& e, cudaStream_t s) {
@@ -343,6 +459,11 @@ void launch_gemm_tc(const bf16* A, long long lda, const bf16* B, long long ldb, 
   if (forced < 0) {
     const char* v = getenv("CLIMBER_GEMM_VARIANT");
     forced = v ? atoi(v) : 0;
+  }
+  if (e.kind == EPI_RESID_NORM) {  // N % 128 == 0 (checked by the caller)
+    if (N % 256 == 0) tc::launch<256, 3, 4, 2, 1>(A, lda, B, ldb, M, N, K, e, s);
+    else tc::launch<128, 4, 4, 2, 1>(A, lda, B, ldb, M, N, K, e, s);
+    return;
   }
   const bool heavy = (e.kind == EPI_STORE || e.kind == EPI_STORE_F32) && e.act != ACT_NONE;
   int var = forced ? forced : (heavy ? 3 : 1);

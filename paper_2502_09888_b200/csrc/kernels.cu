@@ -72,8 +72,10 @@ __global__ void k_embed_hist(const int32_t* __restrict__ item, const uint8_t* __
                              const int* __restrict__ wave_slot, const int* __restrict__ idx_all,
                              const int* __restrict__ vlen_all, const int* __restrict__ bad_all,
                              const T* __restrict__ e_item, const T* __restrict__ e_act,
-                             const T* __restrict__ e_scn, float* __restrict__ X, long long rows, int k,
-                             Dims D) {
+                             const T* __restrict__ e_scn, float* __restrict__ X, T* __restrict__ Xb,
+                             float* __restrict__ part, int pld, long long rows, int k, Dims D) {
+  // Xb / part (fused-norm bf16 path): bf16 copy of the row and its sum of squares
+  // (part[row][0]; the other pld-1 partial slots are 0) for the first GEMM's folded RMSNorm
   long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -83,7 +85,11 @@ __global__ void k_embed_hist(const int32_t* __restrict__ item, const uint8_t* __
   float* out = X + row * D.d;
   if (t >= v) {
     float z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int c = lane * 8; c < D.d; c += 256) store8(out + c, z);
+    for (int c = lane * 8; c < D.d; c += 256) {
+      store8(out + c, z);
+      if (Xb) store8(Xb + row * D.d + c, z);
+    }
+    if (part && lane < pld) part[row * pld + lane] = 0.f;
     return;
   }
   long long ev = ev_off[u] + idx_all[((long long)slot * D.Nb + k) * D.nk + (D.nk - v + t)];
@@ -92,14 +98,23 @@ __global__ void k_embed_hist(const int32_t* __restrict__ item, const uint8_t* __
   if (it < 0 || it >= D.V) it = 0;
   if (a >= D.A) a = 0;
   if (sc >= D.R) sc = 0;
+  float ss = 0.f;
   for (int c = lane * 8; c < D.d; c += 256) {
     float x[8], y[8], z[8];
     load8(e_item + (long long)it * D.d + c, x);
     load8(e_act + (long long)a * D.d + c, y);
     load8(e_scn + (long long)sc * D.d + c, z);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = bad ? __int_as_float(0x7fc00000) : x[i] + y[i] + z[i];
+    for (int i = 0; i < 8; ++i) {
+      x[i] = bad ? __int_as_float(0x7fc00000) : x[i] + y[i] + z[i];
+      ss = fmaf(x[i], x[i], ss);
+    }
     store8(out + c, x);
+    if (Xb) store8(Xb + row * D.d + c, x);
+  }
+  if (part) {
+    ss = warp_sum(ss);
+    if (lane < pld) part[row * pld + lane] = (lane == 0) ? ss : 0.f;
   }
 }
 
@@ -119,7 +134,8 @@ template <typename T>
 __global__ void k_embed_cand(const int32_t* __restrict__ items, const int64_t* __restrict__ cand_off,
                              const int* __restrict__ wave_r, int U, long long P,
                              const T* __restrict__ e_item, const T* __restrict__ e_scn,
-                             float* __restrict__ C, int* __restrict__ err, Dims D) {
+                             float* __restrict__ C, T* __restrict__ Cb, float* __restrict__ part, int pld,
+                             int* __restrict__ err, Dims D) {
   long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (p >= P) return;
@@ -131,13 +147,25 @@ __global__ void k_embed_cand(const int32_t* __restrict__ items, const int64_t* _
     it = 0;
     if (lane == 0) atomicOr(err, ERR_RANGE);
   }
+  float ss = 0.f;
   for (int c = lane * 8; c < D.d; c += 256) {
     float x[8], z[8];
     load8(e_item + (long long)it * D.d + c, x);
     load8(e_scn + (long long)r * D.d + c, z);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = bad ? __int_as_float(0x7fc00000) : x[i] + z[i];
-    for (int k = 0; k < D.Nb; ++k) store8(C + (p * D.Nb + k) * D.d + c, x);
+    for (int i = 0; i < 8; ++i) {
+      x[i] = bad ? __int_as_float(0x7fc00000) : x[i] + z[i];
+      ss = fmaf(x[i], x[i], ss);
+    }
+    for (int k = 0; k < D.Nb; ++k) {
+      store8(C + (p * D.Nb + k) * D.d + c, x);
+      if (Cb) store8(Cb + (p * D.Nb + k) * D.d + c, x);
+    }
+  }
+  if (part) {
+    ss = warp_sum(ss);
+    for (int k = 0; k < D.Nb; ++k)
+      if (lane < pld) part[(p * D.Nb + k) * pld + lane] = (lane == 0) ? ss : 0.f;
   }
 }
 
@@ -609,17 +637,19 @@ void launch_extract(const EventsDev& ev, const int64_t* ev_off, const int* wave_
 template <typename T>
 void launch_embed_hist(const EventsDev& ev, const int64_t* ev_off, const int* wave_slot, int U, const int* idx_all,
                        const int* vlen_all, const int* bad_all, const T* e_item, const T* e_act, const T* e_scn,
-                       float* X, int k, const Dims& D, cudaStream_t s) {
+                       float* X, T* Xb, float* part, int pld, int k, const Dims& D, cudaStream_t s) {
   long long rows = (long long)U * D.nk;
   k_embed_hist<T><<<blocks_for(rows * 32, 256), 256, 0, s>>>(ev.item, ev.action, ev.scenario, ev_off, wave_slot,
-                                                           idx_all, vlen_all, bad_all, e_item, e_act, e_scn, X,
-                                                           rows, k, D);
+                                                           idx_all, vlen_all, bad_all, e_item, e_act, e_scn, X, Xb,
+                                                           part, pld, rows, k, D);
 }
 
 template <typename T>
 void launch_embed_cand(const int32_t* items, const int64_t* cand_off, const int* wave_r, int U, long long P,
-                       const T* e_item, const T* e_scn, float* C, int* err, const Dims& D, cudaStream_t s) {
-  k_embed_cand<T><<<blocks_for(P * 32, 256), 256, 0, s>>>(items, cand_off, wave_r, U, P, e_item, e_scn, C, err, D);
+                       const T* e_item, const T* e_scn, float* C, T* Cb, float* part, int pld, int* err,
+                       const Dims& D, cudaStream_t s) {
+  k_embed_cand<T><<<blocks_for(P * 32, 256), 256, 0, s>>>(items, cand_off, wave_r, U, P, e_item, e_scn, C, Cb, part,
+                                                          pld, err, D);
 }
 
 template <typename T>
@@ -696,10 +726,10 @@ void launch_gemm_simt(const T* A, long long lda, const T* B, long long ldb, long
 
 #define INST(T)                                                                                                  \
   template void launch_embed_hist<T>(const EventsDev&, const int64_t*, const int*, int, const int*, const int*,  \
-                                     const int*, const T*, const T*, const T*, float*, int, const Dims&,         \
-                                     cudaStream_t);                                                              \
+                                     const int*, const T*, const T*, const T*, float*, T*, float*, int, int,     \
+                                     const Dims&, cudaStream_t);                                                 \
   template void launch_embed_cand<T>(const int32_t*, const int64_t*, const int*, int, long long, const T*,       \
-                                     const T*, float*, int*, const Dims&, cudaStream_t);                         \
+                                     const T*, float*, T*, float*, int, int*, const Dims&, cudaStream_t);        \
   template void launch_rmsnorm<T>(const float*, long long, const float*, T*, long long, long long, int, float,   \
                                   cudaStream_t);                                                                 \
   template void launch_convert<T>(const float*, T*, long long, cudaStream_t);                                    \

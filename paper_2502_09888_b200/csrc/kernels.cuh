@@ -17,10 +17,11 @@ void launch_extract(const EventsDev& ev, const int64_t* ev_off, const int* wave_
 template <typename T>
 void launch_embed_hist(const EventsDev& ev, const int64_t* ev_off, const int* wave_slot, int U, const int* idx_all,
                        const int* vlen_all, const int* bad_all, const T* e_item, const T* e_act, const T* e_scn,
-                       float* X, int k, const Dims& D, cudaStream_t s);
+                       float* X, T* Xb, float* part, int pld, int k, const Dims& D, cudaStream_t s);
 template <typename T>
 void launch_embed_cand(const int32_t* items, const int64_t* cand_off, const int* wave_r, int U, long long P,
-                       const T* e_item, const T* e_scn, float* C, int* err, const Dims& D, cudaStream_t s);
+                       const T* e_item, const T* e_scn, float* C, T* Cb, float* part, int pld, int* err,
+                       const Dims& D, cudaStream_t s);
 template <typename T>
 void launch_rmsnorm(const float* X, long long ldx, const float* g, T* out, long long ldo, long long rows, int d,
                     float eps, cudaStream_t s);
@@ -68,6 +69,7 @@ void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r,
 // tcgen05 GEMM (bf16 in, fp32 accumulate in TMEM), gemm_tc.cu.  Returns false
 // if the shape is not supported by the tensor-core kernel.
 bool gemm_tc_supported(long long M, int N, int K, long long lda, long long ldb);
+bool gemm_tc_available();
 void launch_gemm_tc(const bf16* A, long long lda, const bf16* B, long long ldb, long long M, int N, int K,
                     const Epilogue& e, cudaStream_t s);
 
