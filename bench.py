@@ -235,7 +235,8 @@ def roofline(prof, pk, pk_src, bf16=True):
         bound, unit = "tensor", "TFLOP/s"
         ach = p["flops"] / n / (ms_per_launch * 1e-3) / 1e12
         peak = pk["bf16_tflops_sustained"]
-        peak_note = f"bf16 dense, sustained ({pk_src}); kernel uses mma.sync m16n8k16"
+        peak_note = (f"bf16 dense, sustained ({pk_src}); tcgen05/TMEM flash attention (d_h 32/64), "
+                     f"mma.sync m16n8k16 fallback otherwise")
     elif dom in ("attn_sumi", "attn_hist"):
         # fp32 verification build: SIMT FMA; peak = 148 SM x 128 FP32 lanes x 2 FLOP x max SM clock
         bound, unit = "alu", "TFLOP/s"
