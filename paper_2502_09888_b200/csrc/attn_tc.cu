@@ -24,6 +24,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.cuh"
@@ -35,7 +37,7 @@ using namespace tcu;
 
 constexpr int ROWS = 128;
 constexpr int KEYS = PAGE;  // 64 keys per chunk = one K/V page
-constexpr int STAGES = 4;
+constexpr int STAGES = 3;
 constexpr int NSB = 3;      // TMEM score/P buffers
 constexpr int THREADS = 256;
 constexpr float LOG2E = 1.4426950408889634f;
@@ -57,7 +59,9 @@ struct Lay {
   static constexpr int Q_OFF = 0;
   static constexpr int Q_BYTES = ROWS * RB;
   static constexpr int KVB = KEYS * RB;                  // one K (or V) page slice of one head
-  static constexpr int KV_OFF = Q_OFF + Q_BYTES;         // stage s: K at KV_OFF + 2 s KVB, V at + KVB
+  static constexpr int KS_OFF = Q_OFF + Q_BYTES;         // SUMI: the tile's k_self rows (same swizzle as Q)
+  static constexpr int VS_OFF = KS_OFF + Q_BYTES;        // SUMI: the tile's v_self rows
+  static constexpr int KV_OFF = VS_OFF + Q_BYTES;        // stage s: K at KV_OFF + 2 s KVB, V at + KVB
   static constexpr int BAR_OFF = KV_OFF + 2 * STAGES * KVB;
   static constexpr int TOTAL = BAR_OFF + 512 + 1024;
   static constexpr int STG_OFF = KV_OFF;                 // epilogue staging reuses the K/V ring
@@ -74,7 +78,9 @@ struct Args {
   bf16* O;        // [rows][d]
   int k, l;
   Dims D;
+  unsigned long long* trace;  // debug timeline (CLIMBER_ATTN_TRACE), nullptr normally
 };
+constexpr int TRACE_N = 24;
 
 template <int DH, int MODE>
 __global__ void __launch_bounds__(THREADS, 2)
@@ -122,26 +128,6 @@ __global__ void __launch_bounds__(THREADS, 2)
   }
   const int n_chunks = (key_end + KEYS - 1) / KEYS;
 
-  // SUMI self term, issued before the prologue barrier so the row-strided
-  // global loads overlap barrier init / TMEM allocation: s_self = q . k_self,
-  // and v_self is prefetched into L2 for the O initialisation below.
-  float ss_pre = 0.f;
-  if (MODE == MODE_SUMI && warp >= 4) {
-    const int row = (warp - 4) * 32 + lane;
-    if (row < n_rows) {
-      const bf16* qp = a.Q + (row_base + row) * ldq + head * DH;
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(qp + 2 * D.d));
-#pragma unroll
-      for (int c = 0; c < DH; c += 8) {
-        float q[8], kk[8];
-        load8(qp + c, q);
-        load8(qp + D.d + c, kk);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) ss_pre = fmaf(q[i], kk[i], ss_pre);
-      }
-    }
-  }
-
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmQ) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmKV) : "memory");
@@ -162,17 +148,31 @@ __global__ void __launch_bounds__(THREADS, 2)
                  "r"(256));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  unsigned long long* tr = nullptr;
+  const bool tracer = a.trace != nullptr && threadIdx.x == 128;
+  if (tracer) {
+    tr = a.trace + ((long long)(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * TRACE_N;
+    tr[0] = clock64();
+  }
   fence_before();
   __syncthreads();
   fence_after();
+  if (tracer) tr[1] = clock64();
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t tO = tmem_base + NSB * KEYS;  // S/P buffers at tmem_base + b * KEYS
 
   if (warp == 0) {
-    if (lane == 0 && n_chunks > 0) {
+    if (lane == 0 && (n_chunks > 0 || MODE == MODE_SUMI)) {
       // ---------------- TMA producer ----------------
-      mbar_expect_tx(bar_q, Ly::Q_BYTES);
-      tma_load_2d(smem + Ly::Q_OFF, &tmQ, bar_q, head * DH, (int)row_base);
+      if (MODE == MODE_SUMI) {  // q, k_self, v_self of the tile's candidates
+        mbar_expect_tx(bar_q, 3 * Ly::Q_BYTES);
+        tma_load_2d(smem + Ly::Q_OFF, &tmQ, bar_q, head * DH, (int)row_base);
+        tma_load_2d(smem + Ly::KS_OFF, &tmQ, bar_q, D.d + head * DH, (int)row_base);
+        tma_load_2d(smem + Ly::VS_OFF, &tmQ, bar_q, 2 * D.d + head * DH, (int)row_base);
+      } else {
+        mbar_expect_tx(bar_q, Ly::Q_BYTES);
+        tma_load_2d(smem + Ly::Q_OFF, &tmQ, bar_q, head * DH, (int)row_base);
+      }
       for (int j = 0; j < n_chunks; ++j) {
         const int st = j % STAGES;
         mbar_wait(&kv_empty[st], ((j / STAGES) & 1) ^ 1);
@@ -229,12 +229,26 @@ __global__ void __launch_bounds__(THREADS, 2)
     const int row = ew * 32 + lane;  // query row = TMEM lane
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
     const bool valid = row < n_rows;
-    const long long grow = row_base + row;
     const int t_row = tile0 + row;
     float m_used, l;
     if (MODE == MODE_SUMI) {
-      const bf16* qp = a.Q + grow * ldq + head * DH;
-      m_used = ss_pre * sc;
+      // self term from the TMA-loaded q / k_self / v_self tiles (row = lane's
+      // row, 16-byte chunks XOR-swizzled like the TMA box: 128B or 64B pattern)
+      mbar_wait(bar_q, 0);
+      const uint8_t* qrow = smem + Ly::Q_OFF + row * Ly::RB;
+      const uint8_t* krow = smem + Ly::KS_OFF + row * Ly::RB;
+      const uint8_t* vrow = smem + Ly::VS_OFF + row * Ly::RB;
+      auto swz = [&](int j) { return (DH == 64) ? (j ^ (row & 7)) : (j ^ ((row >> 1) & 3)); };
+      float ss = 0.f;
+#pragma unroll
+      for (int j = 0; j < DH / 8; ++j) {
+        float q[8], kk[8];
+        load8(reinterpret_cast<const bf16*>(qrow + (swz(j) << 4)), q);
+        load8(reinterpret_cast<const bf16*>(krow + (swz(j) << 4)), kk);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ss = fmaf(q[i], kk[i], ss);
+      }
+      m_used = valid ? ss * sc : 0.f;
       l = 1.f;
 #pragma unroll
       for (int c = 0; c < DH; c += 32) {  // O = v_self
@@ -242,7 +256,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 #pragma unroll
         for (int cc = 0; cc < 32; cc += 8) {
           if (valid) {
-            load8(qp + 2 * D.d + c + cc, vs + cc);
+            load8(reinterpret_cast<const bf16*>(vrow + (swz((c + cc) / 8) << 4)), vs + cc);
           } else {
 #pragma unroll
             for (int i = 0; i < 8; ++i) vs[cc + i] = 0.f;
@@ -255,10 +269,12 @@ __global__ void __launch_bounds__(THREADS, 2)
       l = 0.f;
     }
     const bool causal_hist = (MODE == MODE_HIST) && D.causal;
+    if (tracer) tr[2] = clock64();
     for (int j = 0; j < n_chunks; ++j) {
       const uint32_t tSj = tmem_base + (j % NSB) * KEYS + lane_off;
       mbar_wait(&s_full[j % NSB], (j / NSB) & 1);
       fence_after();
+      if (tracer && j < 9) tr[3 + 2 * j] = clock64();
       const int key0 = j * KEYS;
       int lim = key_end - key0;  // keys [0, lim) of the chunk are visible to this row
       if (causal_hist) lim = min(lim, t_row - key0 + 1);
@@ -333,12 +349,14 @@ __global__ void __launch_bounds__(THREADS, 2)
       l += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
       fence_before();
       mbar_arrive(&p_full[j % NSB]);
+      if (tracer && j < 9) tr[4 + 2 * j] = clock64();
     }
     // ---- epilogue: O / l -> bf16, staged in smem for coalesced stores
     if (n_chunks > 0) {
       mbar_wait(&o_done[(n_chunks - 1) % NSB], ((n_chunks - 1) / NSB) & 1);
       fence_after();
     }
+    if (tracer) tr[21] = clock64();
     const float inv = (valid && l > 0.f) ? 1.f / l : 0.f;
     constexpr int LDS = DH + 8;
     bf16* stg = reinterpret_cast<bf16*>(smem + Ly::STG_OFF);  // K/V ring fully consumed (last PV done)
@@ -360,17 +378,20 @@ __global__ void __launch_bounds__(THREADS, 2)
       }
     }
     __syncwarp();
+    if (tracer) tr[23] = clock64();
     const int rows_out = (MODE == MODE_SUMI) ? n_rows : min(ROWS, D.nk - tile0);
-    constexpr int LPR = DH / 2;  // lanes per row, 2 bf16 each
-#pragma unroll 4
-    for (int i = 0; i < 32; i += 32 / LPR) {
+    constexpr int LPR = DH / 8;      // lanes per row, 16 B (8 bf16) each
+    constexpr int RPI = 32 / LPR;    // rows per warp instruction
+#pragma unroll
+    for (int i = 0; i < 32; i += RPI) {
       const int rr = ew * 32 + i + lane / LPR;
-      const int cc = (lane % LPR) * 2;
+      const int cc = (lane % LPR) * 8;
       if (rr < rows_out) {
-        const uint32_t val = *reinterpret_cast<const uint32_t*>(stg + rr * LDS + cc);
-        *reinterpret_cast<uint32_t*>(a.O + (row_base + rr) * D.d + head * DH + cc) = val;
+        const uint4 val = *reinterpret_cast<const uint4*>(stg + rr * LDS + cc);
+        *reinterpret_cast<uint4*>(a.O + (row_base + rr) * D.d + head * DH + cc) = val;
       }
     }
+    if (tracer) tr[22] = clock64();
   }
   fence_before();
   __syncthreads();
@@ -433,10 +454,38 @@ void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, 
   CUtensorMap mq, mkv;
   at::map2d(&mq, QKV, P, 3 * D.d, 3LL * D.d, D.dh, at::ROWS);
   at::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, at::KEYS);
-  at::Args a{QKV, cand_off, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, D};
+  at::Args a{QKV, cand_off, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, D, nullptr};
   dim3 grid((Mmax + at::ROWS - 1) / at::ROWS, D.h, U);
+  // debug timeline: CLIMBER_ATTN_TRACE=n records the n-th SUMI launch (clock64 per CTA)
+  static int trace_at = [] { const char* t = getenv("CLIMBER_ATTN_TRACE"); return t ? atoi(t) : -1; }();
+  static int n_launch = 0;
+  unsigned long long* tbuf = nullptr;
+  const long long n_cta = (long long)grid.x * grid.y * grid.z;
+  if (trace_at >= 0 && n_launch++ == trace_at) {
+    cudaMallocManaged(&tbuf, n_cta * at::TRACE_N * 8);
+    cudaMemset(tbuf, 0, n_cta * at::TRACE_N * 8);
+    a.trace = tbuf;
+  }
   if (D.dh == 64) at::launch<64, at::MODE_SUMI>(mq, mkv, a, grid, s);
   else at::launch<32, at::MODE_SUMI>(mq, mkv, a, grid, s);
+  if (tbuf) {
+    cudaStreamSynchronize(s);
+    double acc[at::TRACE_N] = {0};
+    long long cnt = 0;
+    for (long long c = 0; c < n_cta; ++c) {
+      unsigned long long* t = tbuf + c * at::TRACE_N;
+      if (!t[0] || !t[22]) continue;
+      ++cnt;
+      for (int i = 1; i < at::TRACE_N; ++i)
+        if (t[i]) acc[i] += (double)(t[i] - t[0]);
+    }
+    fprintf(stderr, "[attn trace] %lld CTAs; mean cycles since start: prologue %.0f init %.0f", cnt, acc[1] / cnt,
+            acc[2] / cnt);
+    for (int j = 0; j < 9; ++j)
+      if (acc[3 + 2 * j] > 0) fprintf(stderr, " | c%d S %.0f P %.0f", j, acc[3 + 2 * j] / cnt, acc[4 + 2 * j] / cnt);
+    fprintf(stderr, " | o_done %.0f staged %.0f end %.0f\n", acc[21] / cnt, acc[23] / cnt, acc[22] / cnt);
+    cudaFree(tbuf);
+  }
 }
 
 void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r, int U, const bf16* pool,
@@ -445,7 +494,7 @@ void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r,
   CUtensorMap mq, mkv;
   at::map2d(&mq, Q, (long long)U * D.nk, D.d, D.d, D.dh, at::ROWS);
   at::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, at::KEYS);
-  at::Args a{Q, nullptr, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, D};
+  at::Args a{Q, nullptr, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, D, nullptr};
   dim3 grid(D.nk / at::ROWS, D.h, U);
   if (D.dh == 64) at::launch<64, at::MODE_HIST>(mq, mkv, a, grid, s);
   else at::launch<32, at::MODE_HIST>(mq, mkv, a, grid, s);
