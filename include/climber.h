@@ -205,8 +205,33 @@ climber_status climber_rank_host(climber_ctx_t ctx, int32_t B, const int64_t* ev
  * work still reads it.  Double release -> CLIMBER_E_STALE. */
 climber_status climber_kv_release(climber_ctx_t ctx, climber_kv_t kv);
 
-/* Multi-GPU K/V replication for candidate sharding — NEXT;
- * returns CLIMBER_E_UNSUPPORTED in this build. */
+/* ---- multi-GPU candidate sharding (latency mode) ----
+ * The owner rank encodes the user, exports the handle's K/V pages into one
+ * contiguous DEVICE slab, the slab is replicated with a collective of the
+ * caller's process group (e.g. an NCCL broadcast over NVLink), and every other
+ * rank imports it into its own page pool; each rank then scores its shard of
+ * the candidates.  Slab layout: 256-byte header (int32 magic, abi, n_blocks,
+ * n_layers, pages per block, d, dtype, vlen[n_blocks]) followed by the
+ * handle's pages in page-table order ([2][64][d] elements each).  The slab is
+ * only meaningful to a ctx created with the same config. */
+
+/* Bytes of one user's slab for this ctx's config. */
+size_t climber_kv_slab_bytes(climber_ctx_t ctx);
+
+/* Gather the handle's pages into `slab` (DEVICE, >= climber_kv_slab_bytes).
+ * Asynchronous on `stream`. */
+climber_status climber_kv_export(climber_ctx_t ctx, climber_kv_t kv, void* slab, climber_stream_t stream);
+
+/* Allocate a handle in this ctx's pool and scatter the slab's pages into it.
+ * `scenario_r` is the request scenario the slab was encoded with (host
+ * state of the handle).  Asynchronous on `stream`; a slab whose header does not
+ * match this ctx's config sets the device error word (E_CONFIG is returned by
+ * climber_stream_status) and leaves the handle's scores NaN-free but invalid. */
+climber_status climber_kv_import(climber_ctx_t ctx, const void* slab, int32_t scenario_r,
+                                 climber_stream_t stream, climber_kv_t* out);
+
+/* In-library NCCL replication of a handle — not built: use kv_export + the
+ * caller's collective + kv_import.  Returns CLIMBER_E_UNSUPPORTED. */
 climber_status climber_kv_broadcast(climber_ctx_t ctx, climber_kv_t* kv, int32_t root,
                                     climber_stream_t stream);
 

@@ -84,6 +84,9 @@ def lib() -> C.CDLL:
             "climber_launch_count": (I64, [VP]),
             "climber_debug_gemm": (I32, [VP, VP, VP, I64, I32, I32, I32, I32, VP]),
             "climber_profile": (I32, [VP, I32]),
+            "climber_kv_slab_bytes": (C.c_size_t, [VP]),
+            "climber_kv_export": (I32, [VP, VP, VP, VP]),
+            "climber_kv_import": (I32, [VP, VP, I32, VP, P]),
             "climber_profile_read": (I32, [VP, P]),
         }
         for name, (res, args) in sig.items():
@@ -98,7 +101,8 @@ EXPORTED_SYMBOLS = ("climber_arena_bytes", "climber_create", "climber_destroy", 
                     "climber_encode_users", "climber_score_items", "climber_score_items_batched",
                     "climber_rank_host", "climber_kv_release", "climber_kv_broadcast", "climber_stream_status",
                     "climber_last_error", "climber_debug_extract", "climber_debug_mask", "climber_debug_kv",
-                    "climber_launch_count", "climber_debug_gemm", "climber_profile", "climber_profile_read")
+                    "climber_launch_count", "climber_debug_gemm", "climber_profile", "climber_profile_read",
+                    "climber_kv_slab_bytes", "climber_kv_export", "climber_kv_import")
 
 KERNEL_CLASSES = ("extract", "embed", "rmsnorm", "gemm_qkv", "gemm_o", "gemm_ffn_up", "gemm_ffn_down", "gemm_se",
                   "attn_hist", "attn_sumi", "attn_fusion", "head", "other")
@@ -280,6 +284,23 @@ class Climber:
         B = len(arrs[5])
         _check(lib().climber_rank_host(self.h, B, *[_ptr(a) for a in arrs], _ptr(scores), self._stream(stream)))
         return scores
+
+    # -- multi-GPU candidate sharding: K/V slab exchange ---------------------
+    @property
+    def slab_bytes(self) -> int:
+        return int(lib().climber_kv_slab_bytes(self.h))
+
+    def kv_export(self, handle, slab=None, stream=None):
+        """Gather the handle's K/V pages into a CUDA uint8 tensor (the slab)."""
+        if slab is None:
+            slab = self.torch.empty(self.slab_bytes, dtype=self.torch.uint8, device=self.arena.device)
+        _check(lib().climber_kv_export(self.h, C.c_void_p(handle), C.c_void_p(slab.data_ptr()), self._stream(stream)))
+        return slab
+
+    def kv_import(self, slab, r: int, stream=None) -> int:
+        out = C.c_void_p()
+        _check(lib().climber_kv_import(self.h, C.c_void_p(slab.data_ptr()), int(r), self._stream(stream), C.byref(out)))
+        return out.value
 
     def stream_status(self, stream=None):
         _check(lib().climber_stream_status(self.h, self._stream(stream)))

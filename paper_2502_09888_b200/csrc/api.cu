@@ -1031,7 +1031,71 @@ extern "C" climber_status climber_kv_release(climber_ctx_t c, climber_kv_t kv) {
 extern "C" climber_status climber_kv_broadcast(climber_ctx_t c, climber_kv_t* kv, int32_t root,
                                                climber_stream_t stream) {
   (void)c; (void)kv; (void)root; (void)stream;
-  return fail(CLIMBER_E_UNSUPPORTED, "climber_kv_broadcast: multi-GPU candidate sharding is NEXT (world == 1)");
+  return fail(CLIMBER_E_UNSUPPORTED,
+              "climber_kv_broadcast: use climber_kv_export + the caller's collective + climber_kv_import");
+}
+
+static size_t page_bytes(const climber_ctx_s* c) { return (size_t)2 * PAGE * c->D.d * c->esz; }
+
+extern "C" size_t climber_kv_slab_bytes(climber_ctx_t c) {
+  return c ? 256 + (size_t)c->per_slot * page_bytes(c) : 0;
+}
+
+extern "C" climber_status climber_kv_export(climber_ctx_t c, climber_kv_t kv, void* slab, climber_stream_t stream) {
+  if (!c || !slab) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+  if (reinterpret_cast<uintptr_t>(slab) % 16) return fail(CLIMBER_E_INVALID_ARG, "slab must be 16-byte aligned");
+  int slot;
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    climber_status rs = resolve(c, kv, &slot);
+    if (rs != CLIMBER_OK) return rs;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  {
+    Prof p(c, CLIMBER_K_OTHER, s, 0, 2.0 * c->per_slot * page_bytes(c));
+    launch_kv_export(c->pool, c->ptab, c->vlen_all, slot, c->per_slot, (long long)page_bytes(c), slab, c->D,
+                     c->cfg.dtype, s);
+  }
+  return check_launch(c, s);
+}
+
+extern "C" climber_status climber_kv_import(climber_ctx_t c, const void* slab, int32_t scenario_r,
+                                            climber_stream_t stream, climber_kv_t* out) {
+  if (!c || !slab || !out) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+  if (reinterpret_cast<uintptr_t>(slab) % 16) return fail(CLIMBER_E_INVALID_ARG, "slab must be 16-byte aligned");
+  if (scenario_r < 0 || scenario_r >= c->D.R) return fail(CLIMBER_E_OUT_OF_RANGE, "scenario_r out of range");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int slot;
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    if (c->free_slots.empty() || (long long)c->free_pages.size() < c->per_slot)
+      return fail(CLIMBER_E_CAPACITY, "K/V page pool exhausted");
+    CU(cudaEventSynchronize(c->stage_evt));
+    Stage h = stage_layout(c, c->h_stage);
+    slot = c->free_slots.back();
+    c->free_slots.pop_back();
+    SlotState& st = c->slots[slot];
+    st.live = true;
+    st.r = scenario_r;
+    st.pages.resize(c->per_slot);
+    for (int i = 0; i < c->per_slot; ++i) {
+      st.pages[i] = c->free_pages.back();
+      c->free_pages.pop_back();
+      h.ptab[i] = st.pages[i];
+    }
+    h.slots[0] = slot;
+    h.r[0] = scenario_r;
+    h.ev_off[0] = h.ev_off[1] = 0;
+    climber_status rs = stage_upload(c, 1, true, s);
+    if (rs != CLIMBER_OK) return rs;
+    *out = make_handle(c, slot, st.gen);
+  }
+  {
+    Prof p(c, CLIMBER_K_OTHER, s, 0, 2.0 * c->per_slot * page_bytes(c));
+    launch_kv_import(c->pool, c->ptab, c->vlen_all, slot, c->per_slot, (long long)page_bytes(c), slab, c->err, c->D,
+                     c->cfg.dtype, s);
+  }
+  return check_launch(c, s);
 }
 
 extern "C" climber_status climber_stream_status(climber_ctx_t c, climber_stream_t stream) {
@@ -1043,6 +1107,7 @@ extern "C" climber_status climber_stream_status(climber_ctx_t c, climber_stream_
   CU(cudaMemset(c->err, 0, 4));
   if (err & ERR_RANGE) return fail(CLIMBER_E_OUT_OF_RANGE, "an item/action/scenario id was out of range");
   if (err & ERR_UNSORTED) return fail(CLIMBER_E_UNSORTED, "a lifecycle sequence had decreasing timestamps");
+  if (err & ERR_CONFIG) return fail(CLIMBER_E_CONFIG, "an imported K/V slab did not match this ctx's config");
   return CLIMBER_OK;
 }
 

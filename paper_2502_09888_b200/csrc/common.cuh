@@ -18,7 +18,7 @@ struct Dims {
 };
 
 // Device error word bits (climber_stream_status maps them to statuses).
-enum : int { ERR_RANGE = 1, ERR_UNSORTED = 2 };
+enum : int { ERR_RANGE = 1, ERR_UNSORTED = 2, ERR_CONFIG = 4 };
 
 constexpr int PAGE = 64;  // tokens per K/V page
 

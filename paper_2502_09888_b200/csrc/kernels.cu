@@ -565,6 +565,56 @@ __global__ void k_debug_kv(const T* __restrict__ pool, const int* __restrict__ p
   }
 }
 
+// K/V slab export / import (multi-GPU candidate sharding): 16-byte copies of
+// the handle's pages in page-table order, behind a 256-byte header.
+constexpr int SLAB_MAGIC = 0x4B56534C;  // "KVSL"
+
+__global__ void k_kv_export(const uint4* __restrict__ pool, const int* __restrict__ ptab, const int* __restrict__ vlen_all,
+                            int slot, int per_slot, long long page_vec, int* __restrict__ hdr, uint4* __restrict__ body,
+                            Dims D, int dtype) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    hdr[0] = SLAB_MAGIC; hdr[1] = 1; hdr[2] = D.Nb; hdr[3] = D.L; hdr[4] = D.ppb; hdr[5] = D.d; hdr[6] = dtype;
+    for (int k = 0; k < D.Nb; ++k) hdr[8 + k] = vlen_all[(long long)slot * D.Nb + k];
+  }
+  const long long n = (long long)per_slot * page_vec;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += (long long)gridDim.x * blockDim.x) {
+    const long long i = g / page_vec, w = g % page_vec;
+    body[g] = pool[(long long)ptab[(long long)slot * per_slot + i] * page_vec + w];
+  }
+}
+
+__global__ void k_kv_import(uint4* __restrict__ pool, const int* __restrict__ ptab, int* __restrict__ vlen_all, int slot,
+                            int per_slot, long long page_vec, const int* __restrict__ hdr, const uint4* __restrict__ body,
+                            int* __restrict__ err, Dims D, int dtype) {
+  const bool ok = hdr[0] == SLAB_MAGIC && hdr[1] == 1 && hdr[2] == D.Nb && hdr[3] == D.L && hdr[4] == D.ppb &&
+                  hdr[5] == D.d && hdr[6] == dtype;
+  if (!ok) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      atomicOr(err, ERR_CONFIG);
+      for (int k = 0; k < D.Nb; ++k) vlen_all[(long long)slot * D.Nb + k] = 0;
+    }
+    return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < D.Nb) vlen_all[(long long)slot * D.Nb + threadIdx.x] = hdr[8 + threadIdx.x];
+  const long long n = (long long)per_slot * page_vec;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += (long long)gridDim.x * blockDim.x) {
+    const long long i = g / page_vec, w = g % page_vec;
+    pool[(long long)ptab[(long long)slot * per_slot + i] * page_vec + w] = body[g];
+  }
+}
+
+void launch_kv_export(const void* pool, const int* ptab, const int* vlen_all, int slot, int per_slot, long long page_bytes,
+                      void* slab, const Dims& D, int dtype, cudaStream_t s) {
+  k_kv_export<<<592, 256, 0, s>>>((const uint4*)pool, ptab, vlen_all, slot, per_slot, page_bytes / 16, (int*)slab,
+                                  (uint4*)((char*)slab + 256), D, dtype);
+}
+
+void launch_kv_import(void* pool, const int* ptab, int* vlen_all, int slot, int per_slot, long long page_bytes,
+                      const void* slab, int* err, const Dims& D, int dtype, cudaStream_t s) {
+  k_kv_import<<<592, 256, 0, s>>>((uint4*)pool, ptab, vlen_all, slot, per_slot, page_bytes / 16, (const int*)slab,
+                                  (const uint4*)((const char*)slab + 256), err, D, dtype);
+}
+
 // Scatter the staged page-table rows of a call into the per-slot table.
 __global__ void k_scatter_ptab(const int* __restrict__ staged, const int* __restrict__ slots, int B, int per,
                                int* __restrict__ ptab) {

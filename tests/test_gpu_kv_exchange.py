@@ -1,0 +1,87 @@
+"""K/V slab export/import (the multi-GPU candidate-sharding exchange) on one
+GPU: a user encoded in ctx A and imported into ctx B scores bit-identically;
+a slab from another config is rejected; the sharded driver runs on a
+world-size-1 NCCL group."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import synth
+from helpers import make_gpu, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def test_export_import_bitwise():
+    import torch
+    cfg = synth.preset("small")
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 5, B=1)
+    a = make_gpu(cfg, w, 1, kv_users=2)
+    b = make_gpu(cfg, w, 1, kv_users=2)
+    item, action, scenario, ts, cand = to_dev(batch)
+    ha = a.encode_user(item, action, scenario, ts, int(batch.r[0]))
+    sa = a.score_items(ha, cand).cpu().numpy()
+    slab = a.kv_export(ha)
+    hb = b.kv_import(slab, int(batch.r[0]))
+    sb = b.score_items(hb, cand).cpu().numpy()
+    torch.cuda.synchronize()
+    a.stream_status()
+    b.stream_status()
+    assert np.array_equal(sa, sb)
+    # the imported cache equals the original page by page
+    ia, va = a.debug_extract(ha)
+    for k in range(cfg.N_b):
+        for l in range(cfg.L):
+            Ka, Va = a.debug_kv(ha, l, k, int(va[k]))
+            Kb, Vb = b.debug_kv(hb, l, k, int(va[k]))
+            assert np.array_equal(Ka, Kb) and np.array_equal(Va, Vb)
+    a.release(ha)
+    b.release(hb)
+
+
+def test_slab_from_another_config_is_rejected():
+    from paper_2502_09888_b200 import ClimberError
+    cfg = synth.preset("small")
+    w = synth.make_weights(cfg, 0)
+    cl = make_gpu(cfg, w, 1)
+    other = make_gpu(synth.preset("small", L=1), synth.make_weights(synth.preset("small", L=1), 0), 1)
+    batch = synth.make_batch(cfg, 5, B=1)
+    item, action, scenario, ts, cand = to_dev(batch)
+    h = other.encode_user(item, action, scenario, ts, int(batch.r[0]))
+    slab = other.kv_export(h)
+    import torch
+    big = torch.zeros(cl.slab_bytes, dtype=torch.uint8, device="cuda")
+    big[:slab.numel()] = slab[:big.numel()]
+    h2 = cl.kv_import(big, int(batch.r[0]))
+    with pytest.raises(ClimberError) as ei:
+        cl.stream_status()
+    assert ei.value.name == "E_CONFIG"
+    cl.release(h2)
+
+
+def test_sharded_driver_world1_nccl():
+    import torch
+    import torch.distributed as dist
+    from paper_2502_09888_b200.sharded import ClimberBackend, rank_request_sharded
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        cfg = synth.preset("small")
+        w = synth.make_weights(cfg, 0)
+        batch = synth.make_batch(cfg, 6, B=1)
+        cl = make_gpu(cfg, w, 1, kv_users=2)
+        item, action, scenario, ts, cand = to_dev(batch)
+        out = rank_request_sharded(ClimberBackend(cl), dist, (item, action, scenario, ts), int(batch.r[0]), cand)
+        h = cl.encode_user(item, action, scenario, ts, int(batch.r[0]))
+        ref = cl.score_items(h, cand)
+        assert torch.equal(out, ref)
+        cl.release(h)
+    finally:
+        dist.destroy_process_group()

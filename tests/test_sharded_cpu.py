@@ -1,0 +1,104 @@
+"""Candidate sharding + K/V slab exchange protocol (paper_2502_09888_b200.sharded)
+with the gloo backend, world_size 2, on CPU.  The per-rank compute is the fp64
+oracle behind the same backend interface the libclimber adapter implements;
+the gathered scores must equal single-process oracle scores."""
+import os
+import pickle
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_shard_bounds_match_floor_rule():
+    from paper_2502_09888_b200.sharded import shard_bounds
+    for M in (1, 2, 7, 100, 1000, 1001):
+        for G in (1, 2, 3, 4, 8):
+            owner = [m * G // M for m in range(M)]
+            cover = []
+            for g in range(G):
+                lo, hi = shard_bounds(M, G, g)
+                assert all(owner[m] == g for m in range(lo, hi))
+                cover += list(range(lo, hi))
+            assert cover == list(range(M))
+
+
+class OracleBackend:
+    """The oracle behind the libclimber adapter's interface (CPU tensors)."""
+    SLAB = 1 << 22
+
+    def __init__(self, cfg, w, strats):
+        import torch
+        self.torch, self.cfg, self.w, self.strats = torch, cfg, w, strats
+        self.device = torch.device("cpu")
+        self.slab_bytes = self.SLAB
+
+    def encode(self, events, r):
+        import oracle as O
+        item, action, scenario = events
+        return O.encode_user(self.cfg, self.w, self.strats, item, action, scenario, r)
+
+    def export(self, cache, slab):
+        blob = pickle.dumps(cache)
+        slab[:8] = self.torch.tensor(list(len(blob).to_bytes(8, "little")), dtype=self.torch.uint8)
+        slab[8:8 + len(blob)] = self.torch.tensor(list(blob), dtype=self.torch.uint8)
+
+    def import_(self, slab, r):
+        n = int.from_bytes(bytes(slab[:8].tolist()), "little")
+        return pickle.loads(bytes(slab[8:8 + n].tolist()))
+
+    def score(self, cache, items):
+        import oracle as O
+        return self.torch.tensor(O.score_user(self.cfg, self.w, cache, items.numpy()), dtype=self.torch.float32)
+
+    def release(self, cache):
+        pass
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    import synth
+    from paper_2502_09888_b200.sharded import rank_request_sharded
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = synth.preset("tiny", L=2, M=7)
+    w = synth.make_weights(cfg, 0)
+    u = synth.make_user(cfg, np.random.default_rng(3), n_s=120, M=7)
+    item, action, scenario, _ = u.user_events(0)
+    be = OracleBackend(cfg, w, synth.strategies_for(cfg.N_b, cfg.R))
+    events = (item, action, scenario) if rank == 0 else None
+    out = rank_request_sharded(be, dist, events, int(u.r[0]), torch.from_numpy(u.user_cands(0)))
+    q.put((rank, None if out is None else out.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_candidate_sharding_matches_single_process():
+    sys.path.insert(0, ROOT)
+    import oracle as O
+    import synth
+    port = socket.socket()
+    port.bind(("127.0.0.1", 0))
+    p = port.getsockname()[1]
+    port.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, p, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=180) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert res[1] is None
+    cfg = synth.preset("tiny", L=2, M=7)
+    w = synth.make_weights(cfg, 0)
+    u = synth.make_user(cfg, np.random.default_rng(3), n_s=120, M=7)
+    ref = O.sumi_scores(cfg, w, synth.strategies_for(cfg.N_b, cfg.R), u, 0)
+    np.testing.assert_allclose(res[0], ref, rtol=0, atol=1e-6)   # fp32 transport of fp64 scores
