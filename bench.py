@@ -353,7 +353,7 @@ def main():
 
     # ---- per-request latency: one user, M candidates, host call to host scores ----
     lat = None
-    if rank == 0 and args.latency_requests > 0:
+    if args.latency_requests > 0 and world == 1:
         one = [batch.subset([b % B]) for b in range(args.latency_requests + 5)]
         tl = []
         for i, u in enumerate(one):
@@ -363,6 +363,27 @@ def main():
                 tl.append((time.perf_counter() - t0) * 1e3)
         lat = {"p50": float(np.percentile(tl, 50)), "p99": float(np.percentile(tl, 99)), "requests": len(tl),
                "mode": "single GPU per request (B=1, M candidates), climber_rank_host, no CUDA graph"}
+    elif args.latency_requests > 0:
+        # candidate sharding: owner encodes, K/V slab broadcast over
+        # the NCCL group, every rank scores floor(m G / M) == rank, scores gathered
+        from paper_2502_09888_b200.sharded import ClimberBackend, rank_request_sharded
+        be = ClimberBackend(cl)
+        tl = []
+        for i in range(args.latency_requests + 5):
+            u = batch.subset([i % B])
+            items = dev(u.cand)
+            dist.barrier()
+            t0 = time.perf_counter()
+            ev = (dev(u.item), dev(u.action), dev(u.scenario), dev(u.ts)) if rank == 0 else None
+            out = rank_request_sharded(be, dist, ev, int(u.r[0]), items)
+            if rank == 0:
+                out.cpu()
+                if i >= 5:
+                    tl.append((time.perf_counter() - t0) * 1e3)
+        if rank == 0:
+            lat = {"p50": float(np.percentile(tl, 50)), "p99": float(np.percentile(tl, 99)), "requests": len(tl),
+                   "mode": f"candidate-sharded over {world} GPUs: owner encodes, K/V slab broadcast (NCCL), "
+                           f"scores all_gather; host call to host scores"}
 
     if rank == 0:
         pk, pk_src = peaks()
