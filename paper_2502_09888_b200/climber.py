@@ -120,6 +120,9 @@ def debug_gemm(A, B, D, use_tc: bool = True, stream=None, epi: int = 0):
     s = stream if stream is not None else torch.cuda.current_stream()
     M, K = A.shape
     N = B.shape[0]
+    if epi == 3:  # grouped interleaved test mode: A [M][2K], B [2N][K]
+        K //= 2
+        N //= 2
     _check(lib().climber_debug_gemm(C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), C.c_void_p(D.data_ptr()),
                                     M, N, K, int(use_tc), int(epi), C.c_void_p(s.cuda_stream)))
 

@@ -1241,9 +1241,19 @@ extern "C" climber_status climber_debug_kv(climber_ctx_t c, climber_kv_t kv, int
 
 extern "C" climber_status climber_debug_gemm(const void* A, const void* B, void* D, int64_t M, int32_t N, int32_t K,
                                              int32_t use_tc, int32_t epi, climber_stream_t stream) {
-  if (!A || !B || !D || M < 1 || N < 1 || K < 1 || epi < 0 || epi > 2)
+  if (!A || !B || !D || M < 1 || N < 1 || K < 1 || epi < 0 || epi > 3)
     return fail(CLIMBER_E_INVALID_ARG, "bad argument");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (epi == 3) {
+    // grouped (2 interleaved blocks): A is [M][2][K] (block b = columns b*K..), B is [2][N][K],
+    // D is fp32 [M][2][N] += A_b B_b^T -- the candidate-block layout of the batched path
+    if (!use_tc || !gemm_tc_supported(M, N, K, 2 * K, K)) return fail(CLIMBER_E_UNSUPPORTED, "shape");
+    Epilogue e = epi_resid(reinterpret_cast<float*>(D), 2LL * N);
+    e.out_bs = N;
+    launch_gemm_tc_batched((const bf16*)A, 2LL * K, K, (const bf16*)B, K, (long long)N * K, M, N, K, 2, e, s);
+    CU(cudaGetLastError());
+    return CLIMBER_OK;
+  }
   Epilogue e = epi == 0 ? epi_resid(reinterpret_cast<float*>(D), N)
                         : epi_store(D, N, epi == 2 ? ACT_SILU : ACT_NONE);
   if (use_tc) {

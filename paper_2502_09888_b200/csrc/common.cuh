@@ -134,6 +134,10 @@ struct Epilogue {
   long long rs_rs;
   int rs_n;
   float rs_inv_d, rs_eps;
+  // batched (grouped over the N_b blocks) GEMMs: element strides between the
+  // batch entries of each output, and the block index taken from the batch
+  long long out_bs, out_b16_bs, part_bs, rs_bs;
+  int blk_from_batch;
 };
 
 // Page addressing: page = [2 (K,V)][PAGE tokens][d] elements (heads contiguous

@@ -16,6 +16,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -48,7 +49,7 @@ template <int BN, int STAGES, int EPIW, int SBUF, int NORM>
 __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmP,
-              const __grid_constant__ CUtensorMap tmC16, long long M, int N, int K, Epilogue e) {
+              const __grid_constant__ CUtensorMap tmC16, long long M, int N, int K, int batch, Epilogue e) {
   using S = Smem<BN, STAGES, EPIW, SBUF, NORM>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -62,7 +63,8 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = N / BN;
   const long long m_tiles = (M + BM - 1) / BM;
-  const long long num_tiles = m_tiles * n_tiles;
+  const long long tiles_per_b = m_tiles * n_tiles;
+  const long long num_tiles = tiles_per_b * batch;  // batch-major: t -> (b, m_blk, n_blk)
   const int kblocks = K / BK;
 
   if (warp == 0 && lane == 0) {
@@ -98,14 +100,16 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m_blk = (int)(t / n_tiles), n_blk = (int)(t % n_tiles);
+        const int bt = (int)(t / tiles_per_b);
+        const long long tr = t % tiles_per_b;
+        const int m_blk = (int)(tr / n_tiles), n_blk = (int)(tr % n_tiles);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::STAGE_BYTES;
           uint8_t* sb = sa + S::A_BYTES;
           mbar_expect_tx(&full[stage], S::STAGE_BYTES);
-          tma_load_2d(sa, &tmA, &full[stage], kb * BK, m_blk * BM);
-          tma_load_2d(sb, &tmB, &full[stage], kb * BK, n_blk * BN);
+          tma_load_3d(sa, &tmA, &full[stage], kb * BK, m_blk * BM, bt);
+          tma_load_3d(sb, &tmB, &full[stage], kb * BK, n_blk * BN, bt);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -168,15 +172,18 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       uint64_t* lb = ldbar + (warp - 4) * 2;
       uint32_t lph[2] = {0u, 0u};
       constexpr int NCH = BN / 32;
+      int bt = 0;
       auto issue = [&](long long r0, int n0, int set) {
         if (lane == 0) {
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging no longer read by stores
           mbar_expect_tx(&lb[set], 4096);
-          tma_load_2d(stg + set * 6144, &tmD, &lb[set], n0, (int)r0);
+          tma_load_3d(stg + set * 6144, &tmD, &lb[set], n0, (int)r0, bt);
         }
       };
       for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m_blk = (int)(t / n_tiles), n_blk = (int)(t % n_tiles);
+        bt = (int)(t / tiles_per_b);
+        const long long trm = t % tiles_per_b;
+        const int m_blk = (int)(trm / n_tiles), n_blk = (int)(trm % n_tiles);
         const long long row0 = (long long)m_blk * BM + ew * 32;
         const bool rows_ok = row0 < M;  // warp-uniform
         if (rows_ok) {  // the first two chunks of old residual are requested before the accumulator wait
@@ -222,27 +229,29 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&tmD, b, n0, (int)row0);
-              tma_store_2d(&tmC16, b + 4096, n0, (int)row0);
+              tma_store_3d(&tmD, b, n0, (int)row0, bt);
+              tma_store_3d(&tmC16, b + 4096, n0, (int)row0, bt);
               asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
           }
         }
-        if (rows_ok && row0 + lane < M) e.part[(row0 + lane) * e.part_rs + n_blk] = ss;
+        if (rows_ok && row0 + lane < M) e.part[bt * e.part_bs + (row0 + lane) * e.part_rs + n_blk] = ss;
         fence_before();
         mbar_arrive(&tempty[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     } else
     for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      const int m_blk = (int)(t / n_tiles), n_blk = (int)(t % n_tiles);
+      const int bt = (int)(t / tiles_per_b);
+      const long long trm = t % tiles_per_b;
+      const int m_blk = (int)(trm / n_tiles), n_blk = (int)(trm % n_tiles);
       const long long row0 = (long long)m_blk * BM + ew * 32;
       // RMSNorm folded into this GEMM: the per-row 1/rms from the producer's
       // partials, loaded before the accumulator wait so the latency is hidden
       float rsc = 1.f;
       if (e.rs_part != nullptr && row0 + lane < M) {
         float sum = 0.f;
-        for (int j = 0; j < e.rs_n; ++j) sum += e.rs_part[(row0 + lane) * e.rs_rs + j];
+        for (int j = 0; j < e.rs_n; ++j) sum += e.rs_part[bt * e.rs_bs + (row0 + lane) * e.rs_rs + j];
         rsc = rsqrtf(sum * e.rs_inv_d + e.rs_eps);
       }
       mbar_wait(&tfull[acc], acc_phase);
@@ -311,21 +320,22 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
           __syncwarp();
           if (lane == 0 && row0 < M) {
             if (e.kind == EPI_RESID) {
-              tma_reduce_add_2d(&tmD, buf, n0, (int)row0);
+              tma_reduce_add_3d(&tmD, buf, n0, (int)row0, bt);
             } else if (e.kind == EPI_QKV_PAGES) {
               const int cg = n0 + e.col_off;
               if (cg < e.d) {
-                tma_store_2d(&tmD, buf, cg, (int)row0);
+                tma_store_3d(&tmD, buf, cg, (int)row0, bt);
               } else {
                 const int kv = cg >= 2 * e.d ? 1 : 0;
                 const int cc = cg - e.d * (1 + kv);
                 const int u = (int)(row0 / e.nk), tt = (int)(row0 % e.nk);
                 const int slot = e.wave_slot[u];
-                const int page = e.ptab[(((long long)slot * e.Nb + e.blk) * e.L + e.layer) * e.ppb + tt / PAGE];
-                tma_store_2d(&tmP, buf, cc, (int)page_row(page, kv, tt % PAGE));
+                const int blk = e.blk_from_batch ? bt : e.blk;
+                const int page = e.ptab[(((long long)slot * e.Nb + blk) * e.L + e.layer) * e.ppb + tt / PAGE];
+                tma_store_3d(&tmP, buf, cc, (int)page_row(page, kv, tt % PAGE), 0);
               }
             } else {
-              tma_store_2d(&tmD, buf, n0, (int)row0);
+              tma_store_3d(&tmD, buf, n0, (int)row0, bt);
             }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
@@ -377,20 +387,26 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+// 3-D map [batch][rows][cols] (batch stride bs elements, may be < rows * ld for
+// interleaved views such as the N_b block slots of one candidate row)
 static bool make_map(CUtensorMap* map, const void* ptr, long long rows, int cols, long long ld, int box_rows,
-                     int box_cols = BK, bool f32 = false, bool sw64 = false) {
+                     int box_cols = BK, bool f32 = false, bool sw64 = false, int batch = 1, long long bs = 0) {
   auto enc = get_encode();
   if (!enc) return false;
   const int es = f32 ? 4 : 2;
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * es};
-  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+  if (batch <= 1) bs = rows * ld;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)(batch < 1 ? 1 : batch)};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * es, (cuuint64_t)bs * es};
+  cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
                    const_cast<void*>(ptr), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    fprintf(stderr, "[climber] cuTensorMapEncodeTiled failed (%d): rows %lld cols %d ld %lld batch %d bs %lld\n", (int)r,
+            rows, cols, ld, batch, bs);
   return r == CUDA_SUCCESS;
 }
 
@@ -406,25 +422,25 @@ static int num_sms() {
 }
 
 template <int BN, int STAGES, int EPIW, int SBUF, int NORM = 0>
-static void launch(const bf16* A, long long lda, const bf16* B, long long ldb, long long M, int N, int K,
-                   const Epilogue& e, cudaStream_t s) {
+static void launch(const bf16* A, long long lda, long long abs_, const bf16* B, long long ldb, long long bbs,
+                   long long M, int N, int K, int batch, const Epilogue& e, cudaStream_t s) {
   CUtensorMap ma, mb, md, mp, mc;
-  make_map(&ma, A, M, K, lda, BM);
-  make_map(&mb, B, N, K, ldb, BN);
+  make_map(&ma, A, M, K, lda, BM, BK, false, false, batch, abs_);
+  make_map(&mb, B, N, K, ldb, BN, BK, false, false, batch, bbs);
   mp = ma;  // unused unless QKV_PAGES
   mc = ma;  // unused unless RESID_NORM
-  if (e.kind == EPI_RESID_NORM) make_map(&mc, e.out_b16, M, N, e.ldo, 32, 32, false, true);
+  if (e.kind == EPI_RESID_NORM) make_map(&mc, e.out_b16, M, N, e.ldo, 32, 32, false, true, batch, e.out_b16_bs);
   if (e.kind == EPI_QKV_PAGES) {
     if (e.d % 64 == 0) {
-      make_map(&md, e.out, M, e.d, e.ldo, 32, 64, false);          // Q buffer [M][d]
-      make_map(&mp, e.pool, e.pool_rows, e.d, e.d, 32, 64, false);  // pages as [n_pages*2*64][d]
+      make_map(&md, e.out, M, e.d, e.ldo, 32, 64, false, false, batch, e.out_bs);  // Q buffer [b][M][d]
+      make_map(&mp, e.pool, e.pool_rows, e.d, e.d, 32, 64, false);                  // pages as [n_pages*2*64][d]
     } else {
       md = ma;
     }
   } else if (e.kind == EPI_STORE) {
-    make_map(&md, e.out, M, N, e.ldo, 32, 64, false);
+    make_map(&md, e.out, M, N, e.ldo, 32, 64, false, false, batch, e.out_bs);
   } else {
-    make_map(&md, e.out, M, N, e.ldo, 32, 32, true);
+    make_map(&md, e.out, M, N, e.ldo, 32, 32, true, false, batch, e.out_bs);
   }
   constexpr int smem = Smem<BN, STAGES, EPIW, SBUF, NORM>::TOTAL;
   static_assert(smem <= 232448, "smem");
@@ -433,9 +449,9 @@ static void launch(const bf16* A, long long lda, const bf16* B, long long ldb, l
     cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, EPIW, SBUF, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  long long tiles = ((M + BM - 1) / BM) * (N / BN);
+  long long tiles = ((M + BM - 1) / BM) * (N / BN) * batch;
   int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  k_gemm_tc<BN, STAGES, EPIW, SBUF, NORM><<<grid, 128 + 32 * EPIW, smem, s>>>(ma, mb, md, mp, mc, M, N, K, e);
+  k_gemm_tc<BN, STAGES, EPIW, SBUF, NORM><<<grid, 128 + 32 * EPIW, smem, s>>>(ma, mb, md, mp, mc, M, N, K, batch, e);
 }
 
 }  // namespace tc
@@ -448,8 +464,8 @@ bool gemm_tc_supported(long long M, int N, int K, long long lda, long long ldb) 
 
 bool gemm_tc_available() { return tc::get_encode() != nullptr; }
 
-void launch_gemm_tc(const bf16* A, long long lda, const bf16* B, long long ldb, long long M, int N, int K,
-                    const Epilogue& e, cudaStream_t s) {
+void launch_gemm_tc_batched(const bf16* A, long long lda, long long a_bs, const bf16* B, long long ldb,
+                            long long b_bs, long long M, int N, int K, int batch, const Epilogue& e, cudaStream_t s) {
   // Variant per epilogue cost (measured with tools/bench_gemm.py on B200):
   //   1: 4 epilogue warps, 4 stages, double-buffered staging (plain store, residual)
   //   2: 8 epilogue warps, 3 stages, double-buffered staging
@@ -461,20 +477,27 @@ void launch_gemm_tc(const bf16* A, long long lda, const bf16* B, long long ldb, 
     forced = v ? atoi(v) : 0;
   }
   if (e.kind == EPI_RESID_NORM) {  // N % 128 == 0 (checked by the caller)
-    if (N % 256 == 0) tc::launch<256, 3, 4, 2, 1>(A, lda, B, ldb, M, N, K, e, s);
-    else tc::launch<128, 4, 4, 2, 1>(A, lda, B, ldb, M, N, K, e, s);
+    if (N % 256 == 0) tc::launch<256, 3, 4, 2, 1>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+    else tc::launch<128, 4, 4, 2, 1>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
     return;
   }
   const bool heavy = (e.kind == EPI_STORE || e.kind == EPI_STORE_F32) && e.act != ACT_NONE;
   int var = forced ? forced : (heavy ? 3 : 1);
   if (N % 256 == 0) {
-    if (var == 1) tc::launch<256, 4, 4, 2>(A, lda, B, ldb, M, N, K, e, s);
-    else if (var == 2) tc::launch<256, 3, 8, 2>(A, lda, B, ldb, M, N, K, e, s);
-    else tc::launch<256, 4, 8, 1>(A, lda, B, ldb, M, N, K, e, s);
+    if (var == 1) tc::launch<256, 4, 4, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+    else if (var == 2) tc::launch<256, 3, 8, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+    else tc::launch<256, 4, 8, 1>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
   } else {
-    if (var == 1) tc::launch<128, 6, 4, 2>(A, lda, B, ldb, M, N, K, e, s);
-    else tc::launch<128, 5, 8, 2>(A, lda, B, ldb, M, N, K, e, s);
+    if (var == 1) tc::launch<128, 6, 4, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+    else tc::launch<128, 5, 8, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
   }
 }
 
+}  // namespace climber
+
+namespace climber {
+void launch_gemm_tc(const bf16* A, long long lda, const bf16* B, long long ldb, long long M, int N, int K,
+                    const Epilogue& e, cudaStream_t s) {
+  launch_gemm_tc_batched(A, lda, 0, B, ldb, 0, M, N, K, 1, e, s);
+}
 }  // namespace climber

@@ -76,5 +76,9 @@ bool gemm_tc_supported(long long M, int N, int K, long long lda, long long ldb);
 bool gemm_tc_available();
 void launch_gemm_tc(const bf16* A, long long lda, const bf16* B, long long ldb, long long M, int N, int K,
                     const Epilogue& e, cudaStream_t s);
+// grouped over `batch` independent GEMMs (the N_b blocks): A_b = A + b * a_bs,
+// B_b = B + b * b_bs, outputs offset by the Epilogue's *_bs strides
+void launch_gemm_tc_batched(const bf16* A, long long lda, long long a_bs, const bf16* B, long long ldb,
+                            long long b_bs, long long M, int N, int K, int batch, const Epilogue& e, cudaStream_t s);
 
 }  // namespace climber

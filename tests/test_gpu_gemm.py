@@ -42,3 +42,23 @@ def test_gemm_store_epilogues(M, N, K, epi):
         ref = F.silu(ref)
     err = (D.cpu().double() - ref).abs().max().item()
     assert err < 2e-2 * max(1.0, ref.abs().max().item()), err
+
+
+@pytest.mark.parametrize("M,N,K", [(1000, 512, 512), (300, 256, 128)])
+def test_gemm_grouped_interleaved(M, N, K):
+    """Two GEMMs in one launch over an interleaved [M][2][K] A (the N_b block
+    slots of candidate rows): D[:, b] += A[:, b] @ B[b]^T."""
+    import torch
+    from paper_2502_09888_b200.climber import debug_gemm
+    g = torch.Generator().manual_seed(M + N)
+    A = torch.randn(M, 2, K, generator=g).bfloat16()
+    B = torch.randn(2, N, K, generator=g).bfloat16()
+    D0 = torch.randn(M, 2, N, generator=g)
+    D = D0.clone().cuda()
+    debug_gemm(A.cuda().view(M, 2 * K), B.cuda().view(2 * N, K), D, epi=3)
+    torch.cuda.synchronize()
+    ref = D0.double().clone()
+    for b in range(2):
+        ref[:, b] += A[:, b].double() @ B[b].double().T
+    err = (D.cpu().double() - ref).abs().max().item()
+    assert err < K * 2.0 ** -22 * 16, err
