@@ -203,7 +203,7 @@ static void carve(climber_ctx_s* c, Carver& cv) {
   cv.take(c->d_r, Bm * 4);
   cv.take(c->d_ptab_stage, Bm * c->per_slot * 4);
   // scratch
-  long long rows_h = (long long)c->cfg.max_wave_users * D.nk;
+  long long rows_h = (long long)c->cfg.max_wave_users * D.nk * D.Nb;  // grouped encode: all blocks at once
   long long rows_c = (long long)c->cfg.max_wave_pairs * D.Nb;
   c->rows_cap = rows_h > rows_c ? rows_h : rows_c;
   size_t R = (size_t)c->rows_cap;
@@ -823,6 +823,177 @@ static void score_wave_fused(climber_ctx_s* c, const int32_t* items, const int64
 }
 
 // ---------------------------------------------------------------------------
+// grouped fused path: each GEMM / attention launch covers all N_b blocks of a
+// layer (3-D TMA maps, block = batch index), so small waves and single
+// requests fill the GPU with 8x fewer launches (SURVEY K5 "grouped over k").
+// ---------------------------------------------------------------------------
+static void gemm_g(climber_ctx_s* c, int cls, const bf16* A, long long lda, long long a_bs, const bf16* B,
+                   long long ldb, long long b_bs, long long M, int N, int K, int batch, const Epilogue& e,
+                   cudaStream_t s) {
+  Prof p(c, cls, s, 2.0 * M * N * K * batch);
+  launch_gemm_tc_batched(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+}
+
+// debug bisection: CLIMBER_GROUPED_MASK bit i = 0 runs stage i per block
+// (bit 0 QKV, 1 SUMI attention, 2 O-proj, 3 FFN-up, 4 FFN-down)
+static int grouped_mask() {
+  const char* m = getenv("CLIMBER_GROUPED_MASK");
+  return m ? atoi(m) : 31;
+}
+static Epilogue shift_epi(Epilogue e, long long k) {
+  if (e.out) e.out = (char*)e.out + k * e.out_bs * ((e.kind == EPI_STORE || e.kind == EPI_QKV_PAGES) ? 2 : 4);
+  if (e.out_b16) e.out_b16 = (char*)e.out_b16 + k * e.out_b16_bs * 2;
+  if (e.part) e.part += k * e.part_bs;
+  if (e.rs_part) e.rs_part += k * e.rs_bs;
+  return e;
+}
+static void gemm_stage(climber_ctx_s* c, int bit, int cls, const bf16* A, long long lda, long long a_bs, const bf16* B,
+                       long long ldb, long long b_bs, long long M, int N, int K, int batch, const Epilogue& e,
+                       cudaStream_t s) {
+  if (grouped_mask() & bit) {
+    gemm_g(c, cls, A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+  } else {
+    for (int k = 0; k < batch; ++k)
+      gemm_g(c, cls, A + k * a_bs, lda, 0, B + k * b_bs, ldb, 0, M, N, K, 1, shift_epi(e, k), s);
+  }
+}
+
+static bool grouped_ok(const climber_ctx_s* c) {
+  const char* g = getenv("CLIMBER_GROUPED");
+  return c->fused && c->attn_mode == 2 && attn_tc_supported(c->D.dh, c->D.nk, false) && !(g && atoi(g) == 0);
+}
+
+static void encode_wave_grouped(climber_ctx_s* c, const EventsDev& ev, int u0, int U, long long n_events,
+                                cudaStream_t s) {
+  const Dims& D = c->D;
+  const long long rows = (long long)U * D.nk;  // per block
+  const long long d = D.d, F = D.F, pld = c->pld, Nb = D.Nb, Lk = D.L;
+  const int* wslot = c->d_slots + u0;
+  const int* wr = c->d_r + u0;
+  {
+    Prof p(c, CLIMBER_K_EXTRACT, s, 0, (double)n_events * 14 + (double)U * D.Nb * D.nk * 4);
+    launch_extract(ev, c->d_ev_off + u0, wslot, U, c->amask, c->smask, c->idx_all, c->vlen_all, c->bad_all, c->err,
+                   D, s);
+  }
+  bf16* Xb = (bf16*)c->Xb;   // [Nb][rows][d]
+  bf16* Qb = (bf16*)c->QKV;  // [Nb][rows][d]
+  bf16* O = (bf16*)c->O;     // [Nb][rows][d]
+  bf16* Fh = (bf16*)c->Fh;   // [Nb][rows][F]
+  float* X = c->X;           // [Nb][rows][d]
+  const double causal_pairs = D.causal ? (double)D.nk * (D.nk + 1) / 2 : (double)D.nk * D.nk;
+  for (int k = 0; k < D.Nb; ++k) {
+    Prof p(c, CLIMBER_K_EMBED, s, 0, (double)rows * d * (3 * 2 + 4 + 2));
+    launch_embed_hist<bf16>(ev, c->d_ev_off + u0, wslot, U, c->idx_all, c->vlen_all, c->bad_all,
+                            (const bf16*)c->e_item, (const bf16*)c->e_act, (const bf16*)c->e_scn, X + k * rows * d,
+                            Xb + k * rows * d, c->part + k * rows * pld, c->pld, k, D, s);
+  }
+  for (int l = 0; l < D.L; ++l) {
+    Epilogue e{};
+    e.kind = EPI_QKV_PAGES; e.out = Qb; e.ldo = d; e.out_bs = rows * d; e.pool = c->pool; e.ptab = c->ptab;
+    e.wave_slot = wslot; e.pool_rows = c->n_pages * 2 * PAGE; e.blk_from_batch = 1;
+    e.blk = 0; e.layer = l; e.d = D.d; e.h = D.h; e.dh = D.dh; e.nk = D.nk; e.Nb = D.Nb; e.L = D.L; e.ppb = D.ppb;
+    e = with_rs(e, c, c->part, pld);
+    e.rs_bs = rows * pld;
+    const bf16* Wqkv = (const bf16*)c->w_qkv + (size_t)l * 3 * d * d;  // block k at + k * L * 3d * d
+    if (l < D.L - 1) {
+      e.col_off = 0;
+      gemm_g(c, CLIMBER_K_GEMM_QKV, Xb, d, rows * d, Wqkv, d, Lk * 3 * d * d, rows, 3 * D.d, D.d, D.Nb, e, s);
+      {
+        Prof p(c, CLIMBER_K_ATTN_HIST, s, 4.0 * U * causal_pairs * d * Nb, (double)rows * d * 2 * 4 * Nb);
+        launch_attn_hist_tc(Qb, wslot, wr, U, (const bf16*)c->pool, c->n_pages * 2 * PAGE, c->ptab, c->vlen_all,
+                            c->tau, O, 0, l, D, s, D.Nb);
+      }
+      Epilogue eo = epi_resid_norm(X, d, Xb, c->part, pld);
+      eo.out_bs = rows * d; eo.out_b16_bs = rows * d; eo.part_bs = rows * pld;
+      gemm_g(c, CLIMBER_K_GEMM_O, O, d, rows * d, (const bf16*)c->w_o + (size_t)l * d * d, d, Lk * d * d, rows,
+             D.d, D.d, D.Nb, eo, s);
+      Epilogue eu = with_rs(epi_store(Fh, F, ACT_SILU), c, c->part, pld);
+      eu.out_bs = rows * F; eu.rs_bs = rows * pld;
+      gemm_g(c, CLIMBER_K_GEMM_FFN_UP, Xb, d, rows * d, (const bf16*)c->w1 + (size_t)l * F * d, d, Lk * F * d, rows,
+             D.F, D.d, D.Nb, eu, s);
+      gemm_g(c, CLIMBER_K_GEMM_FFN_DOWN, Fh, F, rows * F, (const bf16*)c->w2 + (size_t)l * d * F, F, Lk * d * F,
+             rows, D.d, D.F, D.Nb, eo, s);
+    } else {
+      e.col_off = D.d;  // last layer: only K/V of the history are ever read
+      gemm_g(c, CLIMBER_K_GEMM_QKV, Xb, d, rows * d, Wqkv + d * d, d, Lk * 3 * d * d, rows, 2 * D.d, D.d, D.Nb, e,
+             s);
+    }
+  }
+}
+
+static void score_wave_grouped(climber_ctx_s* c, const int32_t* items, const int64_t* wcand, int u0, int U,
+                               long long P, int Mmax_wave, float* scores, cudaStream_t s) {
+  const Dims& D = c->D;
+  const long long d = D.d, F = D.F, Nb = D.Nb, ldC = Nb * d, pld = c->pld, Lk = D.L;
+  const int* wslot = c->d_slots + u0;
+  const int* wr = c->d_r + u0;
+  bf16* Cb = (bf16*)c->Xb;   // [p][k][d] (interleaved blocks)
+  bf16* QKV = (bf16*)c->QKV; // [k][p][3d]
+  bf16* O = (bf16*)c->O;     // [k][p][d]
+  bf16* Fh = (bf16*)c->Fh;   // [k][p][F]
+  float* C = c->X;           // [p][k][d]
+  {
+    Prof p(c, CLIMBER_K_EMBED, s, 0, (double)P * d * (2 * 2 + 6 * Nb));
+    launch_embed_cand<bf16>(items, wcand, wr, U, P, (const bf16*)c->e_item, (const bf16*)c->e_scn, C, Cb, c->part,
+                            c->pld, c->err, D, s);
+  }
+  // candidate rows of block k: row p at (p * Nb + k) -> batch stride d (elements), partials stride pld
+  for (int l = 0; l < D.L; ++l) {
+    Epilogue eq = with_rs(epi_store(QKV, 3 * d), c, c->part, Nb * pld);
+    eq.out_bs = P * 3 * d; eq.rs_bs = pld;
+    gemm_stage(c, 1, CLIMBER_K_GEMM_QKV, Cb, ldC, d, (const bf16*)c->w_qkv + (size_t)l * 3 * d * d, d, Lk * 3 * d * d, P,
+           3 * D.d, D.d, D.Nb, eq, s);
+    {
+      Prof p(c, CLIMBER_K_ATTN_SUMI, s, 4.0 * P * (D.nk + 1) * d * Nb,
+             ((double)P * d * 2 * 4 + (double)U * D.nk * d * 4) * Nb);
+      if (grouped_mask() & 2) {
+        launch_attn_sumi_tc(QKV, P, wcand, wslot, wr, U, Mmax_wave, (const bf16*)c->pool, c->n_pages * 2 * PAGE,
+                            c->ptab, c->vlen_all, c->tau, O, 0, l, D, s, D.Nb);
+      } else {
+        for (int k = 0; k < D.Nb; ++k)
+          launch_attn_sumi_tc(QKV + k * P * 3 * d, P, wcand, wslot, wr, U, Mmax_wave, (const bf16*)c->pool,
+                              c->n_pages * 2 * PAGE, c->ptab, c->vlen_all, c->tau, O + k * P * d, k, l, D, s, 1);
+      }
+    }
+    Epilogue eo = epi_resid_norm(C, ldC, Cb, c->part, Nb * pld);
+    eo.out_bs = d; eo.out_b16_bs = d; eo.part_bs = pld;
+    gemm_stage(c, 4, CLIMBER_K_GEMM_O, O, d, P * d, (const bf16*)c->w_o + (size_t)l * d * d, d, Lk * d * d, P, D.d, D.d,
+           D.Nb, eo, s);
+    Epilogue eu = with_rs(epi_store(Fh, F, ACT_SILU), c, c->part, Nb * pld);
+    eu.out_bs = P * F; eu.rs_bs = pld;
+    gemm_stage(c, 8, CLIMBER_K_GEMM_FFN_UP, Cb, ldC, d, (const bf16*)c->w1 + (size_t)l * F * d, d, Lk * F * d, P, D.F, D.d,
+           D.Nb, eu, s);
+    gemm_stage(c, 16, CLIMBER_K_GEMM_FFN_DOWN, Fh, F, P * F, (const bf16*)c->w2 + (size_t)l * d * F, F, Lk * d * F, P, D.d,
+           D.F, D.Nb, eo, s);
+  }
+  // ---- BGF (Eq. 4) + SE gate + head: identical to the per-block fused path
+  const long long R = P * Nb;
+  gemm<bf16>(c, CLIMBER_K_GEMM_QKV, Cb, d, (const bf16*)c->fw_qkv, d, R, 3 * D.d, D.d,
+             with_rs(epi_store(QKV, 3 * d), c, c->part, pld), s);
+  {
+    Prof p(c, CLIMBER_K_ATTN_FUSION, s, 4.0 * P * Nb * Nb * d, (double)R * d * 2 * 4);
+    launch_attn_fusion<bf16>(QKV, wcand, wr, U, P, c->tau_f, O, D, s);
+  }
+  gemm<bf16>(c, CLIMBER_K_GEMM_O, O, d, (const bf16*)c->fw_o, d, R, D.d, D.d, epi_resid_norm(C, d, Cb, c->part, pld),
+             s);
+  gemm<bf16>(c, CLIMBER_K_GEMM_FFN_UP, Cb, d, (const bf16*)c->fw1, d, R, D.F, D.d,
+             with_rs(epi_store(Fh, F, ACT_SILU), c, c->part, pld), s);
+  gemm<bf16>(c, CLIMBER_K_GEMM_FFN_DOWN, Fh, F, (const bf16*)c->fw2, F, R, D.d, D.F,
+             epi_resid_norm(C, d, Cb, c->part, pld), s);
+  bf16* Z1 = O;
+  gemm<bf16>(c, CLIMBER_K_GEMM_SE, Cb, D.Dse, (const bf16*)c->w_se1, D.Dse, P, D.Hse, D.Dse,
+             epi_store(Z1, D.Hse, ACT_RELU, c->b_se1), s);
+  float* gate = reinterpret_cast<float*>(c->Fh);
+  Epilogue eg{};
+  eg.kind = EPI_STORE_F32; eg.act = ACT_SIGMOID; eg.out = gate; eg.ldo = D.Dse; eg.bias = c->b_se2;
+  gemm<bf16>(c, CLIMBER_K_GEMM_SE, Z1, D.Hse, (const bf16*)c->w_se2, D.Hse, P, D.Dse, D.Hse, eg, s);
+  {
+    Prof p(c, CLIMBER_K_HEAD, s, 3.0 * P * D.Dse, (double)P * D.Dse * 8 + P * 4);
+    launch_head(C, gate, c->w_head, c->b_head, scores, P, D.Dse, s);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // staging of per-call metadata (one H2D copy per call, pinned buffer reused
 // only after the previous call's copy completed)
 // ---------------------------------------------------------------------------
@@ -921,7 +1092,9 @@ extern "C" climber_status climber_encode_users(climber_ctx_t c, int32_t B, const
     for (int u0 = 0; u0 < B; u0 += c->cfg.max_wave_users) {
       int U = B - u0 < c->cfg.max_wave_users ? B - u0 : c->cfg.max_wave_users;
       long long nev = ev_offsets[u0 + U] - ev_offsets[u0];
-      if (c->fused) encode_wave_fused(c, ev, u0, U, nev, s);
+      if (c->fused && grouped_ok(c) && attn_tc_supported(c->D.dh, c->D.nk, true))
+        encode_wave_grouped(c, ev, u0, U, nev, s);
+      else if (c->fused) encode_wave_fused(c, ev, u0, U, nev, s);
       else if (c->cfg.dtype == CLIMBER_BF16) encode_wave<bf16>(c, ev, u0, U, nev, s);
       else encode_wave<float>(c, ev, u0, U, nev, s);
       climber_status rs = check_launch(c, s);
@@ -994,7 +1167,8 @@ extern "C" climber_status climber_score_items_batched(climber_ctx_t c, int32_t B
       const int32_t* it = items + cand_offsets[w.u0];
       float* sc = scores + cand_offsets[w.u0];
       const int64_t* wc = c->d_cand_off + w.coff;
-      if (c->fused) score_wave_fused(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
+      if (c->fused && grouped_ok(c)) score_wave_grouped(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
+      else if (c->fused) score_wave_fused(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
       else if (c->cfg.dtype == CLIMBER_BF16) score_wave<bf16>(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
       else score_wave<float>(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
       climber_status rs = check_launch(c, s);

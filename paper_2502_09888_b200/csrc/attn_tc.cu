@@ -76,7 +76,9 @@ struct Args {
   const int* vlen_all;
   const float* tau;
   bf16* O;        // [rows][d]
-  int k, l;
+  int k, l;       // first block, layer
+  int U;          // users in the wave
+  long long rows_pb;  // grouped over nbk blocks: block kk's rows start at kk * rows_pb in Q/QKV and O
   Dims D;
   unsigned long long* trace;  // debug timeline (CLIMBER_ATTN_TRACE), nullptr normally
 };
@@ -101,13 +103,15 @@ __global__ void __launch_bounds__(THREADS, 2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NSB);
 
   const Dims& D = a.D;
-  const int u = blockIdx.z, head = blockIdx.y, tile0 = blockIdx.x * ROWS;  // tiles of one (u, h) adjacent
+  const int u = blockIdx.z % a.U, head = blockIdx.y, tile0 = blockIdx.x * ROWS;  // tiles of one (u, h) adjacent
+  const int kk = blockIdx.z / a.U;  // block within a grouped launch
+  const int kblk = a.k + kk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = a.wave_slot[u];
   const int r = a.wave_r[u];
-  const int v = a.vlen_all[(long long)slot * D.Nb + a.k];
-  const int* pages = a.ptab + (((long long)slot * D.Nb + a.k) * D.L + a.l) * D.ppb;
-  const float sc = LOG2E / (sqrtf((float)DH) * a.tau[((a.l * D.Nb + a.k) * D.R + r) * D.h + head]);
+  const int v = a.vlen_all[(long long)slot * D.Nb + kblk];
+  const int* pages = a.ptab + (((long long)slot * D.Nb + kblk) * D.L + a.l) * D.ppb;
+  const float sc = LOG2E / (sqrtf((float)DH) * a.tau[((a.l * D.Nb + kblk) * D.R + r) * D.h + head]);
 
   long long row_base;
   int n_rows, key_end;
@@ -115,13 +119,13 @@ __global__ void __launch_bounds__(THREADS, 2)
   if (MODE == MODE_SUMI) {
     const long long p0 = a.cand_off[u], p1 = a.cand_off[u + 1];
     if (p0 + tile0 >= p1) return;  // CTA-uniform
-    row_base = p0 + tile0;
-    n_rows = (int)((p1 - row_base) < ROWS ? (p1 - row_base) : ROWS);
+    row_base = kk * a.rows_pb + p0 + tile0;
+    n_rows = (int)((p1 - p0 - tile0) < ROWS ? (p1 - p0 - tile0) : ROWS);
     key_end = v;
     ldq = 3LL * D.d;
   } else {
     if (tile0 >= D.nk) return;
-    row_base = (long long)u * D.nk + tile0;
+    row_base = kk * a.rows_pb + (long long)u * D.nk + tile0;
     n_rows = max(0, min(ROWS, v - tile0));
     key_end = D.causal ? min(v, tile0 + ROWS) : v;
     ldq = D.d;
@@ -450,12 +454,13 @@ bool attn_tc_supported(int dh, int nk, bool hist) {
 
 void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, const int* wave_slot,
                          const int* wave_r, int U, int Mmax, const bf16* pool, long long pool_rows, const int* ptab,
-                         const int* vlen_all, const float* tau, bf16* O, int k, int l, const Dims& D, cudaStream_t s) {
+                         const int* vlen_all, const float* tau, bf16* O, int k, int l, const Dims& D, cudaStream_t s,
+                         int nbk) {
   CUtensorMap mq, mkv;
-  at::map2d(&mq, QKV, P, 3 * D.d, 3LL * D.d, D.dh, at::ROWS);
+  at::map2d(&mq, QKV, P * nbk, 3 * D.d, 3LL * D.d, D.dh, at::ROWS);
   at::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, at::KEYS);
-  at::Args a{QKV, cand_off, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, D, nullptr};
-  dim3 grid((Mmax + at::ROWS - 1) / at::ROWS, D.h, U);
+  at::Args a{QKV, cand_off, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, U, P, D, nullptr};
+  dim3 grid((Mmax + at::ROWS - 1) / at::ROWS, D.h, U * nbk);
   // debug timeline: CLIMBER_ATTN_TRACE=n records the n-th SUMI launch (clock64 per CTA)
   static int trace_at = [] { const char* t = getenv("CLIMBER_ATTN_TRACE"); return t ? atoi(t) : -1; }();
   static int n_launch = 0;
@@ -490,12 +495,12 @@ void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, 
 
 void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r, int U, const bf16* pool,
                          long long pool_rows, const int* ptab, const int* vlen_all, const float* tau, bf16* O, int k,
-                         int l, const Dims& D, cudaStream_t s) {
+                         int l, const Dims& D, cudaStream_t s, int nbk) {
   CUtensorMap mq, mkv;
-  at::map2d(&mq, Q, (long long)U * D.nk, D.d, D.d, D.dh, at::ROWS);
+  at::map2d(&mq, Q, (long long)U * D.nk * nbk, D.d, D.d, D.dh, at::ROWS);
   at::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, at::KEYS);
-  at::Args a{Q, nullptr, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, D, nullptr};
-  dim3 grid(D.nk / at::ROWS, D.h, U);
+  at::Args a{Q, nullptr, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, U, (long long)U * D.nk, D, nullptr};
+  dim3 grid(D.nk / at::ROWS, D.h, U * nbk);
   if (D.dh == 64) at::launch<64, at::MODE_HIST>(mq, mkv, a, grid, s);
   else at::launch<32, at::MODE_HIST>(mq, mkv, a, grid, s);
 }

@@ -65,10 +65,11 @@ void launch_attn_hist_mma(const bf16* Q, const int* wave_slot, const int* wave_r
 bool attn_tc_supported(int dh, int nk, bool hist);
 void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, const int* wave_slot,
                          const int* wave_r, int U, int Mmax, const bf16* pool, long long pool_rows, const int* ptab,
-                         const int* vlen_all, const float* tau, bf16* O, int k, int l, const Dims& D, cudaStream_t s);
+                         const int* vlen_all, const float* tau, bf16* O, int k, int l, const Dims& D, cudaStream_t s,
+                         int nbk = 1);
 void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r, int U, const bf16* pool,
                          long long pool_rows, const int* ptab, const int* vlen_all, const float* tau, bf16* O, int k,
-                         int l, const Dims& D, cudaStream_t s);
+                         int l, const Dims& D, cudaStream_t s, int nbk = 1);
 
 // tcgen05 GEMM (bf16 in, fp32 accumulate in TMEM), gemm_tc.cu.  Returns false
 // if the shape is not supported by the tensor-core kernel.
