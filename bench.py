@@ -395,7 +395,12 @@ def main():
                 "data": "synthetic", "config": workload_cfg(cfg), "roofline": roof,
                 "step_tflops": tot_flops / (ms_max * 1e-3) / 1e12,
                 "e2e": e2e, "latency_ms": lat, "gpu_launches": int(launches), "clocks": clk,
-                "kernel_ms": {k: round(v["ms"], 3) for k, v in prof.items() if v["launches"]}}
+                "kernel_ms": {k: round(v["ms"], 3) for k, v in prof.items() if v["launches"]},
+                # per-class achieved rate over the timed steps: TFLOP/s where the class
+                # has algorithmic FLOPs, else GB/s of algorithmic bytes
+                "kernel_rate": {k: (round(v["flops"] / (v["ms"] * 1e-3) / 1e12, 1) if v["flops"] else
+                                    round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1))
+                                for k, v in prof.items() if v["launches"] and v["ms"] > 0}}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(cfg, w, batch, args.cpu_budget)
         print(json.dumps(line), flush=True)

@@ -50,6 +50,18 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (FA4's MUFU offload): x = j + f, j = rne(x), f in
+// [-1/2, 1/2]; 2^f by a degree-3 fit (max rel. error 7.5e-5, far below the
+// bf16 rounding of P), 2^j added to the exponent field with one IMAD.
+__device__ __forceinline__ float ex2_poly(float x) {
+  constexpr float MAGIC = 12582912.f;  // 1.5 * 2^23: t's low mantissa bits hold rne(x)
+  x = fmaxf(x, -126.f);
+  const float t = x + MAGIC;
+  const float f = x - (t - MAGIC);
+  const float p = fmaf(fmaf(fmaf(0.055171628f, f, 0.24261117f), f, 0.69326103f), f, 0.99992806f);
+  return __int_as_float(__float_as_int(t) * (1 << 23) + __float_as_int(p));
+}
+
 enum { MODE_SUMI = 0, MODE_HIST = 1 };
 
 template <int DH>
@@ -84,7 +96,8 @@ struct Args {
 };
 constexpr int TRACE_N = 24;
 
-template <int DH, int MODE>
+// PE8: how many of every 8 scores take ex2_poly instead of the MUFU
+template <int DH, int MODE, int PE8>
 __global__ void __launch_bounds__(THREADS, 2)
     k_attn_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, Args a) {
   using Ly = Lay<DH>;
@@ -329,8 +342,9 @@ __global__ void __launch_bounds__(THREADS, 2)
       if (full) {
 #pragma unroll
         for (int i = 0; i < KEYS; i += 2) {
-          const float e0 = ex2_approx(fmaf(__uint_as_float(sr[i]), sc, nb));
-          const float e1 = ex2_approx(fmaf(__uint_as_float(sr[i + 1]), sc, nb));
+          const float x0 = fmaf(__uint_as_float(sr[i]), sc, nb), x1 = fmaf(__uint_as_float(sr[i + 1]), sc, nb);
+          const float e0 = ((i & 7) < PE8) ? ex2_poly(x0) : ex2_approx(x0);
+          const float e1 = (((i + 1) & 7) < PE8) ? ex2_poly(x1) : ex2_approx(x1);
           ls8[i & 7] += e0;
           ls8[(i + 1) & 7] += e1;
           __nv_bfloat162 pp = __floats2bfloat162_rn(e0, e1);
@@ -433,15 +447,36 @@ static bool map2d(CUtensorMap* m, const void* base, long long rows, int cols, lo
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int DH, int MODE>
-static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s) {
+template <int DH, int MODE, int PE8>
+static void launch_pe(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s) {
   constexpr int smem = Lay<DH>::TOTAL;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_attn_tc<DH, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_attn_tc<DH, MODE, PE8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  k_attn_tc<DH, MODE><<<grid, THREADS, smem, s>>>(mq, mkv, a);
+  k_attn_tc<DH, MODE, PE8><<<grid, THREADS, smem, s>>>(mq, mkv, a);
+}
+
+// CLIMBER_ATTN_PE8 overrides the MUFU/FMA split (measurement knob)
+static int pe8_setting() {
+  static int v = [] {
+    const char* e = getenv("CLIMBER_ATTN_PE8");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <int DH, int MODE>
+static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s) {
+  switch (pe8_setting()) {
+    case 0: launch_pe<DH, MODE, 0>(mq, mkv, a, grid, s); break;
+    case 1: launch_pe<DH, MODE, 1>(mq, mkv, a, grid, s); break;
+    case 3: launch_pe<DH, MODE, 3>(mq, mkv, a, grid, s); break;
+    case 4: launch_pe<DH, MODE, 4>(mq, mkv, a, grid, s); break;
+    case 2: launch_pe<DH, MODE, 2>(mq, mkv, a, grid, s); break;
+    default: launch_pe<DH, MODE, 0>(mq, mkv, a, grid, s); break;
+  }
 }
 
 }  // namespace at

@@ -4,7 +4,7 @@
 // common.cuh.  These are the f_QKV / W_O / f_FFN / squeeze-and-excitation
 // contractions of PAPER.md Eq. 3-4.
 //
-// Structure (one CTA per SM, persistent over output tiles):
+// Structure (persistent over output tiles; default: CTA pairs, see CG below):
 //   warp 0      TMA producer: A tile 128x64 and B tile BNx64 per k-block,
 //               128B-swizzled, into a STAGES-deep smem ring (full/empty mbarriers)
 //   warp 1      MMA issuer: one elected thread issues tcgen05.mma (M=128, N=BN,
@@ -31,10 +31,10 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B rows = one SWIZZLE_128B atom width
 
 
-template <int BN, int STAGES, int EPIW, int SBUF, int NORM = 0>
+template <int BN, int STAGES, int EPIW, int SBUF, int NORM = 0, int CG = 1>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (BN / CG) * BK * 2;  // CG = 2: this CTA's half of the B tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STG_OFF = STAGES * STAGE_BYTES;  // epilogue staging: 4 warps x 2 x (32 rows x 128 B)
   // NORM (EPI_RESID_NORM): per warp 2 sets x (fp32 box 32x32 + bf16 box 32x32) = 12 KB
@@ -45,12 +45,15 @@ struct Smem {
 
 // EPIW epilogue warps (4 or 8), SBUF staging buffers per epilogue warp (1 or 2),
 // NORM = 1: the EPI_RESID_NORM epilogue (residual add + bf16 copy + row sums of squares)
-template <int BN, int STAGES, int EPIW, int SBUF, int NORM>
+// CG = 2: CTA pair (2x1 cluster) computing a 256 x BN tile with cta_group::2
+// MMAs issued by the leader; CTA r owns rows 128 r .. 128 r + 127 of the tile
+// (its A half, its TMEM lanes, its epilogue) and loads B rows r BN/2 .. of it.
+template <int BN, int STAGES, int EPIW, int SBUF, int NORM, int CG>
 __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmP,
               const __grid_constant__ CUtensorMap tmC16, long long M, int N, int K, int batch, Epilogue e) {
-  using S = Smem<BN, STAGES, EPIW, SBUF, NORM>;
+  using S = Smem<BN, STAGES, EPIW, SBUF, NORM, CG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
@@ -61,8 +64,10 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ldbar + 2 * EPIW);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int crank = CG == 2 ? (int)cluster_rank() : 0;
+  const long long tile_start = blockIdx.x / CG, tile_step = gridDim.x / CG;  // one tile per cluster
   const int n_tiles = N / BN;
-  const long long m_tiles = (M + BM - 1) / BM;
+  const long long m_tiles = (M + CG * BM - 1) / (CG * BM);
   const long long tiles_per_b = m_tiles * n_tiles;
   const long long num_tiles = tiles_per_b * batch;  // batch-major: t -> (b, m_blk, n_blk)
   const int kblocks = K / BK;
@@ -79,50 +84,67 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 32 * EPIW);
+      mbar_init(&tempty[a], CG * EPIW);  // one arrival per epilogue warp of the pair (leader's copy)
     }
     for (int a = 0; a < 2 * EPIW; ++a) mbar_init(&ldbar[a], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(2 * BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(2 * BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive / complete_tx
+  else __syncthreads();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // the accumulator-empty barrier lives in the leader (cluster address)
+  const uint32_t tempty_c0 = CG == 2 ? mapa(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
       int stage = 0;
       uint32_t phase = 0;
-      for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (long long t = tile_start; t < num_tiles; t += tile_step) {
         const int bt = (int)(t / tiles_per_b);
         const long long tr = t % tiles_per_b;
         const int m_blk = (int)(tr / n_tiles), n_blk = (int)(tr % n_tiles);
+        const int arow = (m_blk * CG + crank) * BM, brow = n_blk * BN + crank * (BN / CG);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::STAGE_BYTES;
           uint8_t* sb = sa + S::A_BYTES;
-          mbar_expect_tx(&full[stage], S::STAGE_BYTES);
-          tma_load_3d(sa, &tmA, &full[stage], kb * BK, m_blk * BM, bt);
-          tma_load_3d(sb, &tmB, &full[stage], kb * BK, n_blk * BN, bt);
+          if constexpr (CG == 2) {  // both halves complete on the leader's full barrier
+            const uint32_t fb = mapa(smem_u32(&full[stage]), 0);
+            if (crank == 0) mbar_expect_tx(&full[stage], 2 * S::STAGE_BYTES);
+            tma_load_3d_cg2(sa, &tmA, fb, kb * BK, arow, bt);
+            tma_load_3d_cg2(sb, &tmB, fb, kb * BK, brow, bt);
+          } else {
+            mbar_expect_tx(&full[stage], S::STAGE_BYTES);
+            tma_load_3d(sa, &tmA, &full[stage], kb * BK, arow, bt);
+            tma_load_3d(sb, &tmB, &full[stage], kb * BK, brow, bt);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
-      constexpr uint32_t idesc = idesc_bf16(BM, BN);
+    if (lane == 0 && crank == 0) {
+      // ---------------- MMA issuer (the pair's leader) ----------------
+      constexpr uint32_t idesc = idesc_bf16(CG * BM, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (long long t = tile_start; t < num_tiles; t += tile_step) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -133,12 +155,16 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
           uint8_t* sb = sa + S::A_BYTES;
           const uint64_t da = sdesc(sa), db = sdesc(sb);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)  // +32 B along K inside the swizzle atom = +2 in the addr field
-            mma_bf16(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) ? 1u : 0u);
-          mma_commit(&empty[stage]);
+          for (int k = 0; k < BK / 16; ++k) {  // +32 B along K inside the swizzle atom = +2 in the addr field
+            if constexpr (CG == 2) mma_bf16_cg2(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) ? 1u : 0u);
+            else mma_bf16(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) ? 1u : 0u);
+          }
+          if constexpr (CG == 2) mma_commit_cg2(&empty[stage]);
+          else mma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[acc]);
+        if constexpr (CG == 2) mma_commit_cg2(&tfull[acc]);
+        else mma_commit(&tfull[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -180,11 +206,11 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
           tma_load_3d(stg + set * 6144, &tmD, &lb[set], n0, (int)r0, bt);
         }
       };
-      for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (long long t = tile_start; t < num_tiles; t += tile_step) {
         bt = (int)(t / tiles_per_b);
         const long long trm = t % tiles_per_b;
         const int m_blk = (int)(trm / n_tiles), n_blk = (int)(trm % n_tiles);
-        const long long row0 = (long long)m_blk * BM + ew * 32;
+        const long long row0 = (long long)(m_blk * CG + crank) * BM + ew * 32;
         const bool rows_ok = row0 < M;  // warp-uniform
         if (rows_ok) {  // the first two chunks of old residual are requested before the accumulator wait
           issue(row0, n_blk * BN, 0);
@@ -237,15 +263,16 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
         }
         if (rows_ok && row0 + lane < M) e.part[bt * e.part_bs + (row0 + lane) * e.part_rs + n_blk] = ss;
         fence_before();
-        mbar_arrive(&tempty[acc]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_c0 + acc * 8);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     } else
-    for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (long long t = tile_start; t < num_tiles; t += tile_step) {
       const int bt = (int)(t / tiles_per_b);
       const long long trm = t % tiles_per_b;
       const int m_blk = (int)(trm / n_tiles), n_blk = (int)(trm % n_tiles);
-      const long long row0 = (long long)m_blk * BM + ew * 32;
+      const long long row0 = (long long)(m_blk * CG + crank) * BM + ew * 32;
       // RMSNorm folded into this GEMM: the per-row 1/rms from the producer's
       // partials, loaded before the accumulator wait so the latency is hidden
       float rsc = 1.f;
@@ -358,16 +385,21 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
         }
       }
       fence_before();
-      mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_c0 + acc * 8);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // the leader's MMAs read the peer's smem until the last tile
+  else __syncthreads();
   if (warp == 2) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
+    if constexpr (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
   }
 }
 
@@ -421,12 +453,12 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int EPIW, int SBUF, int NORM = 0>
+template <int BN, int STAGES, int EPIW, int SBUF, int NORM = 0, int CG = 1>
 static void launch(const bf16* A, long long lda, long long abs_, const bf16* B, long long ldb, long long bbs,
                    long long M, int N, int K, int batch, const Epilogue& e, cudaStream_t s) {
   CUtensorMap ma, mb, md, mp, mc;
   make_map(&ma, A, M, K, lda, BM, BK, false, false, batch, abs_);
-  make_map(&mb, B, N, K, ldb, BN, BK, false, false, batch, bbs);
+  make_map(&mb, B, N, K, ldb, BN / CG, BK, false, false, batch, bbs);
   mp = ma;  // unused unless QKV_PAGES
   mc = ma;  // unused unless RESID_NORM
   if (e.kind == EPI_RESID_NORM) make_map(&mc, e.out_b16, M, N, e.ldo, 32, 32, false, true, batch, e.out_b16_bs);
@@ -442,16 +474,34 @@ static void launch(const bf16* A, long long lda, long long abs_, const bf16* B, 
   } else {
     make_map(&md, e.out, M, N, e.ldo, 32, 32, true, false, batch, e.out_bs);
   }
-  constexpr int smem = Smem<BN, STAGES, EPIW, SBUF, NORM>::TOTAL;
+  constexpr int smem = Smem<BN, STAGES, EPIW, SBUF, NORM, CG>::TOTAL;
   static_assert(smem <= 232448, "smem");
+  auto kern = k_gemm_tc<BN, STAGES, EPIW, SBUF, NORM, CG>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, EPIW, SBUF, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  long long tiles = ((M + BM - 1) / BM) * (N / BN) * batch;
-  int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  k_gemm_tc<BN, STAGES, EPIW, SBUF, NORM><<<grid, 128 + 32 * EPIW, smem, s>>>(ma, mb, md, mp, mc, M, N, K, batch, e);
+  const long long tiles = ((M + CG * BM - 1) / (CG * BM)) * (N / BN) * batch;  // per CTA (pair)
+  const long long slots = num_sms() / CG;
+  const int grid = (int)(tiles < slots ? tiles : slots) * CG;
+  if constexpr (CG == 1) {
+    kern<<<grid, 128 + 32 * EPIW, smem, s>>>(ma, mb, md, mp, mc, M, N, K, batch, e);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(128 + 32 * EPIW);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CG;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, ma, mb, md, mp, mc, M, N, K, batch, e);
+  }
 }
 
 }  // namespace tc
@@ -471,10 +521,27 @@ void launch_gemm_tc_batched(const bf16* A, long long lda, long long a_bs, const 
   //   2: 8 epilogue warps, 3 stages, double-buffered staging
   //   3: 8 epilogue warps, 4 stages, single staging buffer (SiLU / sigmoid:
   //      MUFU-heavy epilogues need 8 warps to keep up with the MMA)
-  static int forced = -1;
+  static int forced = -1, cg = -1;
   if (forced < 0) {
     const char* v = getenv("CLIMBER_GEMM_VARIANT");
     forced = v ? atoi(v) : 0;
+    const char* c = getenv("CLIMBER_GEMM_CG");
+    cg = c ? atoi(c) : 2;
+  }
+  if (cg == 2) {  // CTA pairs: 256 x BN tiles, each CTA streams half of B
+    if (e.kind == EPI_RESID_NORM) {
+      if (N % 256 == 0) tc::launch<256, 5, 4, 2, 1, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+      else tc::launch<128, 6, 4, 2, 1, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+      return;
+    }
+    const bool heavy = (e.kind == EPI_STORE || e.kind == EPI_STORE_F32) && e.act != ACT_NONE;
+    if (N % 256 == 0) {
+      if (heavy) tc::launch<256, 6, 8, 1, 0, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+      else tc::launch<256, 6, 4, 2, 0, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+    } else {
+      tc::launch<128, 8, 4, 2, 0, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+    }
+    return;
   }
   if (e.kind == EPI_RESID_NORM) {  // N % 128 == 0 (checked by the caller)
     if (N % 256 == 0) tc::launch<256, 3, 4, 2, 1>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
