@@ -7,18 +7,20 @@
 //              (causal) or j < v (requires n_k % 128 == 0).
 //
 // CTA = 8 warps, one 128-row query tile (TMEM lane = query row); 2 CTAs/SM:
-//   warp 0   TMA: Q tile once; K and V of one 64-token page per chunk into a
-//            4-stage ring
+//   warp 0   TMA: Q (and SUMI k_self / v_self) tiles once; K and V of one
+//            64-token page per chunk into a 5-stage ring (stages 3 and 4 reuse
+//            the self tiles once the self term is read; TMA latency under load
+//            is ~2000 cycles, so five pages stay in flight)
 //   warp 1   MMA (one thread): S_j = Q K_j^T (M=128, N=64, K=d_h) into one of
-//            three TMEM score buffers, so QK^T of chunk j+1 only waits for
-//            PV of chunk j-2 and overlaps the softmax of chunk j; O += P_j V_j
-//            (M=128, N=d_h, K=64) with P_j read from TMEM (it overwrites S_j in
-//            place as packed bf16), V MN-major
+//            three TMEM score buffers, issued two chunks ahead and interleaved
+//            step by step with O += P_j V_j (M=128, N=d_h, K=64; P_j read from
+//            TMEM where it overwrote S_j as packed bf16, V MN-major): chains of
+//            N=64 MMAs are latency-bound, two independent chains overlap
 //   warp 2   TMEM allocator (3 x 64 score columns + d_h output columns = 256)
 //   warps 4-7 softmax, one thread per query row, two passes over its S row in
-//            TMEM (max, then exp2 -> packed bf16 P); lazy online max (O in TMEM
-//            is rescaled only when the row max grows by more than 2^8);
-//            epilogue O / l -> bf16 -> global.
+//            TMEM (max, then exp2 -> packed bf16 P; packed FFMA2/FADD2 and
+//            3-input max); lazy online max (O in TMEM is rescaled only when the
+//            row max grows by more than 2^8); epilogue O / l -> bf16 -> global.
 // The SUMI self term initialises the row state: m = s_self, l = 1, O = v_self
 // (tcgen05.st), so no candidate ever reads another candidate's K/V.
 #include <cuda.h>
@@ -37,7 +39,8 @@ using namespace tcu;
 
 constexpr int ROWS = 128;
 constexpr int KEYS = PAGE;  // 64 keys per chunk = one K/V page
-constexpr int STAGES = 3;
+constexpr int STAGES = 5;  // K/V pages in flight (TMA latency under load is ~2000 cycles)
+constexpr int FREE_STAGES = 3;  // stages 3, 4 alias the SUMI k_self / v_self tiles (free after init)
 constexpr int NSB = 3;      // TMEM score/P buffers
 constexpr int THREADS = 256;
 constexpr float LOG2E = 1.4426950408889634f;
@@ -62,6 +65,40 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(t) * (1 << 23) + __float_as_int(p));
 }
 
+// Blackwell packed FP32x2 FMA / add and 3-input max (FFMA2, FADD2, FMNMX3):
+// half the issue slots of the scalar forms in the softmax loop
+__device__ __forceinline__ uint64_t pk2(float x, float y) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(uint64_t r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float max3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+#ifdef CLIMBER_ATTN_SPIN
+#define MBW mbar_wait_spin
+#else
+#define MBW mbar_wait
+#endif
+
 enum { MODE_SUMI = 0, MODE_HIST = 1 };
 
 template <int DH>
@@ -73,8 +110,11 @@ struct Lay {
   static constexpr int KVB = KEYS * RB;                  // one K (or V) page slice of one head
   static constexpr int KS_OFF = Q_OFF + Q_BYTES;         // SUMI: the tile's k_self rows (same swizzle as Q)
   static constexpr int VS_OFF = KS_OFF + Q_BYTES;        // SUMI: the tile's v_self rows
-  static constexpr int KV_OFF = VS_OFF + Q_BYTES;        // stage s: K at KV_OFF + 2 s KVB, V at + KVB
-  static constexpr int BAR_OFF = KV_OFF + 2 * STAGES * KVB;
+  static constexpr int KV_OFF = VS_OFF + Q_BYTES;        // stage s < 3: K at KV_OFF + 2 s KVB, V at + KVB
+  static_assert(2 * KVB == Q_BYTES, "one ring stage = one self tile");
+  static constexpr int BAR_OFF = KV_OFF + 2 * FREE_STAGES * KVB;
+  // stages 3 and 4 reuse the k_self / v_self tiles once the self term is read
+  __device__ static constexpr int stage_off(int st) { return st < FREE_STAGES ? KV_OFF + 2 * st * KVB : KS_OFF + 2 * (st - FREE_STAGES) * KVB; }
   static constexpr int TOTAL = BAR_OFF + 512 + 1024;
   static constexpr int STG_OFF = KV_OFF;                 // epilogue staging reuses the K/V ring
 };
@@ -94,7 +134,7 @@ struct Args {
   Dims D;
   unsigned long long* trace;  // debug timeline (CLIMBER_ATTN_TRACE), nullptr normally
 };
-constexpr int TRACE_N = 24;
+constexpr int TRACE_N = 48;  // CLIMBER_ATTN_TRACE_BUILD: 0-23 softmax timeline, 24-31 MMA p_full seen, 32-39 QK issue
 
 // PE8: how many of every 8 scores take ex2_poly instead of the MUFU
 template <int DH, int MODE, int PE8>
@@ -113,7 +153,8 @@ __global__ void __launch_bounds__(THREADS, 2)
   uint64_t* s_full = bars + 1 + 2 * STAGES;    // [NSB]
   uint64_t* p_full = s_full + NSB;             // [NSB]
   uint64_t* o_done = p_full + NSB;             // [NSB]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NSB);
+  uint64_t* self_done = o_done + NSB;          // SUMI: k_self / v_self tiles read (stages 3, 4 free)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(self_done + 1);
 
   const Dims& D = a.D;
   const int u = blockIdx.z % a.U, head = blockIdx.y, tile0 = blockIdx.x * ROWS;  // tiles of one (u, h) adjacent
@@ -153,6 +194,7 @@ __global__ void __launch_bounds__(THREADS, 2)
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
+    mbar_init(self_done, 128);
     for (int b = 0; b < NSB; ++b) {
       mbar_init(&s_full[b], 1);
       mbar_init(&p_full[b], 128);
@@ -165,12 +207,16 @@ __global__ void __launch_bounds__(THREADS, 2)
                  "r"(256));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+#ifdef CLIMBER_ATTN_TRACE_BUILD
   unsigned long long* tr = nullptr;
   const bool tracer = a.trace != nullptr && threadIdx.x == 128;
-  if (tracer) {
+  if (a.trace != nullptr && (threadIdx.x >= 128 ? (threadIdx.x & 31) == 0 : threadIdx.x == 32))
     tr = a.trace + ((long long)(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * TRACE_N;
-    tr[0] = clock64();
-  }
+  if (tracer) tr[0] = clock64();
+#else
+  constexpr unsigned long long* tr = nullptr;
+  constexpr bool tracer = false;
+#endif
   fence_before();
   __syncthreads();
   fence_after();
@@ -179,6 +225,11 @@ __global__ void __launch_bounds__(THREADS, 2)
   const uint32_t tO = tmem_base + NSB * KEYS;  // S/P buffers at tmem_base + b * KEYS
 
   if (warp == 0) {
+    // page ids of this (user, block, layer): one warp-wide load into smem (up
+    // to 64 pages), so the producer never waits on a global load per chunk
+    int* spg = reinterpret_cast<int*>(smem + Ly::BAR_OFF + 256);
+    for (int j = lane; j < n_chunks && j < 64; j += 32) spg[j] = pages[j];
+    __syncwarp();
     if (lane == 0 && (n_chunks > 0 || MODE == MODE_SUMI)) {
       // ---------------- TMA producer ----------------
       if (MODE == MODE_SUMI) {  // q, k_self, v_self of the tile's candidates
@@ -192,10 +243,11 @@ __global__ void __launch_bounds__(THREADS, 2)
       }
       for (int j = 0; j < n_chunks; ++j) {
         const int st = j % STAGES;
-        mbar_wait(&kv_empty[st], ((j / STAGES) & 1) ^ 1);
+        const int page = (j < 64) ? spg[j] : pages[j];
+        MBW(&kv_empty[st], ((j / STAGES) & 1) ^ 1);
+        if (MODE == MODE_SUMI && j == FREE_STAGES) MBW(self_done, 0);
         mbar_expect_tx(&kv_full[st], 2 * Ly::KVB);
-        uint8_t* kd = smem + Ly::KV_OFF + 2 * st * Ly::KVB;
-        const int page = pages[j];
+        uint8_t* kd = smem + Ly::stage_off(st);
         tma_load_2d(kd, &tmKV, &kv_full[st], head * DH, (int)page_row(page, 0, 0));
         tma_load_2d(kd + Ly::KVB, &tmKV, &kv_full[st], head * DH, (int)page_row(page, 1, 0));
       }
@@ -206,38 +258,52 @@ __global__ void __launch_bounds__(THREADS, 2)
       constexpr uint32_t idesc_qk = idesc_bf16_major(ROWS, KEYS, 0, 0);
       constexpr uint32_t idesc_pv = idesc_bf16_major(ROWS, DH, 0, 1);
       const uint64_t qd = make_sdesc(smem_u32(smem + Ly::Q_OFF), 16, 8 * Ly::RB, Ly::SWZ);
-      mbar_wait(bar_q, 0);
-      auto issue_qk = [&](int j) {
-        const int st = j % STAGES;
-        mbar_wait(&kv_full[st], (j / STAGES) & 1);
+      MBW(bar_q, 0);
+      // S runs two chunks ahead of P: iteration j issues PV(j) and QK(j+2)
+      // step by step interleaved (two independent accumulation chains keep the
+      // tensor pipe busy; a lone chain of N=64 MMAs is latency-bound)
+      auto kv_wait = [&](int j) {
+        MBW(&kv_full[j % STAGES], (j / STAGES) & 1);
         fence_after();
-        const uint64_t kd = make_sdesc(smem_u32(smem + Ly::KV_OFF + 2 * st * Ly::KVB), 16, 8 * Ly::RB, Ly::SWZ);
+      };
+      auto kdesc = [&](int j) { return make_sdesc(smem_u32(smem + Ly::stage_off(j % STAGES)), 16, 8 * Ly::RB, Ly::SWZ); };
+      for (int j = 0; j < 2 && j < n_chunks; ++j) {
+        kv_wait(j);
+        const uint64_t kd = kdesc(j);
         const uint32_t tSj = tmem_base + (j % NSB) * KEYS;
+        if (tr && j < 8) tr[32 + j] = clock64();
 #pragma unroll
         for (int s = 0; s < DH / 16; ++s) mma_bf16(tSj, qd + 2 * s, kd + 2 * s, idesc_qk, s > 0 ? 1u : 0u);
         mma_commit(&s_full[j % NSB]);
-      };
-      issue_qk(0);
+      }
       for (int j = 0; j < n_chunks; ++j) {
         const int st = j % STAGES;
-        if (j + 1 < n_chunks) {
-          const int jp = j + 1 - NSB;  // previous user of buffer (j+1) % NSB
-          if (jp >= 0) mbar_wait(&o_done[jp % NSB], (jp / NSB) & 1);
-          issue_qk(j + 1);
+        const int jq = j + 2;
+        const bool q = jq < n_chunks;
+        uint64_t kd = 0;
+        uint32_t tSq = 0;
+        if (q) {
+          if (j >= 1) MBW(&o_done[(j - 1) % NSB], ((j - 1) / NSB) & 1);  // buffer jq % 3: PV(j-1) read it
+          kv_wait(jq);
+          kd = kdesc(jq);
+          tSq = tmem_base + (jq % NSB) * KEYS;
         }
-        mbar_wait(&p_full[j % NSB], (j / NSB) & 1);
+        MBW(&p_full[j % NSB], (j / NSB) & 1);
         fence_after();
-        const uint64_t vd = make_sdesc(smem_u32(smem + Ly::KV_OFF + 2 * st * Ly::KVB + Ly::KVB), 16, 8 * Ly::RB,
-                                       Ly::SWZ);
+        if (tr && j < 8) tr[24 + j] = clock64();
+        if (tr && q && jq < 8) tr[32 + jq] = clock64();
+        const uint64_t vd = make_sdesc(smem_u32(smem + Ly::stage_off(st) + Ly::KVB), 16, 8 * Ly::RB, Ly::SWZ);
         const uint32_t tPj = tmem_base + (j % NSB) * KEYS;
 #pragma unroll
         for (int s = 0; s < KEYS / 16; ++s) {
           const uint64_t vds = vd + (uint64_t)((16 * Ly::RB) >> 4) * s;  // 16 keys = 2 groups of 8 rows
           const uint32_t acc = (MODE == MODE_SUMI || j > 0 || s > 0) ? 1u : 0u;
           mma_bf16_ts(tO, tPj + 8 * s, vds, idesc_pv, acc);  // 16 keys of P = 8 packed columns
+          if (q && s < DH / 16) mma_bf16(tSq, qd + 2 * s, kd + 2 * s, idesc_qk, s > 0 ? 1u : 0u);
         }
         mma_commit(&o_done[j % NSB]);
         mma_commit(&kv_empty[st]);
+        if (q) mma_commit(&s_full[jq % NSB]);
       }
     }
   } else if (warp >= 4) {
@@ -251,7 +317,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     if (MODE == MODE_SUMI) {
       // self term from the TMA-loaded q / k_self / v_self tiles (row = lane's
       // row, 16-byte chunks XOR-swizzled like the TMA box: 128B or 64B pattern)
-      mbar_wait(bar_q, 0);
+      MBW(bar_q, 0);
       const uint8_t* qrow = smem + Ly::Q_OFF + row * Ly::RB;
       const uint8_t* krow = smem + Ly::KS_OFF + row * Ly::RB;
       const uint8_t* vrow = smem + Ly::VS_OFF + row * Ly::RB;
@@ -281,6 +347,9 @@ __global__ void __launch_bounds__(THREADS, 2)
         }
         tmem_st32(tO + lane_off + c, vs);
       }
+      // the self tiles become K/V ring stages 3 and 4
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(self_done);
     } else {
       m_used = -INFINITY;
       l = 0.f;
@@ -289,7 +358,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     if (tracer) tr[2] = clock64();
     for (int j = 0; j < n_chunks; ++j) {
       const uint32_t tSj = tmem_base + (j % NSB) * KEYS + lane_off;
-      mbar_wait(&s_full[j % NSB], (j / NSB) & 1);
+      MBW(&s_full[j % NSB], (j / NSB) & 1);
       fence_after();
       if (tracer && j < 9) tr[3 + 2 * j] = clock64();
       const int key0 = j * KEYS;
@@ -300,13 +369,16 @@ __global__ void __launch_bounds__(THREADS, 2)
       tmem_ld32_nw(tSj, sr);
       tmem_ld32_nw(tSj + 32, sr + 32);
       tmem_ld_wait();
+      const int tph = -1;
+      if (tph >= 0) tr[tph] = clock64();
       float mx8[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
       const bool full = lim >= KEYS;  // no masking in full chunks (the common case)
       if (full) {
 #pragma unroll
-        for (int i = 0; i < KEYS; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(sr[i]));
+        for (int i = 0; i < KEYS; i += 2)
+          mx8[(i >> 1) & 7] = max3(mx8[(i >> 1) & 7], __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
       } else {
 #pragma unroll
         for (int i = 0; i < KEYS; ++i)
@@ -324,7 +396,7 @@ __global__ void __launch_bounds__(THREADS, 2)
         m_used = mx;
       }
       if ((MODE == MODE_SUMI || j > 0) && __any_sync(0xffffffffu, mine)) {
-        if (j > 0) mbar_wait(&o_done[(j - 1) % NSB], ((j - 1) / NSB) & 1);  // PV(j-1) finished writing O
+        if (j > 0) MBW(&o_done[(j - 1) % NSB], ((j - 1) / NSB) & 1);  // PV(j-1) finished writing O
         fence_after();
 #pragma unroll
         for (int c = 0; c < DH; c += 32) {
@@ -336,19 +408,27 @@ __global__ void __launch_bounds__(THREADS, 2)
         }
       }
       // pass 2: P = exp2(s sc - m) as packed bf16, written over S_j in TMEM
+      if (tph >= 0) tr[tph + 1] = clock64();
       const float nb = (m_used == -INFINITY) ? 0.f : -m_used;
       float ls8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       uint32_t pk[KEYS / 2];
       if (full) {
+        const uint64_t sc2 = pk2(sc, sc), nb2 = pk2(nb, nb);
+        uint64_t ls2[4] = {0ull, 0ull, 0ull, 0ull};  // packed (0.f, 0.f)
 #pragma unroll
         for (int i = 0; i < KEYS; i += 2) {
-          const float x0 = fmaf(__uint_as_float(sr[i]), sc, nb), x1 = fmaf(__uint_as_float(sr[i + 1]), sc, nb);
-          const float e0 = ((i & 7) < PE8) ? ex2_poly(x0) : ex2_approx(x0);
-          const float e1 = (((i + 1) & 7) < PE8) ? ex2_poly(x1) : ex2_approx(x1);
-          ls8[i & 7] += e0;
-          ls8[(i + 1) & 7] += e1;
+          const float2 x = upk2(fma2(pk2(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])), sc2, nb2));
+          const float e0 = ((i & 7) < PE8) ? ex2_poly(x.x) : ex2_approx(x.x);
+          const float e1 = (((i + 1) & 7) < PE8) ? ex2_poly(x.y) : ex2_approx(x.y);
+          ls2[(i >> 1) & 3] = add2(ls2[(i >> 1) & 3], pk2(e0, e1));
           __nv_bfloat162 pp = __floats2bfloat162_rn(e0, e1);
           pk[i >> 1] = *reinterpret_cast<uint32_t*>(&pp);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 t = upk2(ls2[q]);
+          ls8[2 * q] = t.x;
+          ls8[2 * q + 1] = t.y;
         }
       } else {
 #pragma unroll
@@ -361,17 +441,20 @@ __global__ void __launch_bounds__(THREADS, 2)
           pk[i >> 1] = *reinterpret_cast<uint32_t*>(&pp);
         }
       }
+      if (tph >= 0) tr[tph + 2] = clock64();
       tmem_st16u(tSj, pk);
       tmem_st16u(tSj + 16, pk + 16);
       tmem_st_wait();
+      if (tph >= 0) tr[tph + 3] = clock64();
       l += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
       fence_before();
       mbar_arrive(&p_full[j % NSB]);
       if (tracer && j < 9) tr[4 + 2 * j] = clock64();
+
     }
     // ---- epilogue: O / l -> bf16, staged in smem for coalesced stores
     if (n_chunks > 0) {
-      mbar_wait(&o_done[(n_chunks - 1) % NSB], ((n_chunks - 1) / NSB) & 1);
+      MBW(&o_done[(n_chunks - 1) % NSB], ((n_chunks - 1) / NSB) & 1);
       fence_after();
     }
     if (tracer) tr[21] = clock64();
@@ -449,7 +532,8 @@ static bool map2d(CUtensorMap* m, const void* base, long long rows, int cols, lo
 
 template <int DH, int MODE, int PE8>
 static void launch_pe(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s) {
-  constexpr int smem = Lay<DH>::TOTAL;
+  // CLIMBER_ATTN_1CTA=1 (measurement knob): request enough smem for 1 CTA/SM
+  static const int smem = getenv("CLIMBER_ATTN_1CTA") ? 150 * 1024 : Lay<DH>::TOTAL;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_attn_tc<DH, MODE, PE8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -517,13 +601,19 @@ void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, 
       if (!t[0] || !t[22]) continue;
       ++cnt;
       for (int i = 1; i < at::TRACE_N; ++i)
-        if (t[i]) acc[i] += (double)(t[i] - t[0]);
+        if (t[i]) acc[i] += (double)(long long)(t[i] - t[0]);
     }
     fprintf(stderr, "[attn trace] %lld CTAs; mean cycles since start: prologue %.0f init %.0f", cnt, acc[1] / cnt,
             acc[2] / cnt);
     for (int j = 0; j < 9; ++j)
       if (acc[3 + 2 * j] > 0) fprintf(stderr, " | c%d S %.0f P %.0f", j, acc[3 + 2 * j] / cnt, acc[4 + 2 * j] / cnt);
     fprintf(stderr, " | o_done %.0f staged %.0f end %.0f\n", acc[21] / cnt, acc[23] / cnt, acc[22] / cnt);
+    fprintf(stderr, "[attn trace] MMA p_full(j) seen: %.0f %.0f %.0f %.0f %.0f %.0f %.0f %.0f\n",
+            acc[24] / cnt, acc[25] / cnt, acc[26] / cnt, acc[27] / cnt, acc[28] / cnt, acc[29] / cnt, acc[30] / cnt,
+            acc[31] / cnt);
+    fprintf(stderr, "[attn trace] QK issue:");
+    for (int j = 0; j < 8; ++j) fprintf(stderr, " %.0f", acc[32 + j] / cnt);
+    fprintf(stderr, "\n");
     cudaFree(tbuf);
   }
 }
