@@ -218,11 +218,17 @@ def roofline(prof, pk, pk_src, bf16=True):
     p = prof[dom]
     n = max(p["launches"], 1)
     ms_per_launch = p["ms"] / n
-    traffic = None
+    traffic, traffic_info = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(dom)
+            t = json.load(open(tpath)).get(dom)
+            if isinstance(t, dict):  # one captured launch: DRAM bytes vs its algorithmic bytes
+                traffic = t["bytes"]
+                traffic_info = {"algorithmic_bytes": t.get("algorithmic_bytes"), "launch": t.get("launch"),
+                                "capture": t.get("capture")}
+            else:
+                traffic = t
         except Exception:
             traffic = None
     if dom.startswith("gemm"):
@@ -249,7 +255,7 @@ def roofline(prof, pk, pk_src, bf16=True):
         peak = pk["hbm_gbs"]
         peak_note = f"HBM copy ({pk_src})"
     return {"kernel": dom, "bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
-            "traffic": traffic, "launches": int(p["launches"]), "ms_per_launch": ms_per_launch,
+            "traffic": traffic, "traffic_launch": traffic_info, "launches": int(p["launches"]), "ms_per_launch": ms_per_launch,
             "share_of_step": p["ms"] / tot_ms if tot_ms else None, "peak_source": peak_note}
 
 
