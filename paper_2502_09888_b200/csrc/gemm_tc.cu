@@ -528,6 +528,19 @@ void launch_gemm_tc_batched(const bf16* A, long long lda, long long a_bs, const 
     const char* c = getenv("CLIMBER_GEMM_CG");
     cg = c ? atoi(c) : 2;
   }
+  // small launches (one request in latency mode): 256-row pair tiles leave
+  // most SMs idle, so switch to 128 x 128 single-CTA tiles (4x the tiles)
+  const long long pair_ctas = ((M + 255) / 256) * (N / (N % 256 == 0 ? 256 : 128)) * batch * 2;
+  if (pair_ctas < 2LL * tc::num_sms()) {
+    if (e.kind == EPI_RESID_NORM) {
+      tc::launch<128, 4, 4, 2, 1>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+    } else {
+      const bool heavy = (e.kind == EPI_STORE || e.kind == EPI_STORE_F32) && e.act != ACT_NONE;
+      if (heavy) tc::launch<128, 5, 8, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+      else tc::launch<128, 6, 4, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+    }
+    return;
+  }
   if (cg == 2) {  // CTA pairs: 256 x BN tiles, each CTA streams half of B
     if (e.kind == EPI_RESID_NORM) {
       if (N % 256 == 0) tc::launch<256, 5, 4, 2, 1, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
