@@ -212,7 +212,7 @@ static void carve(climber_ctx_s* c, Carver& cv) {
   cv.take(c->QKV, R * 3 * d * e);
   cv.take(c->O, R * d * e);
   cv.take(c->Fh, R * F * e);
-  c->pld = D.d % 256 == 0 ? D.d / 256 : (D.d >= 128 ? D.d / 128 : 1);  // = N / BN of the RESID_NORM GEMMs
+  c->pld = D.d >= 128 ? D.d / 128 : 1;  // one partial per 128 columns of the RESID_NORM GEMMs
   cv.take(c->Xb, R * d * 2);
   cv.take(c->part, R * c->pld * 4);
 }

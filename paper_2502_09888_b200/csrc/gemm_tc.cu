@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       // 128B-swizzled) is TMA-loaded into one of two staging sets (two chunks in
       // flight), C += acc in registers (thread = row), the new C is written back
       // in place and as bf16 into a 32x32 box (64B-swizzled), two TMA stores; the
-      // row's sum of squares over the tile's columns goes to part[m][n_tile].
+      // row's sum of squares over each 128 columns goes to part[m][n0 / 128].
       uint64_t* lb = ldbar + (warp - 4) * 2;
       uint32_t lph[2] = {0u, 0u};
       constexpr int NCH = BN / 32;
@@ -260,8 +260,13 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
               asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
           }
+          // one partial per 128 columns (the same slots whatever BN is)
+          if ((q & 3) == 3) {
+            if (rows_ok && row0 + lane < M)
+              e.part[bt * e.part_bs + (row0 + lane) * e.part_rs + n_blk * (BN / 128) + (q >> 2)] = ss;
+            ss = 0.f;
+          }
         }
-        if (rows_ok && row0 + lane < M) e.part[bt * e.part_bs + (row0 + lane) * e.part_rs + n_blk] = ss;
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty_c0 + acc * 8);

@@ -61,6 +61,14 @@ def test_large_bf16():
     _check_cfg(cfg, B=2, users=[0, 1], max_wave_pairs=2000)
 
 
+@pytest.mark.parametrize("name", ["large", "medium"])
+def test_single_request_bf16(name):
+    # latency mode (B = 1): launches below two waves of CTA pairs take the
+    # 128 x 128 single-CTA GEMM tiles, whose RESID_NORM epilogue must write
+    # the same per-128-column norm partials as the 256-wide pair tiles
+    _check_cfg(synth.preset(name), B=1, users=[0])
+
+
 def test_sweep_corner_bf16():
     cfg = synth.preset("sweep", L=2, n_k=64, M=100, n_s=1536)
     _check_cfg(cfg, B=2, users=[0, 1])
