@@ -368,7 +368,7 @@ def main():
             if i >= 5:
                 tl.append((time.perf_counter() - t0) * 1e3)
         lat = {"p50": float(np.percentile(tl, 50)), "p99": float(np.percentile(tl, 99)), "requests": len(tl),
-               "mode": "single GPU per request (B=1, M candidates), climber_rank_host, no CUDA graph"}
+               "mode": "single GPU per request (B=1, M candidates), climber_rank_host: H2D + one CUDA graph (encode + score, captured once per shape) + D2H"}
     elif args.latency_requests > 0:
         # candidate sharding: owner encodes, K/V slab broadcast over
         # the NCCL group, every rank scores floor(m G / M) == rank, scores gathered

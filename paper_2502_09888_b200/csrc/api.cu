@@ -108,6 +108,15 @@ struct climber_ctx_s {
   // rank_host staging (device, lazily allocated)
   void* io = nullptr;
   size_t io_bytes = 0;
+  // latency mode (rank_host with B = 1): the encode + score kernel sequence
+  // captured once per (events, candidates) shape and replayed as one CUDA graph
+  cudaGraphExec_t g_exec = nullptr;
+  long long g_E = -1, g_P = -1;
+  void* g_io = nullptr;
+  long long g_launches = 0;
+  long long g_seen_E = -1, g_seen_P = -1;  // last shape run eagerly
+  cudaStream_t g_stream = nullptr;          // capture stream
+  bool graphs = true;
 };
 
 static uint16_t g_next_ctx_id = 1;
@@ -320,6 +329,8 @@ extern "C" climber_status climber_create(const climber_config* cfg, const climbe
     c->attn_mode = (ea && strcmp(ea, "simt") == 0) ? 0 : (ea && strcmp(ea, "mma") == 0) ? 1 : 2;
     const char* sc = getenv("CLIMBER_SYNC_CHECK");
     c->sync_check = sc && atoi(sc) != 0;
+    const char* gr = getenv("CLIMBER_GRAPHS");
+    c->graphs = !(gr && atoi(gr) == 0);
 
     const size_t d = D.d, L = D.L, Nb = D.Nb, F = D.F;
     // Fused-norm bf16 path: every RMSNorm gain is folded into the rows (input
@@ -410,6 +421,8 @@ extern "C" climber_status climber_destroy(climber_ctx_t c) {
   cudaDeviceSynchronize();
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->io) cudaFree(c->io);
+  if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
+  if (c->g_stream) cudaStreamDestroy(c->g_stream);
   cudaEventDestroy(c->stage_evt);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete c;
@@ -1286,6 +1299,107 @@ extern "C" climber_status climber_stream_status(climber_ctx_t c, climber_stream_
 }
 
 // ---------------------------------------------------------------------------
+// latency mode: one request (B = 1) as one CUDA graph.  The host bookkeeping
+// (slot / page allocation) and ONE metadata upload (event and candidate
+// offsets, slot, scenario, page table) run eagerly; every kernel reads the
+// request's slot from device memory, so the encode + score launch sequence
+// depends only on (E, P) and is captured once per shape, then replayed.
+// ---------------------------------------------------------------------------
+static climber_status rank_one_graph(climber_ctx_s* c, long long E, long long P, const climber_events& ev,
+                                     int32_t r, const int32_t* d_items, float* d_scores, float* h_scores,
+                                     cudaStream_t s) {
+  if (r < 0 || r >= c->D.R) return fail(CLIMBER_E_OUT_OF_RANGE, "scenario_r out of range");
+  if (E < 0) return fail(CLIMBER_E_INVALID_ARG, "ev_offsets decreasing");
+  if (P < 1 || P > c->cfg.max_candidates) return fail(CLIMBER_E_INVALID_ARG, "M=%lld outside [1, max_candidates]", P);
+  if (P > c->cfg.max_wave_pairs) return fail(CLIMBER_E_INVALID_ARG, "M exceeds max_wave_pairs");
+  climber_kv_t kv;
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    if (c->free_slots.empty() || (long long)c->free_pages.size() < c->per_slot)
+      return fail(CLIMBER_E_CAPACITY, "K/V page pool exhausted");
+    CU(cudaEventSynchronize(c->stage_evt));
+    Stage h = stage_layout(c, c->h_stage);
+    const int slot = c->free_slots.back();
+    c->free_slots.pop_back();
+    SlotState& st = c->slots[slot];
+    st.live = true;
+    st.r = r;
+    st.pages.resize(c->per_slot);
+    for (int i = 0; i < c->per_slot; ++i) {
+      st.pages[i] = c->free_pages.back();
+      c->free_pages.pop_back();
+      h.ptab[i] = st.pages[i];
+    }
+    h.slots[0] = slot;
+    h.r[0] = r;
+    h.ev_off[0] = 0;
+    h.ev_off[1] = E;
+    h.cand_off[0] = 0;
+    h.cand_off[1] = P;
+    kv = make_handle(c, slot, st.gen);
+    climber_status rs = stage_upload(c, 1, true, s);
+    if (rs != CLIMBER_OK) return rs;
+  }
+  EventsDev evd{ev.item, ev.action, ev.scenario, ev.ts};
+  climber_status st = CLIMBER_OK;
+  const bool have = c->g_exec && c->g_E == E && c->g_P == P && c->g_io == c->io;
+  if (!have && !(c->g_seen_E == E && c->g_seen_P == P)) {
+    // first request of this shape: run eagerly (loads every kernel it needs;
+    // lazy module loading is not permitted inside a capture); a repeat of
+    // the shape is captured
+    c->g_seen_E = E;
+    c->g_seen_P = P;
+    encode_wave_grouped(c, evd, 0, 1, E, s);
+    score_wave_grouped(c, d_items, c->d_cand_off, 0, 1, P, (int)P, d_scores, s);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_scores, d_scores, P * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) st = fail(CLIMBER_E_CUDA, "rank_host: %s", cudaGetErrorString(e));
+    climber_kv_release(c, kv);
+    return st;
+  }
+  if (!have) {
+    if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
+    c->g_exec = nullptr;
+    cudaGraph_t graph = nullptr;
+    const long long l0 = c->launches;
+    // capture on a private stream (the caller's may be the legacy default
+    // stream, which cannot capture); nothing executes during capture
+    cudaError_t e = cudaSuccess;
+    if (!c->g_stream) e = cudaStreamCreateWithFlags(&c->g_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamBeginCapture(c->g_stream, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      encode_wave_grouped(c, evd, 0, 1, E, c->g_stream);
+      score_wave_grouped(c, d_items, c->d_cand_off, 0, 1, P, (int)P, d_scores, c->g_stream);
+      e = cudaStreamEndCapture(c->g_stream, &graph);
+    }
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&c->g_exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+      c->g_exec = nullptr;
+      st = fail(CLIMBER_E_CUDA, "rank_host graph capture: %s", cudaGetErrorString(e));
+    } else {
+      c->g_E = E;
+      c->g_P = P;
+      c->g_io = c->io;
+      c->g_launches = c->launches - l0;
+      c->launches = l0;
+    }
+  }
+  if (st == CLIMBER_OK) {
+    cudaError_t e = cudaGraphLaunch(c->g_exec, s);
+    c->launches += c->g_launches;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_scores, d_scores, P * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) st = fail(CLIMBER_E_CUDA, "rank_host: %s", cudaGetErrorString(e));
+  } else {
+    cudaStreamSynchronize(s);
+  }
+  climber_kv_release(c, kv);
+  return st;
+}
+
+// ---------------------------------------------------------------------------
 // end-to-end call with host buffers
 // ---------------------------------------------------------------------------
 extern "C" climber_status climber_rank_host(climber_ctx_t c, int32_t B, const int64_t* ev_offsets,
@@ -1329,6 +1443,9 @@ extern "C" climber_status climber_rank_host(climber_ctx_t c, int32_t B, const in
     co[b] = cand_offsets[b] - c0;
   }
   climber_events ev{d_item, d_act, d_scn, d_ts};
+  if (B == 1 && c->graphs && !c->prof && !c->sync_check && grouped_ok(c) &&
+      attn_tc_supported(c->D.dh, c->D.nk, true))
+    return rank_one_graph(c, E, P, ev, scenario_r[0], d_items, d_scores, scores + c0, s);
   std::vector<climber_kv_t> kvs(B);
   climber_status st = climber_encode_users(c, B, eo.data(), &ev, scenario_r, stream, kvs.data());
   if (st != CLIMBER_OK) return st;

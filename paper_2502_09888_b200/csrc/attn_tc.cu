@@ -137,7 +137,7 @@ struct Args {
 constexpr int TRACE_N = 48;  // CLIMBER_ATTN_TRACE_BUILD: 0-23 softmax timeline, 24-31 MMA p_full seen, 32-39 QK issue
 
 // PE8: how many of every 8 scores take ex2_poly instead of the MUFU
-template <int DH, int MODE, int PE8>
+template <int DH, int MODE, int PE8, int ES = 0>
 __global__ void __launch_bounds__(THREADS, 2)
     k_attn_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, Args a) {
   using Ly = Lay<DH>;
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(THREADS, 2)
       for (int j = 0; j < n_chunks; ++j) {
         const int st = j % STAGES;
         const int jq = j + 2;
-        const bool q = jq < n_chunks;
+        bool q = jq < n_chunks;
         uint64_t kd = 0;
         uint32_t tSq = 0;
         if (q) {
@@ -287,6 +287,12 @@ __global__ void __launch_bounds__(THREADS, 2)
           kv_wait(jq);
           kd = kdesc(jq);
           tSq = tmem_base + (jq % NSB) * KEYS;
+          if (ES) {  // S(j+2) now, before waiting for P(j)
+#pragma unroll
+            for (int s = 0; s < DH / 16; ++s) mma_bf16(tSq, qd + 2 * s, kd + 2 * s, idesc_qk, s > 0 ? 1u : 0u);
+            mma_commit(&s_full[jq % NSB]);
+            q = false;
+          }
         }
         MBW(&p_full[j % NSB], (j / NSB) & 1);
         fence_after();
@@ -502,6 +508,539 @@ __global__ void __launch_bounds__(THREADS, 2)
   }
 }
 
+// ===========================================================================
+// Persistent two-tile attention (default).  One CTA per SM (all 512 TMEM
+// columns) loops over work items; an item = two adjacent 128-row query tiles
+// of one (user, block, head), so every K/V page loaded serves 256 query rows.
+//   warp 0     K/V producer: streams 64-key pages of every item into a ring
+//              that runs across items (the warp holds the item's page ids)
+//   warp 1     MMA issuer (one thread) for both tiles: S = Q K^T two chunks
+//              ahead, interleaved with O += P V (P from TMEM, V MN-major)
+//   warp 2     TMEM allocator
+//   warp 3     item decoder + Q / k_self / v_self producer: writes the item's
+//              descriptor to smem and loads its q tiles into one of two
+//              buffers while the previous item still runs
+//   warps 4-7  softmax + epilogue of tile 0, warps 8-11 of tile 1; each
+//              warpgroup owns half of TMEM (3 x 64 score/P columns + d_h
+//              output columns); the two ping-pong on the MUFU
+// Row arithmetic is identical to k_attn_tc (same online-softmax steps).
+// ===========================================================================
+constexpr int PT_THREADS = 384;
+constexpr int PT_WT = 2;  // query tiles per item
+
+template <int DH>
+struct PLay {
+  static constexpr int RB = DH * 2;
+  static constexpr uint32_t SWZ = (DH == 64) ? 2u : 4u;
+  static constexpr int QB = ROWS * RB;   // one 128-row tile of q (or k_self, v_self)
+  static constexpr int KVB = KEYS * RB;  // one 64-key page slice of K (or V) of one head
+  static constexpr int Q_OFF = 0;        // [2 buffers][PT_WT tiles]
+  static constexpr int KS_OFF = Q_OFF + 2 * PT_WT * QB;
+  static constexpr int VS_OFF = KS_OFF + PT_WT * QB;
+  static constexpr int KV_OFF = VS_OFF + PT_WT * QB;
+  static constexpr int ST_RAW = (232448 - 1024 - 2048 - KV_OFF) / (2 * KVB);
+  static constexpr int ST = ST_RAW > 8 ? 8 : ST_RAW;  // K/V ring stages
+  static constexpr int BAR_OFF = KV_OFF + ST * 2 * KVB;
+  static constexpr int DESC_OFF = BAR_OFF + 512;
+  static constexpr int TOTAL = BAR_OFF + 1024 + 1024;
+  static_assert(ST >= 4, "K/V ring too shallow");
+  static_assert(TOTAL <= 232448, "smem");
+};
+
+struct PArgs {
+  Args a;
+  int n_pairs;  // items per (z, head)
+  long long n_items;
+};
+
+// One work item as the decoder wrote it to shared memory.
+struct PDesc {
+  long long row_base[PT_WT];
+  int n_rows[PT_WT], rows_out[PT_WT], nch[PT_WT], key_end[PT_WT], tile0[PT_WT];
+  int nkv, head, end;
+  float sc;
+};
+
+template <int DH, int MODE>
+__device__ __forceinline__ bool pt_decode(const PArgs& pa, long long it, PDesc& I, const int** pages) {
+  const Args& a = pa.a;
+  const Dims& D = a.D;
+  const int pair = (int)(it % pa.n_pairs);
+  const long long rest = it / pa.n_pairs;
+  I.head = (int)(rest % D.h);
+  const int z = (int)(rest / D.h);
+  const int u = z % a.U, kk = z / a.U, kblk = a.k + kk;
+  const int slot = a.wave_slot[u];
+  const int v = a.vlen_all[(long long)slot * D.Nb + kblk];
+  *pages = a.ptab + (((long long)slot * D.Nb + kblk) * D.L + a.l) * D.ppb;
+  I.nkv = 0;
+  I.end = 0;
+  bool live = false;
+  long long p0 = 0, mu = 0;
+  if (MODE == MODE_SUMI) {
+    p0 = a.cand_off[u];
+    mu = a.cand_off[u + 1] - p0;
+  }
+#pragma unroll
+  for (int w = 0; w < PT_WT; ++w) {
+    const int t0 = (pair * PT_WT + w) * ROWS;
+    I.tile0[w] = t0;
+    if (MODE == MODE_SUMI) {
+      const long long left = mu - t0;
+      I.n_rows[w] = left <= 0 ? 0 : (left < ROWS ? (int)left : ROWS);
+      I.rows_out[w] = I.n_rows[w];
+      I.key_end[w] = v;
+      I.nch[w] = I.n_rows[w] > 0 ? (v + KEYS - 1) / KEYS : 0;
+      I.row_base[w] = kk * a.rows_pb + p0 + t0;
+    } else {
+      I.rows_out[w] = t0 < D.nk ? min(ROWS, D.nk - t0) : 0;
+      I.n_rows[w] = max(0, min(ROWS, v - t0));
+      I.key_end[w] = D.causal ? min(v, t0 + ROWS) : v;
+      I.nch[w] = I.n_rows[w] > 0 ? (I.key_end[w] + KEYS - 1) / KEYS : 0;
+      I.row_base[w] = kk * a.rows_pb + (long long)u * D.nk + t0;
+    }
+    I.nkv = max(I.nkv, I.nch[w]);
+    live = live || I.rows_out[w] > 0;
+  }
+  if (live) {
+    const int r = a.wave_r[u];
+    I.sc = LOG2E / (sqrtf((float)DH) * a.tau[((a.l * D.Nb + kblk) * D.R + r) * D.h + I.head]);
+  }
+  return live;
+}
+
+template <int DH, int MODE, int EARLY_S>
+__global__ void __launch_bounds__(PT_THREADS, 1)
+    k_attn_pt(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, PArgs pa) {
+  using Ly = PLay<DH>;
+  constexpr int ST = Ly::ST;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Ly::BAR_OFF);
+  uint64_t* q_full = bars + 0;        // [2] item descriptor + q tiles of buffer b
+  uint64_t* q_empty = bars + 2;       // [2] MMA read q (last QK) and every softmax thread read the descriptor
+  uint64_t* self_full = bars + 4;     // SUMI: k_self / v_self tiles landed
+  uint64_t* self_empty = bars + 5;    // SUMI: both warpgroups read them
+  uint64_t* kv_full = bars + 6;       // [ST]
+  uint64_t* kv_empty = kv_full + ST;  // [ST]
+  uint64_t* s_full = kv_empty + ST;   // [PT_WT][NSB]
+  uint64_t* p_full = s_full + PT_WT * NSB;
+  uint64_t* o_done = p_full + PT_WT * NSB;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + PT_WT * NSB);
+  PDesc* desc = reinterpret_cast<PDesc*>(smem + Ly::DESC_OFF);  // [2]
+
+  const Args& a = pa.a;
+  const Dims& D = a.D;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmQ) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmKV) : "memory");
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&q_full[b], 1);
+      mbar_init(&q_empty[b], 1 + 256);
+    }
+    mbar_init(self_full, 1);
+    mbar_init(self_empty, 256);
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int b = 0; b < PT_WT * NSB; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 128);
+      mbar_init(&o_done[b], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- K/V producer ----------------
+    long long gk = 0;
+    for (long long it = blockIdx.x; it < pa.n_items; it += gridDim.x) {
+      PDesc I;
+      const int* pages;
+      if (!pt_decode<DH, MODE>(pa, it, I, &pages)) continue;
+      const int pg0 = lane < I.nkv ? pages[lane] : 0;
+      const int pg1 = lane + 32 < I.nkv ? pages[lane + 32] : 0;
+      for (int j = 0; j < I.nkv; ++j, ++gk) {
+        const int page = j < 64 ? __shfl_sync(0xffffffffu, j < 32 ? pg0 : pg1, j & 31) : pages[j];
+        if (lane == 0) {
+          const int st = (int)(gk % ST);
+          MBW(&kv_empty[st], (uint32_t)((gk / ST) & 1) ^ 1);
+          mbar_expect_tx(&kv_full[st], 2 * Ly::KVB);
+          uint8_t* kd = smem + Ly::KV_OFF + st * 2 * Ly::KVB;
+          tma_load_2d(kd, &tmKV, &kv_full[st], I.head * DH, (int)page_row(page, 0, 0));
+          tma_load_2d(kd + Ly::KVB, &tmKV, &kv_full[st], I.head * DH, (int)page_row(page, 1, 0));
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp == 3) {
+    // ---------------- item decoder + q / self producer ----------------
+    if (lane == 0) {
+      long long seq = 0;
+      for (long long it = blockIdx.x;; it += gridDim.x) {
+        PDesc I;
+        const int* pages;
+        const bool done = it >= pa.n_items;
+        if (!done && !pt_decode<DH, MODE>(pa, it, I, &pages)) continue;
+        const int b = (int)(seq & 1);
+        MBW(&q_empty[b], (uint32_t)((seq >> 1) & 1) ^ 1);
+        if (done) {
+          desc[b].end = 1;
+          mbar_arrive(&q_full[b]);
+          break;
+        }
+        desc[b] = I;
+        uint32_t bytes = 0;
+#pragma unroll
+        for (int w = 0; w < PT_WT; ++w)
+          if (MODE == MODE_SUMI ? I.n_rows[w] > 0 : I.nch[w] > 0) bytes += Ly::QB;
+        mbar_expect_tx(&q_full[b], bytes);
+#pragma unroll
+        for (int w = 0; w < PT_WT; ++w)
+          if (MODE == MODE_SUMI ? I.n_rows[w] > 0 : I.nch[w] > 0)
+            tma_load_2d(smem + Ly::Q_OFF + (b * PT_WT + w) * Ly::QB, &tmQ, &q_full[b], I.head * DH,
+                        (int)I.row_base[w]);
+        if (MODE == MODE_SUMI) {
+          MBW(self_empty, (uint32_t)(seq & 1) ^ 1);
+          uint32_t sb = 0;
+#pragma unroll
+          for (int w = 0; w < PT_WT; ++w)
+            if (I.n_rows[w] > 0) sb += 2 * Ly::QB;
+          mbar_expect_tx(self_full, sb);
+#pragma unroll
+          for (int w = 0; w < PT_WT; ++w) {
+            if (I.n_rows[w] <= 0) continue;
+            tma_load_2d(smem + Ly::KS_OFF + w * Ly::QB, &tmQ, self_full, D.d + I.head * DH, (int)I.row_base[w]);
+            tma_load_2d(smem + Ly::VS_OFF + w * Ly::QB, &tmQ, self_full, 2 * D.d + I.head * DH, (int)I.row_base[w]);
+          }
+        }
+        ++seq;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer for both tiles ----------------
+      constexpr uint32_t idesc_qk = idesc_bf16_major(ROWS, KEYS, 0, 0);
+      constexpr uint32_t idesc_pv = idesc_bf16_major(ROWS, DH, 0, 1);
+      long long gk = 0;
+      long long cs[PT_WT] = {0, 0};
+      for (long long seq = 0;; ++seq) {
+        const int b = (int)(seq & 1);
+        MBW(&q_full[b], (uint32_t)((seq >> 1) & 1));
+        fence_after();
+        const PDesc& I = desc[b];
+        if (I.end) break;
+        int nch[PT_WT];
+#pragma unroll
+        for (int w = 0; w < PT_WT; ++w) nch[w] = I.nch[w];
+        const int nkv = I.nkv;
+        auto kv_wait = [&](int j) {
+          MBW(&kv_full[(gk + j) % ST], (uint32_t)(((gk + j) / ST) & 1));
+          fence_after();
+        };
+        auto kdesc = [&](int j) {
+          return make_sdesc(smem_u32(smem + Ly::KV_OFF + (int)((gk + j) % ST) * 2 * Ly::KVB), 16, 8 * Ly::RB, Ly::SWZ);
+        };
+        auto qdesc = [&](int w) {
+          return make_sdesc(smem_u32(smem + Ly::Q_OFF + (b * PT_WT + w) * Ly::QB), 16, 8 * Ly::RB, Ly::SWZ);
+        };
+        auto sbuf = [&](int w, long long c) { return tmem_base + w * 256 + (uint32_t)(c % NSB) * KEYS; };
+        for (int j = 0; j < 2 && j < nkv; ++j) {
+          kv_wait(j);
+          const uint64_t kd = kdesc(j);
+#pragma unroll
+          for (int w = 0; w < PT_WT; ++w) {
+            if (j >= nch[w]) continue;
+            const long long c = cs[w] + j;  // score buffer c % 3 was last read by PV(c - 3)
+            if (c >= 3) MBW(&o_done[w * NSB + (int)((c - 3) % NSB)], (uint32_t)(((c - 3) / NSB) & 1));
+            const uint64_t qd = qdesc(w);
+            const uint32_t tS = sbuf(w, c);
+#pragma unroll
+            for (int s = 0; s < DH / 16; ++s) mma_bf16(tS, qd + 2 * s, kd + 2 * s, idesc_qk, s > 0 ? 1u : 0u);
+            mma_commit(&s_full[w * NSB + (int)(c % NSB)]);
+          }
+        }
+        if (nkv <= 2) mma_commit(&q_empty[b]);
+        for (int j = 0; j < nkv; ++j) {
+          const int jq = j + 2;
+          uint64_t kq = 0;
+          if (jq < nkv) {
+            kv_wait(jq);
+            kq = kdesc(jq);
+          }
+          const uint64_t vd = kdesc(j) + (uint64_t)(Ly::KVB >> 4);
+          if (EARLY_S) {
+            // S(j+2) as soon as its buffer is free (PV(j-1) done), ahead of
+            // waiting for P(j): the score chain gets a full softmax period more slack
+#pragma unroll
+            for (int w = 0; w < PT_WT; ++w) {
+              if (jq >= nch[w]) continue;
+              const long long c = cs[w] + j;
+              if (c >= 1) MBW(&o_done[w * NSB + (int)((c - 1) % NSB)], (uint32_t)(((c - 1) / NSB) & 1));
+              fence_after();
+              const uint64_t qd = qdesc(w);
+              const uint32_t tSq = sbuf(w, c + 2);
+#pragma unroll
+              for (int s = 0; s < DH / 16; ++s) mma_bf16(tSq, qd + 2 * s, kq + 2 * s, idesc_qk, s > 0 ? 1u : 0u);
+              mma_commit(&s_full[w * NSB + (int)((c + 2) % NSB)]);
+            }
+#pragma unroll
+            for (int w = 0; w < PT_WT; ++w) {
+              if (j >= nch[w]) continue;
+              const long long c = cs[w] + j;
+              MBW(&p_full[w * NSB + (int)(c % NSB)], (uint32_t)((c / NSB) & 1));
+              fence_after();
+              const uint32_t tO = tmem_base + w * 256 + NSB * KEYS;
+              const uint32_t tP = sbuf(w, c);
+#pragma unroll
+              for (int s = 0; s < KEYS / 16; ++s) {
+                const uint64_t vds = vd + (uint64_t)((16 * Ly::RB) >> 4) * s;
+                const uint32_t acc = (MODE == MODE_SUMI || j > 0 || s > 0) ? 1u : 0u;
+                mma_bf16_ts(tO, tP + 8 * s, vds, idesc_pv, acc);
+              }
+              mma_commit(&o_done[w * NSB + (int)(c % NSB)]);
+            }
+            mma_commit(&kv_empty[(gk + j) % ST]);
+            if (jq == nkv - 1) mma_commit(&q_empty[b]);
+            continue;
+          }
+#pragma unroll
+          for (int w = 0; w < PT_WT; ++w) {
+            if (j >= nch[w]) continue;
+            const bool q = jq < nch[w];
+            const long long c = cs[w] + j;
+            if (q && c >= 1) MBW(&o_done[w * NSB + (int)((c - 1) % NSB)], (uint32_t)(((c - 1) / NSB) & 1));
+            MBW(&p_full[w * NSB + (int)(c % NSB)], (uint32_t)((c / NSB) & 1));
+            fence_after();
+            const uint64_t qd = qdesc(w);
+            const uint32_t tO = tmem_base + w * 256 + NSB * KEYS;
+            const uint32_t tP = sbuf(w, c);
+            const uint32_t tSq = sbuf(w, c + 2);
+#pragma unroll
+            for (int s = 0; s < KEYS / 16; ++s) {
+              const uint64_t vds = vd + (uint64_t)((16 * Ly::RB) >> 4) * s;
+              const uint32_t acc = (MODE == MODE_SUMI || j > 0 || s > 0) ? 1u : 0u;
+              mma_bf16_ts(tO, tP + 8 * s, vds, idesc_pv, acc);
+              if (q && s < DH / 16) mma_bf16(tSq, qd + 2 * s, kq + 2 * s, idesc_qk, s > 0 ? 1u : 0u);
+            }
+            mma_commit(&o_done[w * NSB + (int)(c % NSB)]);
+            if (q) mma_commit(&s_full[w * NSB + (int)((c + 2) % NSB)]);
+          }
+          mma_commit(&kv_empty[(gk + j) % ST]);
+          if (jq == nkv - 1) mma_commit(&q_empty[b]);  // the item's last QK has been issued
+        }
+        gk += nkv;
+#pragma unroll
+        for (int w = 0; w < PT_WT; ++w) cs[w] += nch[w];
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- softmax + epilogue, warpgroup wg owns tile wg ----------------
+    const int wg = (warp - 4) >> 2;
+    const int ew = (warp - 4) & 3;
+    const int row = ew * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
+    const uint32_t tO = tmem_base + wg * 256 + NSB * KEYS + lane_off;
+    long long cs = 0;
+    for (long long seq = 0;; ++seq) {
+      const int b = (int)(seq & 1);
+      MBW(&q_full[b], (uint32_t)((seq >> 1) & 1));
+      const PDesc& I = desc[b];
+      if (I.end) break;
+      const int nch = I.nch[wg];
+      const int n_rows = I.n_rows[wg];
+      const int key_end = I.key_end[wg];
+      const int rows_out = I.rows_out[wg];
+      const long long row_base = I.row_base[wg];
+      const int tile0 = I.tile0[wg];
+      const int head = I.head;
+      const float sc = I.sc;
+      const bool valid = row < n_rows;
+      float m_used, l;
+      if (MODE == MODE_SUMI) {
+        MBW(self_full, (uint32_t)(seq & 1));
+        if (n_rows > 0) {
+          const uint8_t* qrow = smem + Ly::Q_OFF + (b * PT_WT + wg) * Ly::QB + row * Ly::RB;
+          const uint8_t* krow = smem + Ly::KS_OFF + wg * Ly::QB + row * Ly::RB;
+          const uint8_t* vrow = smem + Ly::VS_OFF + wg * Ly::QB + row * Ly::RB;
+          auto swz = [&](int j) { return (DH == 64) ? (j ^ (row & 7)) : (j ^ ((row >> 1) & 3)); };
+          float ss = 0.f;
+#pragma unroll
+          for (int j = 0; j < DH / 8; ++j) {
+            float q[8], kk[8];
+            load8(reinterpret_cast<const bf16*>(qrow + (swz(j) << 4)), q);
+            load8(reinterpret_cast<const bf16*>(krow + (swz(j) << 4)), kk);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) ss = fmaf(q[i], kk[i], ss);
+          }
+          m_used = valid ? ss * sc : 0.f;
+          l = 1.f;
+#pragma unroll
+          for (int c = 0; c < DH; c += 32) {  // O = v_self
+            float vs[32];
+#pragma unroll
+            for (int cc = 0; cc < 32; cc += 8) {
+              if (valid) {
+                load8(reinterpret_cast<const bf16*>(vrow + (swz((c + cc) / 8) << 4)), vs + cc);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) vs[cc + i] = 0.f;
+              }
+            }
+            tmem_st32(tO + c, vs);
+          }
+        } else {
+          m_used = 0.f;
+          l = 1.f;
+        }
+        fence_before();
+        mbar_arrive(self_empty);
+      } else {
+        m_used = -INFINITY;
+        l = 0.f;
+      }
+      mbar_arrive(&q_empty[b]);  // descriptor (and q rows) read
+      const bool causal_hist = (MODE == MODE_HIST) && D.causal;
+      const int t_row = tile0 + row;
+      for (int j = 0; j < nch; ++j) {
+        const long long c = cs + j;
+        const int bb = (int)(c % NSB);
+        const uint32_t tSj = tmem_base + wg * 256 + bb * KEYS + lane_off;
+        MBW(&s_full[wg * NSB + bb], (uint32_t)((c / NSB) & 1));
+        fence_after();
+        const int key0 = j * KEYS;
+        int lim = key_end - key0;
+        if (causal_hist) lim = min(lim, t_row - key0 + 1);
+        uint32_t sr[KEYS];
+        tmem_ld32_nw(tSj, sr);
+        tmem_ld32_nw(tSj + 32, sr + 32);
+        tmem_ld_wait();
+        float mx8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
+        const bool full = lim >= KEYS;
+        if (full) {
+#pragma unroll
+          for (int i = 0; i < KEYS; i += 2)
+            mx8[(i >> 1) & 7] = max3(mx8[(i >> 1) & 7], __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < KEYS; ++i)
+            if (i < lim) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(sr[i]));
+        }
+        const float mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                 fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        const float mx = mraw * sc;
+        const bool mine = mx > m_used + RESCALE_LOG2;
+        const float alpha = mine ? exp2f(m_used - mx) : 1.f;
+        if (mine) {
+          l *= alpha;
+          m_used = mx;
+        }
+        if ((MODE == MODE_SUMI || j > 0) && __any_sync(0xffffffffu, mine)) {
+          if (j > 0) MBW(&o_done[wg * NSB + (int)((c - 1) % NSB)], (uint32_t)(((c - 1) / NSB) & 1));
+          fence_after();
+#pragma unroll
+          for (int cc = 0; cc < DH; cc += 32) {
+            float o[32];
+            tmem_ld32(tO + cc, o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] *= alpha;
+            tmem_st32(tO + cc, o);
+          }
+        }
+        const float nb = (m_used == -INFINITY) ? 0.f : -m_used;
+        float ls8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[KEYS / 2];
+        if (full) {
+          const uint64_t sc2 = pk2(sc, sc), nb2 = pk2(nb, nb);
+          uint64_t ls2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+          for (int i = 0; i < KEYS; i += 2) {
+            const float2 x = upk2(fma2(pk2(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])), sc2, nb2));
+            const float e0 = ex2_approx(x.x);
+            const float e1 = ex2_approx(x.y);
+            ls2[(i >> 1) & 3] = add2(ls2[(i >> 1) & 3], pk2(e0, e1));
+            __nv_bfloat162 pp = __floats2bfloat162_rn(e0, e1);
+            pk[i >> 1] = *reinterpret_cast<uint32_t*>(&pp);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 t = upk2(ls2[q]);
+            ls8[2 * q] = t.x;
+            ls8[2 * q + 1] = t.y;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < KEYS; i += 2) {
+            const float e0 = (i < lim) ? ex2_approx(fmaf(__uint_as_float(sr[i]), sc, nb)) : 0.f;
+            const float e1 = (i + 1 < lim) ? ex2_approx(fmaf(__uint_as_float(sr[i + 1]), sc, nb)) : 0.f;
+            ls8[i & 7] += e0;
+            ls8[(i + 1) & 7] += e1;
+            __nv_bfloat162 pp = __floats2bfloat162_rn(e0, e1);
+            pk[i >> 1] = *reinterpret_cast<uint32_t*>(&pp);
+          }
+        }
+        tmem_st16u(tSj, pk);
+        tmem_st16u(tSj + 16, pk + 16);
+        tmem_st_wait();
+        l += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
+        fence_before();
+        mbar_arrive(&p_full[wg * NSB + bb]);
+      }
+      // ---- epilogue: O / l -> bf16, one 2*DH-byte row per thread straight to global
+      if (nch > 0) {
+        const long long c = cs + nch - 1;
+        MBW(&o_done[wg * NSB + (int)(c % NSB)], (uint32_t)((c / NSB) & 1));
+        fence_after();
+      }
+      const bool have_o = (MODE == MODE_SUMI) ? n_rows > 0 : nch > 0;
+      const float inv = (valid && l > 0.f) ? 1.f / l : 0.f;
+      bf16* orow = a.O + (row_base + row) * D.d + head * DH;
+      const bool wr_row = row < rows_out;
+#pragma unroll
+      for (int cc = 0; cc < DH; cc += 32) {
+        float o[32];
+        if (have_o) {
+          tmem_ld32(tO + cc, o);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = 0.f;
+        }
+        if (wr_row) {
+#pragma unroll
+          for (int q = 0; q < 32; q += 8) {
+            float y[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) y[i] = o[q + i] * inv;
+            store8(orow + cc + q, y);
+          }
+        }
+      }
+      fence_before();  // TMEM reads of O complete before the next item's PV / init
+      cs += nch;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -535,32 +1074,57 @@ static void launch_pe(const CUtensorMap& mq, const CUtensorMap& mkv, const Args&
   // CLIMBER_ATTN_1CTA=1 (measurement knob): request enough smem for 1 CTA/SM
   static const int smem = getenv("CLIMBER_ATTN_1CTA") ? 150 * 1024 : Lay<DH>::TOTAL;
   static bool attr = false;
+  static const bool es = [] { const char* e = getenv("CLIMBER_ATTN_EARLY_S"); return !(e && atoi(e) == 0); }();
   if (!attr) {
-    cudaFuncSetAttribute(k_attn_tc<DH, MODE, PE8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_attn_tc<DH, MODE, PE8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_attn_tc<DH, MODE, PE8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  k_attn_tc<DH, MODE, PE8><<<grid, THREADS, smem, s>>>(mq, mkv, a);
+  if (es) k_attn_tc<DH, MODE, PE8, 1><<<grid, THREADS, smem, s>>>(mq, mkv, a);
+  else k_attn_tc<DH, MODE, PE8, 0><<<grid, THREADS, smem, s>>>(mq, mkv, a);
 }
 
-// CLIMBER_ATTN_PE8 overrides the MUFU/FMA split (measurement knob)
-static int pe8_setting() {
-  static int v = [] {
-    const char* e = getenv("CLIMBER_ATTN_PE8");
-    return e ? atoi(e) : 0;
+template <int DH, int MODE>
+static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s) {
+  launch_pe<DH, MODE, 0>(mq, mkv, a, grid, s);
+}
+
+// CLIMBER_ATTN_EARLY_S=0 interleaves S(j+2) with PV(j) after P(j) (measurement knob)
+static bool early_s() {
+  static bool v = [] {
+    const char* e = getenv("CLIMBER_ATTN_EARLY_S");
+    return !(e && atoi(e) == 0);
   }();
   return v;
 }
 
 template <int DH, int MODE>
-static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s) {
-  switch (pe8_setting()) {
-    case 0: launch_pe<DH, MODE, 0>(mq, mkv, a, grid, s); break;
-    case 1: launch_pe<DH, MODE, 1>(mq, mkv, a, grid, s); break;
-    case 3: launch_pe<DH, MODE, 3>(mq, mkv, a, grid, s); break;
-    case 4: launch_pe<DH, MODE, 4>(mq, mkv, a, grid, s); break;
-    case 2: launch_pe<DH, MODE, 2>(mq, mkv, a, grid, s); break;
-    default: launch_pe<DH, MODE, 0>(mq, mkv, a, grid, s); break;
+static void launch_pt(const CUtensorMap& mq, const CUtensorMap& mkv, const PArgs& pa, cudaStream_t s) {
+  constexpr int smem = PLay<DH>::TOTAL;
+  static bool attr = false;
+  static int n_sm = 148;
+  if (!attr) {
+    cudaFuncSetAttribute(k_attn_pt<DH, MODE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_attn_pt<DH, MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    attr = true;
   }
+  if (pa.n_items <= 0) return;
+  const int grid = (int)(pa.n_items < n_sm ? pa.n_items : n_sm);
+  if (early_s()) k_attn_pt<DH, MODE, 1><<<grid, PT_THREADS, smem, s>>>(mq, mkv, pa);
+  else k_attn_pt<DH, MODE, 0><<<grid, PT_THREADS, smem, s>>>(mq, mkv, pa);
+}
+
+// CLIMBER_ATTN_KERNEL=2 selects the persistent two-tile kernel (measured
+// ~16% slower than two one-tile CTAs per SM at `large`; kept as a knob)
+static bool use_pt() {
+  static bool v = [] {
+    const char* e = getenv("CLIMBER_ATTN_KERNEL");
+    return e && atoi(e) == 2;
+  }();
+  return v;
 }
 
 }  // namespace at
@@ -580,6 +1144,13 @@ void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, 
   at::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, at::KEYS);
   at::Args a{QKV, cand_off, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, U, P, D, nullptr};
   dim3 grid((Mmax + at::ROWS - 1) / at::ROWS, D.h, U * nbk);
+  if (at::use_pt()) {
+    at::PArgs pa{a, (int)((grid.x + at::PT_WT - 1) / at::PT_WT), 0};
+    pa.n_items = (long long)pa.n_pairs * D.h * U * nbk;
+    if (D.dh == 64) at::launch_pt<64, at::MODE_SUMI>(mq, mkv, pa, s);
+    else at::launch_pt<32, at::MODE_SUMI>(mq, mkv, pa, s);
+    return;
+  }
   // debug timeline: CLIMBER_ATTN_TRACE=n records the n-th SUMI launch (clock64 per CTA)
   static int trace_at = [] { const char* t = getenv("CLIMBER_ATTN_TRACE"); return t ? atoi(t) : -1; }();
   static int n_launch = 0;
@@ -626,6 +1197,13 @@ void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r,
   at::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, at::KEYS);
   at::Args a{Q, nullptr, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, U, (long long)U * D.nk, D, nullptr};
   dim3 grid(D.nk / at::ROWS, D.h, U * nbk);
+  if (at::use_pt()) {
+    at::PArgs pa{a, (int)((grid.x + at::PT_WT - 1) / at::PT_WT), 0};
+    pa.n_items = (long long)pa.n_pairs * D.h * U * nbk;
+    if (D.dh == 64) at::launch_pt<64, at::MODE_HIST>(mq, mkv, pa, s);
+    else at::launch_pt<32, at::MODE_HIST>(mq, mkv, pa, s);
+    return;
+  }
   if (D.dh == 64) at::launch<64, at::MODE_HIST>(mq, mkv, a, grid, s);
   else at::launch<32, at::MODE_HIST>(mq, mkv, a, grid, s);
 }

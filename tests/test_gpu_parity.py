@@ -202,3 +202,35 @@ def test_rank_host_end_to_end():
                           batch.cand_offsets, batch.cand)
     s_dev = gpu_scores(cl, batch)
     assert np.array_equal(s_host, s_dev)
+
+
+def _one_user(batch, b):
+    """Host arrays of user b alone (offsets rebased to 0)."""
+    e0, e1 = int(batch.ev_offsets[b]), int(batch.ev_offsets[b + 1])
+    c0, c1 = int(batch.cand_offsets[b]), int(batch.cand_offsets[b + 1])
+    return (np.array([0, e1 - e0], np.int64), batch.item[e0:e1], batch.action[e0:e1], batch.scenario[e0:e1],
+            batch.ts[e0:e1], batch.r[b:b + 1], np.array([0, c1 - c0], np.int64), batch.cand[c0:c1])
+
+
+@pytest.mark.parametrize("name", ["small", "medium"])
+def test_latency_mode_cuda_graph(name):
+    # rank_host with B = 1 replays one captured CUDA graph per (events, candidates)
+    # shape; the scores must equal the eager encode + score path bit for bit,
+    # across replays, shape changes and handle slots
+    cfg = synth.preset(name)
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 3, B=4)
+    cl = make_gpu(cfg, w, 4)
+    eager = gpu_scores(cl, batch)
+    n_before = cl.launch_count
+    for rep in range(2):
+        for b in (0, 1, 1, 2, 0, 3):
+            got = cl.rank_host(*_one_user(batch, b))
+            c0, c1 = int(batch.cand_offsets[b]), int(batch.cand_offsets[b + 1])
+            assert np.array_equal(got, eager[c0:c1]), (name, rep, b)
+    assert cl.launch_count > n_before  # replays are counted as kernel launches
+    cl.stream_status()
+    ref = oracle_scores(cfg, w, batch, [1])[1]
+    c0, c1 = int(batch.cand_offsets[1]), int(batch.cand_offsets[2])
+    ab, rel = parity_err(cl.rank_host(*_one_user(batch, 1)), ref)
+    assert ab <= tolerance(cfg) and rel <= tolerance(cfg)
