@@ -16,6 +16,10 @@ Parity status per function (DESIGN.md §2 lists the pins):
   atl_* / encode_user / score_user ... pinned (torch-SDPA reduction, brute force,
                                        zero-weights closed form, rescaling invariants)
   bgf / head ......................... pinned (zero-weights closed form, N_b=1 case)
+  bucket_pos, bucket_time, rel_bias .. pinned (boundary tables written independently,
+                                       shift invariance, (W_q, f_b, tau) rescaling,
+                                       torch-SDPA float-mask reduction, one-hot bias
+                                       closed forms, SUMI == brute force with bias)
   absolute score values .............. parity unpinned (synthetic weights; the paper
                                        prints only AUCs)
 """

@@ -120,9 +120,11 @@ def softmax_tau(z: np.ndarray, tau: float, mask: np.ndarray = None) -> np.ndarra
     return e / np.sum(e, axis=-1, keepdims=True)
 
 
-def attention(Q, K, V, tau_heads, d_h, mask=None):
-    """Multi-head attention of Eq. 3 with f_b = 0 (G6):
-    per head h, A_h = Softmax(Q_h K_h^T / (sqrt(d_h) * tau[h])) (G2, G3), O_h = A_h V_h.
+def attention(Q, K, V, tau_heads, d_h, mask=None, bias=None):
+    """Multi-head attention of Eq. 3: per head h,
+    R_h = Q_h K_h^T + f_b[h]  (f_b = 0 unless ``bias`` [H][T][S] is given, G6),
+    A_h = Softmax(R_h / (sqrt(d_h) * tau[h]))  (G2, G3: Eq. 3 divides R, bias
+    included, by f_tc), O_h = A_h V_h.
     Q [T][d], K,V [S][d], mask [T][S] bool or None.  Heads are contiguous d_h
     column groups."""
     T = Q.shape[0]
@@ -132,9 +134,62 @@ def attention(Q, K, V, tau_heads, d_h, mask=None):
         return out
     for hh in range(H):
         sl = slice(hh * d_h, (hh + 1) * d_h)
-        R = Q[:, sl] @ K[:, sl].T / math.sqrt(d_h)
-        A = softmax_tau(R, float(tau_heads[hh]), mask)
+        R = Q[:, sl] @ K[:, sl].T
+        if bias is not None:
+            R = R + bias[hh]
+        A = softmax_tau(R / math.sqrt(d_h), float(tau_heads[hh]), mask)
         out[:, sl] = A @ V[:, sl]
+    return out
+
+
+# ---------------------------------------------------------------------------
+# relative attention bias f_b^{p,t}(a_k, r) of Eq. 3 (
+# SURVEY §8(f) NEXT-1; readings G6b-G6e in DESIGN.md): a per-(layer, block,
+# scenario, head) table over bucketed position offsets plus one over bucketed
+# time deltas ("bias[head][i][j] = b_pos[..][bucket_p(i-j)] +
+# b_time[..][bucket_t(t_i - t_j)]").
+# ---------------------------------------------------------------------------
+NB_POS = 128                                       # 64 offset buckets per sign
+NB_TIME = 14                                       # 7 time buckets per sign
+TIME_EDGES = (60, 3600, 86400, 604800, 2592000)    # 1 min, 1 h, 1 d, 1 w, 30 d
+
+
+def bucket_pos(delta: int) -> int:
+    """T5-style log buckets, integer-exact (G6c): |delta| < 16 gets
+    its own bucket; above, 4 buckets per octave, 16 + 4 (e - 4) + the two bits
+    after the leading one, e = floor(log2 |delta|), capped at 63; negative
+    offsets (bidirectional history only) use buckets 64..127."""
+    a = abs(int(delta))
+    if a < 16:
+        b = a
+    else:
+        e = a.bit_length() - 1
+        b = min(16 + 4 * (e - 4) + ((a >> (e - 2)) & 3), 63)
+    return b + (64 if delta < 0 else 0)
+
+
+def bucket_time(dt: int) -> int:
+    """Time-delta buckets in seconds {0, <1m, <1h, <1d, <1w, <30d, >=30d}
+    (S:L285); negative deltas use buckets 7..13."""
+    a = abs(int(dt))
+    b = 0 if a == 0 else 1 + sum(1 for edge in TIME_EDGES if a >= edge)
+    return b + (7 if dt < 0 else 0)
+
+
+def rel_bias(b_pos_heads, b_time_heads, pos_q, t_q, pos_k, t_k) -> np.ndarray:
+    """f_b [H][T][S] for query positions/times (pos_q, t_q) and key positions/
+    times (pos_k, t_k); b_*_heads [H][NB]."""
+    dp = np.subtract.outer(np.asarray(pos_q, np.int64), np.asarray(pos_k, np.int64))
+    dt = np.subtract.outer(np.asarray(t_q, np.int64), np.asarray(t_k, np.int64))
+    # the scalar bucket functions, evaluated once per distinct offset
+    up, ip = np.unique(dp, return_inverse=True)
+    ut, it = np.unique(dt, return_inverse=True)
+    bp = np.array([bucket_pos(x) for x in up], np.int64)[ip].reshape(dp.shape)
+    bt = np.array([bucket_time(x) for x in ut], np.int64)[it].reshape(dt.shape)
+    H = len(b_pos_heads)
+    out = np.zeros((H,) + dp.shape, f64)
+    for hh in range(H):
+        out[hh] = np.asarray(b_pos_heads[hh], f64)[bp] + np.asarray(b_time_heads[hh], f64)[bt]
     return out
 
 
@@ -167,12 +222,19 @@ def ffn_residual(X, lw: LayerW, eps):
     return X + silu(rmsnorm(X, lw.g2, eps) @ lw.w1) @ lw.w2
 
 
-def atl_layer(X, lw: LayerW, tau_heads, d_h, mask, eps):
-    """One ATL (Eq. 3) over a whole sequence with an explicit mask.
-    Returns (X_next, K, V)."""
+def atl_layer(X, lw: LayerW, tau_heads, d_h, mask, eps, bias=None):
+    """One ATL (Eq. 3) over a whole sequence with an explicit mask
+    (and relative bias [H][T][T] when given).  Returns (X_next, K, V)."""
     Q, K, V = qkv(X, lw, eps)
-    X = X + attention(Q, K, V, tau_heads, d_h, mask) @ lw.w_o
+    X = X + attention(Q, K, V, tau_heads, d_h, mask, bias) @ lw.w_o
     return ffn_residual(X, lw, eps), K, V
+
+
+def _bias_tables(w, l, k, r):
+    """The (layer, block, scenario) slices of the bias tables, or None (f_b = 0)."""
+    if getattr(w, "b_pos", None) is None:
+        return None
+    return np.asarray(w.b_pos[l, k, r], f64), np.asarray(w.b_time[l, k, r], f64)
 
 
 # ---------------------------------------------------------------------------
@@ -199,11 +261,19 @@ class Cache:
     K: list                  # K[k][l] -> [v_k][d] fp64
     V: list
     r: int
+    t_hist: list = None      # [N_b] -> int64 [v_k] event times of S_k (relative bias)
+    t_req: int = 0           # request time (G6e: the last event's timestamp)
 
 
-def encode_user(cfg, w, strategies, item, action, scenario, r: int) -> Cache:
+def request_time(ts) -> int:
+    """G6e: the events passed to encode end at the request, so the request
+    (= candidate) time is the last event's timestamp; 0 for an empty sequence."""
+    return int(ts[-1]) if ts is not None and len(ts) > 0 else 0
+
+
+def encode_user(cfg, w, strategies, item, action, scenario, r: int, ts=None) -> Cache:
     idx, vlen = extract(action, scenario, strategies, cfg.n_k)
-    Ks, Vs = [], []
+    Ks, Vs, Ts = [], [], []
     for k in range(cfg.N_b):
         X = embed_history(w, item, action, scenario, idx[k])
         v = X.shape[0]
@@ -211,31 +281,43 @@ def encode_user(cfg, w, strategies, item, action, scenario, r: int) -> Cache:
             mask = np.tril(np.ones((v, v), bool))       # G1: causal history
         else:
             mask = np.ones((v, v), bool)
+        sel = idx[k][idx[k] >= 0]
+        t_k = np.asarray(ts, np.int64)[sel] if ts is not None else np.zeros(v, np.int64)
+        pos = np.arange(v)                              # G6d: position = index within S_k
         Kk, Vk = [], []
         for l in range(cfg.L):
             lw = block_layer(w, k, l)
-            X, K, V = atl_layer(X, lw, w.tau[l, k, r], cfg.d_h, mask, cfg.rms_eps)
+            tb = _bias_tables(w, l, k, r)
+            bias = rel_bias(tb[0], tb[1], pos, t_k, pos, t_k) if tb is not None else None
+            X, K, V = atl_layer(X, lw, w.tau[l, k, r], cfg.d_h, mask, cfg.rms_eps, bias)
             Kk.append(K)
             Vk.append(V)
         Ks.append(Kk)
         Vs.append(Vk)
-    return Cache(idx, vlen, Ks, Vs, r)
+        Ts.append(t_k)
+    return Cache(idx, vlen, Ks, Vs, r, Ts, request_time(ts))
 
 
 # ---------------------------------------------------------------------------
 # a4: score M candidates against the cache
 # ---------------------------------------------------------------------------
-def candidate_layer(C, lw: LayerW, tau_heads, d_h, K_hist, V_hist, eps):
+def candidate_layer(C, lw: LayerW, tau_heads, d_h, K_hist, V_hist, eps, tables=None, t_hist=None, t_req=0):
     """Each candidate row attends to the cached history K/V of this layer and
-    to itself only (full-visible to history, diagonal among candidates)."""
+    to itself only (full-visible to history, diagonal among candidates).  With
+    bias tables, a candidate sits at position v_k and time t_req (G6d, G6e)."""
     Q, Ks, Vs = qkv(C, lw, eps)
     Mc = C.shape[0]
-    H = len(tau_heads)
+    v = K_hist.shape[0]
+    bias = None
+    if tables is not None:
+        pos_k = np.arange(v + 1)                        # history 0..v-1, self at v
+        t_k = np.concatenate([np.asarray(t_hist, np.int64), [t_req]])
+        bias = rel_bias(tables[0], tables[1], [v], [t_req], pos_k, t_k)
     O = np.zeros_like(Q)
     for m in range(Mc):
         Kc = np.vstack([K_hist, Ks[m:m + 1]])
         Vc = np.vstack([V_hist, Vs[m:m + 1]])
-        O[m] = attention(Q[m:m + 1], Kc, Vc, tau_heads, d_h)[0]
+        O[m] = attention(Q[m:m + 1], Kc, Vc, tau_heads, d_h, None, bias)[0]
     C = C + O @ lw.w_o
     return ffn_residual(C, lw, eps)
 
@@ -249,7 +331,9 @@ def block_outputs(cfg, w, cache: Cache, cands) -> np.ndarray:
         C = c0.copy()
         for l in range(cfg.L):
             C = candidate_layer(C, block_layer(w, k, l), w.tau[l, k, cache.r], cfg.d_h,
-                                cache.K[k][l], cache.V[k][l], cfg.rms_eps)
+                                cache.K[k][l], cache.V[k][l], cfg.rms_eps,
+                                _bias_tables(w, l, k, cache.r),
+                                cache.t_hist[k] if cache.t_hist is not None else None, cache.t_req)
         E[:, k, :] = C
     return E
 
@@ -284,16 +368,17 @@ def score_user(cfg, w, cache: Cache, cands) -> np.ndarray:
 
 
 def sumi_scores(cfg, w, strategies, batch, b: int) -> np.ndarray:
-    item, action, scenario, _ = batch.user_events(b)
-    cache = encode_user(cfg, w, strategies, item, action, scenario, int(batch.r[b]))
+    item, action, scenario, ts = batch.user_events(b)
+    cache = encode_user(cfg, w, strategies, item, action, scenario, int(batch.r[b]), ts)
     return score_user(cfg, w, cache, batch.user_cands(b))
 
 
 # ---------------------------------------------------------------------------
 # brute force: every item appended alone to [S_k], no cache
 # ---------------------------------------------------------------------------
-def brute_force_scores(cfg, w, strategies, item, action, scenario, r: int, cands) -> np.ndarray:
+def brute_force_scores(cfg, w, strategies, item, action, scenario, r: int, cands, ts=None) -> np.ndarray:
     idx, _ = extract(action, scenario, strategies, cfg.n_k)
+    t_req = request_time(ts)
     out = np.zeros(len(cands), f64)
     for m, c in enumerate(cands):
         E = np.zeros((1, cfg.N_b, cfg.d), f64)
@@ -306,8 +391,14 @@ def brute_force_scores(cfg, w, strategies, item, action, scenario, r: int, cands
             else:                                             # prefix-LM
                 mask = np.ones((T, T), bool)
                 mask[:T - 1, T - 1] = False
+            sel = idx[k][idx[k] >= 0]                         # the sequence [S_k ; item]:
+            pos = np.arange(T)                                # positions 0..T-1
+            t_seq = np.concatenate([np.asarray(ts, np.int64)[sel] if ts is not None else np.zeros(T - 1, np.int64),
+                                    [t_req]])                 # item at the request time
             for l in range(cfg.L):
-                X, _, _ = atl_layer(X, block_layer(w, k, l), w.tau[l, k, r], cfg.d_h, mask, cfg.rms_eps)
+                tb = _bias_tables(w, l, k, r)
+                bias = rel_bias(tb[0], tb[1], pos, t_seq, pos, t_seq) if tb is not None else None
+                X, _, _ = atl_layer(X, block_layer(w, k, l), w.tau[l, k, r], cfg.d_h, mask, cfg.rms_eps, bias)
             E[0, k] = X[-1]
         out[m] = head(cfg, w, bgf(cfg, w, E, r))[0]
     return out

@@ -52,6 +52,7 @@ class Config:
     se_reduction: int = 4
     rms_eps: float = 1e-6
     zipf_s: float = 1.1
+    rel_bias: int = 0     # 1: Eq. 3's relative bias f_b^{p,t}(a_k, r)
 
     @property
     def d_h(self) -> int:
@@ -161,12 +162,33 @@ class Weights:
     b_se2: np.ndarray      # [N_b d]
     w_head: np.ndarray     # [N_b d]
     b_head: np.ndarray     # [1]
+    # relative attention bias tables (Eq. 3 f_b^{p,t}(a_k, r)), only when cfg.rel_bias:
+    b_pos: Optional[np.ndarray] = None   # [L][N_b][R][h][NB_POS]  position-offset buckets
+    b_time: Optional[np.ndarray] = None  # [L][N_b][R][h][NB_TIME] time-delta buckets
 
     def scaled(self, **repl) -> "Weights":
         return dataclasses.replace(self, **repl)
 
 
+# Shapes of the bias tables (interface sizes): 64 position
+# buckets per offset sign, 7 time-delta buckets per sign.
+NB_POS = 128
+NB_TIME = 14
+
+
 def make_weights(cfg: Config, seed: int = 0) -> Weights:
+    w = _make_weights(cfg, seed)
+    if cfg.rel_bias:
+        # a separate stream, so the other parameters do not depend on rel_bias;
+        # std 0.5 sqrt(d_h): comparable to the raw q.k scores the bias is added to
+        rng = np.random.default_rng(np.random.PCG64([seed, 7]))
+        sd = 0.5 * cfg.d_h ** 0.5
+        w.b_pos = _normal(rng, (cfg.L, cfg.N_b, cfg.R, cfg.h, NB_POS), sd)
+        w.b_time = _normal(rng, (cfg.L, cfg.N_b, cfg.R, cfg.h, NB_TIME), sd)
+    return w
+
+
+def _make_weights(cfg: Config, seed: int) -> Weights:
     rng = np.random.default_rng(np.random.PCG64(seed))
     d, L, N_b, F, R, h = cfg.d, cfg.L, cfg.N_b, cfg.F, cfg.R, cfg.h
     Dse, Hse = cfg.D_se, cfg.H_se
@@ -204,7 +226,7 @@ def zero_weights_like(w: Weights, keep=("emb_item", "emb_act", "emb_scn", "w_hea
     """Every listed-not-kept parameter set to 0 (zero-weights closed form)."""
     repl = {}
     for f in dataclasses.fields(w):
-        if f.name not in keep:
+        if f.name not in keep and getattr(w, f.name) is not None:
             repl[f.name] = np.zeros_like(getattr(w, f.name))
     return w.scaled(**repl)
 

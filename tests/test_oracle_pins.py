@@ -343,3 +343,169 @@ def test_flop_counter_vs_table4_shape():
         vals.append(O.flops_user(cfg, [cfg.n_k] * cfg.N_b, 1000)["total"])
     inc = np.diff(vals)
     assert np.all(inc == inc[0])
+
+
+# ---------------------------------------------------------------------------
+# relative attention bias f_b^{p,t}(a_k, r) (Eq. 3; NEXT-1,
+# readings G6b-G6e in DESIGN.md)
+# ---------------------------------------------------------------------------
+def test_bucket_functions_vs_boundary_tables():
+    # positions: 16 exact buckets, then each octave [2^e, 2^(e+1)) cut into 4
+    # equal-width parts (bucket = 16 + 4 (e - 4) + part), capped at 63 (S:L285 T5 style)
+    ref = {}
+    for a in range(0, 20000):
+        if a < 16:
+            ref[a] = a
+        else:
+            e = 4
+            while 2 ** (e + 1) <= a:
+                e += 1
+            part = (a - 2 ** e) // (2 ** e // 4)
+            ref[a] = min(16 + 4 * (e - 4) + part, 63)
+    for a, b in ref.items():
+        assert O.bucket_pos(a) == b, a
+        if a > 0:
+            assert O.bucket_pos(-a) == b + 64
+    assert O.bucket_pos(16) == 16 and O.bucket_pos(20) == 17 and O.bucket_pos(31) == 19
+    assert O.bucket_pos(32) == 20 and O.bucket_pos(1023) == 39 and O.bucket_pos(1 << 20) == 63
+    # time deltas in seconds: {0, <1 min, <1 h, <1 d, <1 w, <30 d, >= 30 d}
+    table = [(0, 0), (1, 1), (59, 1), (60, 2), (3599, 2), (3600, 3), (86399, 3), (86400, 4),
+             (7 * 86400 - 1, 4), (7 * 86400, 5), (30 * 86400 - 1, 5), (30 * 86400, 6), (10 ** 9, 6)]
+    for dt, b in table:
+        assert O.bucket_time(dt) == b, dt
+        if dt > 0:
+            assert O.bucket_time(-dt) == b + 7
+
+
+def _bias_user(cfg, seed, n_s=120, M=6):
+    u = synth.make_user(cfg, np.random.default_rng(seed), n_s=n_s, M=M)
+    return u
+
+
+def test_constant_bias_is_a_softmax_shift():
+    # a bias that is the same for every (query, key) pair of a row cannot change
+    # the softmax (it is added inside R before the normalisation, Eq. 3)
+    cfg = synth.preset("tiny", L=2, rel_bias=1)
+    w = synth.make_weights(cfg, 3)
+    strats = synth.strategies_for(cfg.N_b, cfg.R)
+    u = _bias_user(cfg, 21)
+    w0 = w.scaled(b_pos=None, b_time=None)
+    wc = w.scaled(b_pos=np.full_like(w.b_pos, 1.75), b_time=np.full_like(w.b_time, -0.5))
+    s0, sc, sb = (O.sumi_scores(cfg, ww, strats, u, 0) for ww in (w0, wc, w))
+    assert np.max(np.abs(sc - s0)) < 1e-12
+    assert np.max(np.abs(sb - s0)) > 1e-3        # the drawn tables do matter
+
+
+def test_bias_enters_before_the_temperature():
+    # (W_q, f_b, tau) -> alpha (W_q, f_b, tau) leaves (q.k + f_b) / (sqrt(d_h) tau)
+    # unchanged; scaling the bias less than tau does not (pins R = QK^T + f_b, then / f_tc)
+    cfg = synth.preset("tiny", L=2, rel_bias=1)
+    w = synth.make_weights(cfg, 4)
+    strats = synth.strategies_for(cfg.N_b, cfg.R)
+    u = _bias_user(cfg, 22)
+    base = O.sumi_scores(cfg, w, strats, u, 0)
+    a = 2.5
+    wq = w.w_qkv.copy()
+    wq[..., :cfg.d] *= a
+    w_all = w.scaled(w_qkv=wq, b_pos=w.b_pos * a, b_time=w.b_time * a, tau=w.tau * a)
+    assert np.max(np.abs(O.sumi_scores(cfg, w_all, strats, u, 0) - base)) < 1e-10
+    w_nob = w.scaled(w_qkv=wq, tau=w.tau * a)
+    assert np.max(np.abs(O.sumi_scores(cfg, w_nob, strats, u, 0) - base)) > 1e-4
+
+
+@pytest.mark.parametrize("causal", [1, 0])
+def test_bias_reduces_to_sdpa_float_mask(causal):
+    # N_b = 1: the block stack equals a pre-norm Transformer whose attention is
+    # torch SDPA with an additive float mask f_b / (sqrt(d_h) tau) (library routine)
+    cfg = synth.preset("tiny", N_b=1, n_k=64, L=2, hist_causal=causal, rel_bias=1)
+    w = synth.make_weights(cfg, 6)
+    strats = synth.strategies_for(1, cfg.R)
+    u = _bias_user(cfg, 23, n_s=40, M=3)
+    item, action, scenario, ts = u.user_events(0)
+    r = int(u.r[0])
+    cache = O.encode_user(cfg, w, strats, item, action, scenario, r, ts)
+    E = O.block_outputs(cfg, w, cache, u.user_cands(0))
+    d, dh, H = cfg.d, cfg.d_h, cfg.h
+    for m, c in enumerate(u.user_cands(0)):
+        X = torch.tensor(np.vstack([np.asarray(w.emb_item[item], np.float64) + w.emb_act[action] + w.emb_scn[scenario],
+                                    np.asarray(w.emb_item[c], np.float64) + w.emb_scn[r]]))
+        T = X.shape[0]
+        times = np.concatenate([ts, [ts[-1]]])          # the item sits at the request time
+        for l in range(cfg.L):
+            t = lambda a_: torch.tensor(np.asarray(a_, np.float64))
+            g1, wqkv, wo, g2, w1, w2 = (t(getattr(w, n)[0, l]) for n in ("g1", "w_qkv", "w_o", "g2", "w1", "w2"))
+            P = Fnn.rms_norm(X, (d,), weight=g1, eps=cfg.rms_eps) @ wqkv
+            q, kk, v = (P[:, i * d:(i + 1) * d].view(T, H, dh).transpose(0, 1) for i in range(3))
+            tau = t(w.tau[l, 0, r])
+            q = q / tau.view(H, 1, 1)
+            mask = torch.zeros(H, T, T, dtype=torch.float64)
+            for i in range(T):
+                for j in range(T):
+                    allowed = (j <= i) if causal else (j < T - 1 or i == T - 1)
+                    if not allowed:
+                        mask[:, i, j] = -math.inf
+                        continue
+                    bp, bt = O.bucket_pos(i - j), O.bucket_time(int(times[i]) - int(times[j]))
+                    for hh in range(H):
+                        mask[hh, i, j] = float(w.b_pos[l, 0, r, hh, bp] + w.b_time[l, 0, r, hh, bt]) / (
+                            math.sqrt(dh) * float(tau[hh]))
+            a_ = Fnn.scaled_dot_product_attention(q[None], kk[None], v[None], attn_mask=mask[None])[0]
+            X = X + a_.transpose(0, 1).reshape(T, d) @ wo
+            X = X + Fnn.silu(Fnn.rms_norm(X, (d,), weight=g2, eps=cfg.rms_eps) @ w1) @ w2
+        np.testing.assert_allclose(E[m, 0], X[-1].numpy(), rtol=0, atol=1e-10)
+
+
+def test_one_hot_position_bias_closed_forms():
+    # a dominant bias on one position bucket makes every row attend to exactly
+    # one key: bucket 0 -> itself (A = I), bucket 1 -> the previous token
+    # (offset i - j = +1, pins the sign of the position offset)
+    rng = np.random.default_rng(9)
+    T, H, dh = 7, 2, 4
+    Q, K, V = rng.standard_normal((3, T, H * dh))
+    pos = np.arange(T)
+    t0 = np.zeros(T, np.int64)
+    for bucket, shift in ((0, 0), (1, 1)):
+        bp = np.zeros((H, O.NB_POS))
+        bp[:, bucket] = 1e4
+        bias = O.rel_bias(bp, np.zeros((H, O.NB_TIME)), pos, t0, pos, t0)
+        out = O.attention(Q, K, V, [0.8, 1.7], dh, None, bias)
+        np.testing.assert_allclose(out[shift:], V[:T - shift], rtol=0, atol=1e-12)
+
+
+def test_one_hot_time_bias_picks_the_event_within_the_hour():
+    # the candidate (at the request time t_req = last event) attends only to the
+    # history event whose age t_req - t_j falls in [1 min, 1 h) when that bucket
+    # dominates: pins t_req - t_j (not t_j - t_req) and the bucket edges
+    H, dh = 2, 4
+    t_hist = np.array([0, 100_000, 196_400, 199_000, 199_990], np.int64)   # ages 2e5, 1e5, 3600, 1000, 10
+    t_req = 200_000
+    v = len(t_hist)
+    rng = np.random.default_rng(10)
+    q, ks, vs = rng.standard_normal((3, 1, H * dh))
+    Kh, Vh = rng.standard_normal((2, v, H * dh))
+    bt = np.zeros((H, O.NB_TIME))
+    bt[:, 2] = 1e4                                    # bucket 2 = [60 s, 1 h)
+    bias = O.rel_bias(np.zeros((H, O.NB_POS)), bt, [v], [t_req], np.arange(v + 1),
+                      np.concatenate([t_hist, [t_req]]))
+    out = O.attention(q, np.vstack([Kh, ks]), np.vstack([Vh, vs]), [1.0, 0.6], dh, None, bias)
+    np.testing.assert_allclose(out[0], Vh[3], rtol=0, atol=1e-12)        # age 1000 s only
+
+
+def test_sumi_equals_brute_force_with_bias():
+    rng = np.random.default_rng(12)
+    n_trip = 0
+    for si, sh in enumerate([dict(N_b=2, n_k=8, L=2, d=16, h=2), dict(N_b=1, n_k=12, L=2, d=16, h=4)]):
+        for causal in (1, 0):
+            cfg = synth.preset("tiny", V=200, M=4, hist_causal=causal, rel_bias=1, **sh)
+            w = synth.make_weights(cfg, 200 + si)
+            strats = synth.strategies_for(cfg.N_b, cfg.R)
+            for t in range(12):
+                n_s = int(rng.integers(0, 40))       # includes v_k = 0 cases
+                u = synth.make_user(cfg, rng, n_s=n_s, M=int(rng.integers(1, 5)))
+                item, action, scenario, ts = u.user_events(0)
+                s = O.sumi_scores(cfg, w, strats, u, 0)
+                bf = O.brute_force_scores(cfg, w, strats, item, action, scenario, int(u.r[0]),
+                                          u.user_cands(0), ts)
+                assert np.max(np.abs(s - bf) / np.maximum(np.abs(bf), 1)) < 1e-12
+                n_trip += 1
+    assert n_trip >= 48
