@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define CLIMBER_ABI_VERSION 1
+#define CLIMBER_ABI_VERSION 2  /* 2: climber_config.rel_bias, climber_weights.b_pos / b_time */
 
 typedef enum {
   CLIMBER_OK = 0,
@@ -92,6 +92,14 @@ typedef struct {
   int32_t max_wave_users;   /* users encoded per internal wave (scratch sizing) */
   int32_t max_wave_pairs;   /* candidate pairs scored per internal wave (scratch sizing) */
   int64_t kv_pages;         /* K/V page-pool capacity in pages */
+  int32_t rel_bias;         /* 0: f_b = 0 (the north-star formula, G6); 1: Eq. 3's relative
+                             * attention bias f_b^{p,t}(a_k, r):
+                             * R = QK^T + b_pos[bucket_p(i - j)] + b_time[bucket_t(t_i - t_j)],
+                             * divided by sqrt(d_h) tau with the scores (G6b).  Position =
+                             * index within S_k, a candidate sits at v_k; time = event
+                             * timestamp, a candidate at the request time = the last
+                             * event's timestamp (G6d, G6e).  BF16 needs d_h in {32, 64} and
+                             * n_k % 128 == 0 (tcgen05 attention), else CLIMBER_E_CONFIG. */
 } climber_config;
 
 /* One extraction strategy a_k (Eq. 2): keep event e iff
@@ -139,6 +147,11 @@ typedef struct {
   const float* b_se2;     /* [D]     */
   const float* w_head;    /* [D]     */
   float b_head;
+  const float* b_pos;     /* [L][N_b][R][h][128] position-offset buckets (rel_bias = 1, else NULL):
+                           * |i-j| < 16 -> |i-j|; else 16 + 4 (e - 4) + the 2 bits after the
+                           * leading one of |i-j| (e = floor log2), capped at 63; +64 if i < j */
+  const float* b_time;    /* [L][N_b][R][h][14] time-delta buckets in seconds {0, <1m, <1h, <1d,
+                           * <1w, <30d, >=30d}; +7 if t_i < t_j (rel_bias = 1, else NULL) */
 } climber_weights;
 
 typedef struct climber_ctx_s* climber_ctx_t;

@@ -17,7 +17,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libclimber.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 BF16, FP32 = 0, 1
 STATUS = {0: "OK", 1: "E_INVALID_ARG", 2: "E_CONFIG", 3: "E_OUT_OF_RANGE", 4: "E_UNSORTED",
           5: "E_CAPACITY", 6: "E_STALE", 7: "E_CUDA", 8: "E_NCCL", 9: "E_NUMERIC", 10: "E_UNSUPPORTED"}
@@ -35,7 +35,7 @@ class _Config(C.Structure):
         "abi_version", "d", "n_heads", "n_layers", "n_blocks", "n_k", "ffn_mult", "se_reduction", "vocab",
         "n_actions", "n_scenarios", "max_candidates", "hist_causal", "dtype", "page_tokens")] + [
         ("rms_eps", C.c_float), ("max_batch_users", C.c_int32), ("max_wave_users", C.c_int32),
-        ("max_wave_pairs", C.c_int32), ("kv_pages", C.c_int64)]
+        ("max_wave_pairs", C.c_int32), ("kv_pages", C.c_int64), ("rel_bias", C.c_int32)]
 
 
 class _Strategy(C.Structure):
@@ -51,7 +51,8 @@ WEIGHT_NAMES = ("emb_item", "emb_act", "emb_scn", "g1", "w_qkv", "w_o", "g2", "w
 
 
 class _Weights(C.Structure):
-    _fields_ = [(n, C.c_void_p) for n in WEIGHT_NAMES] + [("b_head", C.c_float)]
+    _fields_ = [(n, C.c_void_p) for n in WEIGHT_NAMES] + [("b_head", C.c_float), ("b_pos", C.c_void_p),
+                                                          ("b_time", C.c_void_p)]
 
 
 _LIB = None
@@ -148,13 +149,14 @@ class ModelConfig:
     hist_causal: int = 1
     dtype: str = "bf16"
     rms_eps: float = 1e-6
+    rel_bias: int = 0
 
     @classmethod
     def from_any(cls, cfg, M_max: Optional[int] = None) -> "ModelConfig":
         return cls(d=cfg.d, h=cfg.h, L=cfg.L, N_b=cfg.N_b, n_k=cfg.n_k, V=cfg.V, R=cfg.R,
                    M_max=M_max or cfg.M, n_actions=getattr(cfg, "n_actions", 6), ffn_mult=cfg.ffn_mult,
                    se_reduction=cfg.se_reduction, hist_causal=cfg.hist_causal, dtype=cfg.dtype,
-                   rms_eps=cfg.rms_eps)
+                   rms_eps=cfg.rms_eps, rel_bias=getattr(cfg, "rel_bias", 0))
 
 
 class Climber:
@@ -186,6 +188,7 @@ class Climber:
         c.max_wave_users = max_wave_users
         c.max_wave_pairs = max_wave_pairs or max(cfg.M_max, min(max_users * cfg.M_max, 65536))
         c.kv_pages = kv_users * per_user
+        c.rel_bias = int(cfg.rel_bias)
         self._c = c
         L = lib()
         nbytes = L.climber_arena_bytes(C.byref(c))
@@ -200,6 +203,12 @@ class Climber:
             self._keep.append(a)
             setattr(w, n, a.ctypes.data)
         w.b_head = float(np.asarray(weights.b_head).reshape(-1)[0])
+        for n in ("b_pos", "b_time"):
+            t = getattr(weights, n, None)
+            if cfg.rel_bias and t is not None:
+                a = np.ascontiguousarray(t, dtype=np.float32)
+                self._keep.append(a)
+                setattr(w, n, a.ctypes.data)
         st = (_Strategy * cfg.N_b)(*[_Strategy(int(a), int(s)) for a, s in strategies])
         h = C.c_void_p()
         _check(L.climber_create(C.byref(c), st, C.byref(w), C.c_void_p(self.arena.data_ptr()), nbytes, 0, 1, None,

@@ -66,6 +66,8 @@ struct climber_ctx_s {
   // weights (device)
   void *e_item, *e_act, *e_scn;
   float *g1, *g2, *tau, *fg1, *fg2, *tau_f, *b_se1, *b_se2, *w_head;
+  float *bpos = nullptr, *btime = nullptr, *cbias = nullptr;  // relative bias (rel_bias = 1)
+  long long *hts = nullptr, *treq = nullptr;
   void *w_qkv, *w_o, *w1, *w2, *fw_qkv, *fw_o, *fw1, *fw2, *w_se1, *w_se2;
   float b_head;
   unsigned long long *amask, *smask;
@@ -162,6 +164,12 @@ static bool dims_from(const climber_config* cfg, Dims* D, std::string* why) {
   D->F = cfg->ffn_mult * cfg->d; D->Dse = cfg->n_blocks * cfg->d; D->Hse = D->Dse / cfg->se_reduction;
   D->V = cfg->vocab; D->A = cfg->n_actions; D->R = cfg->n_scenarios; D->Mmax = cfg->max_candidates;
   D->causal = cfg->hist_causal ? 1 : 0; D->ppb = (cfg->n_k + PAGE - 1) / PAGE; D->eps = cfg->rms_eps;
+  D->bpos = D->btime = nullptr; D->hts = D->treq = nullptr; D->cbias = nullptr;
+  if (cfg->rel_bias != 0 && cfg->rel_bias != 1) { *why = "rel_bias must be 0 or 1"; return false; }
+  if (cfg->rel_bias && cfg->dtype == CLIMBER_BF16 && !((dh == 32 || dh == 64) && cfg->n_k % 128 == 0)) {
+    *why = "rel_bias on the bf16 path needs d_h in {32, 64} and n_k % 128 == 0 (tcgen05 attention)";
+    return false;
+  }
   return true;
 }
 
@@ -193,6 +201,10 @@ static void carve(climber_ctx_s* c, Carver& cv) {
   cv.take(c->w_head, (size_t)D.Dse * 4);
   cv.take(c->amask, Nb * 8);
   cv.take(c->smask, Nb * 8);
+  if (c->cfg.rel_bias) {
+    cv.take(c->bpos, L * Nb * D.R * D.h * NB_POS * 4);
+    cv.take(c->btime, L * Nb * D.R * D.h * NB_TIME * 4);
+  }
   // K/V pool: page = [2][h][64][dh]
   c->per_slot = D.Nb * D.L * D.ppb;
   c->n_pages = c->cfg.kv_pages;
@@ -204,6 +216,11 @@ static void carve(climber_ctx_s* c, Carver& cv) {
   cv.take(c->idx_all, S * Nb * D.nk * 4);
   cv.take(c->bad_all, S * 4);
   cv.take(c->err, 256);
+  if (c->cfg.rel_bias) {  // per handle: history token times, request time, candidate bias rows
+    cv.take(c->hts, S * Nb * D.nk * 8);
+    cv.take(c->treq, S * 8);
+    cv.take(c->cbias, S * L * Nb * D.h * D.nk * 4);
+  }
   // per-call metadata
   size_t Bm = c->cfg.max_batch_users;
   cv.take(c->d_ev_off, (Bm + 1) * 8);
@@ -295,6 +312,8 @@ extern "C" climber_status climber_create(const climber_config* cfg, const climbe
                            w->w_se1, w->b_se1, w->w_se2, w->b_se2, w->w_head};
     for (const float* p : need)
       if (!p) return fail(CLIMBER_E_INVALID_ARG, "null weight pointer");
+    if (cfg->rel_bias && (!w->b_pos || !w->b_time))
+      return fail(CLIMBER_E_INVALID_ARG, "rel_bias = 1 needs the b_pos and b_time tables");
     size_t ntau = (size_t)D.L * D.Nb * D.R * D.h;
     for (size_t i = 0; i < ntau; ++i)
       if (!(w->tau[i] > 0.f) || !std::isfinite(w->tau[i])) return fail(CLIMBER_E_CONFIG, "tau[%zu] <= 0 or non-finite", i);
@@ -382,6 +401,15 @@ extern "C" climber_status climber_create(const climber_config* cfg, const climbe
     up.put(c->w_se2, w->w_se2, 1, D.Hse, D.Dse, true, true);
     up.put(c->b_se2, w->b_se2, 1, 1, D.Dse, false, false);
     up.put(c->w_head, w->w_head, 1, 1, D.Dse, false, false);
+    if (cfg->rel_bias) {  // fp32 tables, as given
+      up.put(c->bpos, w->b_pos, 1, 1, (size_t)L * Nb * D.R * D.h * NB_POS, false, false);
+      up.put(c->btime, w->b_time, 1, 1, (size_t)L * Nb * D.R * D.h * NB_TIME, false, false);
+      c->D.bpos = c->bpos;
+      c->D.btime = c->btime;
+      c->D.hts = c->hts;
+      c->D.treq = c->treq;
+      c->D.cbias = c->cbias;
+    }
     if (up.st != CLIMBER_OK) {
       delete c;
       return up.st;
@@ -511,6 +539,10 @@ static void encode_wave(climber_ctx_s* c, const EventsDev& ev, int u0, int U, lo
     Prof p(c, CLIMBER_K_EXTRACT, s, 0, (double)n_events * 14 + (double)U * D.Nb * D.nk * 4);
     launch_extract(ev, c->d_ev_off + u0, wslot, U, c->amask, c->smask, c->idx_all, c->vlen_all, c->bad_all, c->err,
                    D, s);
+  }
+  if (c->cfg.rel_bias) {
+    Prof p(c, CLIMBER_K_OTHER, s, 0, (double)U * D.L * D.Nb * D.h * D.nk * 12);
+    launch_cand_bias(wslot, c->d_r + u0, U, c->vlen_all, D, s);
   }
   T* H = (T*)c->H;
   T* Qb = (T*)c->QKV;
@@ -728,6 +760,10 @@ static void encode_wave_fused(climber_ctx_s* c, const EventsDev& ev, int u0, int
     launch_extract(ev, c->d_ev_off + u0, wslot, U, c->amask, c->smask, c->idx_all, c->vlen_all, c->bad_all, c->err,
                    D, s);
   }
+  if (c->cfg.rel_bias) {
+    Prof p(c, CLIMBER_K_OTHER, s, 0, (double)U * D.L * D.Nb * D.h * D.nk * 12);
+    launch_cand_bias(wslot, c->d_r + u0, U, c->vlen_all, D, s);
+  }
   bf16* Xb = (bf16*)c->Xb;
   bf16* Qb = (bf16*)c->QKV;
   bf16* O = (bf16*)c->O;
@@ -887,6 +923,10 @@ static void encode_wave_grouped(climber_ctx_s* c, const EventsDev& ev, int u0, i
     Prof p(c, CLIMBER_K_EXTRACT, s, 0, (double)n_events * 14 + (double)U * D.Nb * D.nk * 4);
     launch_extract(ev, c->d_ev_off + u0, wslot, U, c->amask, c->smask, c->idx_all, c->vlen_all, c->bad_all, c->err,
                    D, s);
+  }
+  if (c->cfg.rel_bias) {
+    Prof p(c, CLIMBER_K_OTHER, s, 0, (double)U * D.L * D.Nb * D.h * D.nk * 12);
+    launch_cand_bias(wslot, c->d_r + u0, U, c->vlen_all, D, s);
   }
   bf16* Xb = (bf16*)c->Xb;   // [Nb][rows][d]
   bf16* Qb = (bf16*)c->QKV;  // [Nb][rows][d]
@@ -1230,6 +1270,7 @@ extern "C" size_t climber_kv_slab_bytes(climber_ctx_t c) {
 
 extern "C" climber_status climber_kv_export(climber_ctx_t c, climber_kv_t kv, void* slab, climber_stream_t stream) {
   if (!c || !slab) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+  if (c->cfg.rel_bias) return fail(CLIMBER_E_UNSUPPORTED, "K/V slabs do not carry the relative-bias state yet");
   if (reinterpret_cast<uintptr_t>(slab) % 16) return fail(CLIMBER_E_INVALID_ARG, "slab must be 16-byte aligned");
   int slot;
   {
@@ -1249,6 +1290,7 @@ extern "C" climber_status climber_kv_export(climber_ctx_t c, climber_kv_t kv, vo
 extern "C" climber_status climber_kv_import(climber_ctx_t c, const void* slab, int32_t scenario_r,
                                             climber_stream_t stream, climber_kv_t* out) {
   if (!c || !slab || !out) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+  if (c->cfg.rel_bias) return fail(CLIMBER_E_UNSUPPORTED, "K/V slabs do not carry the relative-bias state yet");
   if (reinterpret_cast<uintptr_t>(slab) % 16) return fail(CLIMBER_E_INVALID_ARG, "slab must be 16-byte aligned");
   if (scenario_r < 0 || scenario_r >= c->D.R) return fail(CLIMBER_E_OUT_OF_RANGE, "scenario_r out of range");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -137,7 +137,7 @@ struct Args {
 constexpr int TRACE_N = 48;  // CLIMBER_ATTN_TRACE_BUILD: 0-23 softmax timeline, 24-31 MMA p_full seen, 32-39 QK issue
 
 // PE8: how many of every 8 scores take ex2_poly instead of the MUFU
-template <int DH, int MODE, int PE8, int ES = 0>
+template <int DH, int MODE, int PE8, int ES = 0, int BIAS = 0>
 __global__ void __launch_bounds__(THREADS, 2)
     k_attn_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, Args a) {
   using Ly = Lay<DH>;
@@ -319,6 +319,23 @@ __global__ void __launch_bounds__(THREADS, 2)
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
     const bool valid = row < n_rows;
     const int t_row = tile0 + row;
+    // relative bias (Eq. 3 f_b, BIAS = 1): this (layer, block, scenario,
+    // head)'s tables staged in smem; history token times / candidate-row bias
+    float* sbp = reinterpret_cast<float*>(smem + Ly::BAR_OFF + 512);
+    float* sbt = sbp + NB_POS;
+    const long long* ht = nullptr;
+    const float* cbr = nullptr;
+    long long t_time = 0;
+    if constexpr (BIAS) {
+      const long long br = bias_row(D, a.l, kblk, r, head);
+      const int i = ew * 32 + lane;
+      sbp[i] = D.bpos[br * NB_POS + i];
+      if (i < NB_TIME) sbt[i] = D.btime[br * NB_TIME + i];
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      ht = D.hts + ((long long)slot * D.Nb + kblk) * D.nk;
+      cbr = D.cbias + ((((long long)slot * D.L + a.l) * D.Nb + kblk) * D.h + head) * D.nk;
+      if (MODE == MODE_HIST && t_row < v) t_time = ht[t_row];
+    }
     float m_used, l;
     if (MODE == MODE_SUMI) {
       // self term from the TMA-loaded q / k_self / v_self tiles (row = lane's
@@ -337,6 +354,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 #pragma unroll
         for (int i = 0; i < 8; ++i) ss = fmaf(q[i], kk[i], ss);
       }
+      if constexpr (BIAS) ss += sbp[bucket_pos(0)] + sbt[bucket_time(0)];  // self: offset 0, delta 0
       m_used = valid ? ss * sc : 0.f;
       l = 1.f;
 #pragma unroll
@@ -375,6 +393,29 @@ __global__ void __launch_bounds__(THREADS, 2)
       tmem_ld32_nw(tSj, sr);
       tmem_ld32_nw(tSj + 32, sr + 32);
       tmem_ld_wait();
+      if constexpr (BIAS) {  // R = QK^T + f_b (before the 1/(sqrt(d_h) tau) scaling, Eq. 3)
+        if (MODE == MODE_SUMI) {
+          const float4* c4 = reinterpret_cast<const float4*>(cbr + key0);
+#pragma unroll
+          for (int i = 0; i < KEYS; i += 4) {
+            const float4 b = c4[i >> 2];
+            sr[i] = __float_as_uint(__uint_as_float(sr[i]) + b.x);
+            sr[i + 1] = __float_as_uint(__uint_as_float(sr[i + 1]) + b.y);
+            sr[i + 2] = __float_as_uint(__uint_as_float(sr[i + 2]) + b.z);
+            sr[i + 3] = __float_as_uint(__uint_as_float(sr[i + 3]) + b.w);
+          }
+        } else {
+          const longlong2* h2 = reinterpret_cast<const longlong2*>(ht + key0);
+#pragma unroll
+          for (int i = 0; i < KEYS; i += 2) {
+            const longlong2 tk = h2[i >> 1];
+            const float b0 = sbp[bucket_pos(t_row - (key0 + i))] + sbt[bucket_time(t_time - tk.x)];
+            const float b1 = sbp[bucket_pos(t_row - (key0 + i + 1))] + sbt[bucket_time(t_time - tk.y)];
+            sr[i] = __float_as_uint(__uint_as_float(sr[i]) + b0);
+            sr[i + 1] = __float_as_uint(__uint_as_float(sr[i + 1]) + b1);
+          }
+        }
+      }
       const int tph = -1;
       if (tph >= 0) tr[tph] = clock64();
       float mx8[8];
@@ -1073,14 +1114,17 @@ template <int DH, int MODE, int PE8>
 static void launch_pe(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s) {
   // CLIMBER_ATTN_1CTA=1 (measurement knob): request enough smem for 1 CTA/SM
   static const int smem = getenv("CLIMBER_ATTN_1CTA") ? 150 * 1024 : Lay<DH>::TOTAL;
+  constexpr int smem_b = Lay<DH>::TOTAL + 1024;  // + the staged relative-bias tables
   static bool attr = false;
   static const bool es = [] { const char* e = getenv("CLIMBER_ATTN_EARLY_S"); return !(e && atoi(e) == 0); }();
   if (!attr) {
     cudaFuncSetAttribute(k_attn_tc<DH, MODE, PE8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(k_attn_tc<DH, MODE, PE8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_attn_tc<DH, MODE, PE8, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_b);
     attr = true;
   }
-  if (es) k_attn_tc<DH, MODE, PE8, 1><<<grid, THREADS, smem, s>>>(mq, mkv, a);
+  if (a.D.bpos) k_attn_tc<DH, MODE, PE8, 1, 1><<<grid, THREADS, smem_b, s>>>(mq, mkv, a);
+  else if (es) k_attn_tc<DH, MODE, PE8, 1><<<grid, THREADS, smem, s>>>(mq, mkv, a);
   else k_attn_tc<DH, MODE, PE8, 0><<<grid, THREADS, smem, s>>>(mq, mkv, a);
 }
 
@@ -1144,7 +1188,7 @@ void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, 
   at::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, at::KEYS);
   at::Args a{QKV, cand_off, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, U, P, D, nullptr};
   dim3 grid((Mmax + at::ROWS - 1) / at::ROWS, D.h, U * nbk);
-  if (at::use_pt()) {
+  if (at::use_pt() && !D.bpos) {
     at::PArgs pa{a, (int)((grid.x + at::PT_WT - 1) / at::PT_WT), 0};
     pa.n_items = (long long)pa.n_pairs * D.h * U * nbk;
     if (D.dh == 64) at::launch_pt<64, at::MODE_SUMI>(mq, mkv, pa, s);
@@ -1197,7 +1241,7 @@ void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r,
   at::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, at::KEYS);
   at::Args a{Q, nullptr, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, U, (long long)U * D.nk, D, nullptr};
   dim3 grid(D.nk / at::ROWS, D.h, U * nbk);
-  if (at::use_pt()) {
+  if (at::use_pt() && !D.bpos) {
     at::PArgs pa{a, (int)((grid.x + at::PT_WT - 1) / at::PT_WT), 0};
     pa.n_items = (long long)pa.n_pairs * D.h * U * nbk;
     if (D.dh == 64) at::launch_pt<64, at::MODE_HIST>(mq, mkv, pa, s);

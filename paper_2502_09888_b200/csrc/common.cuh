@@ -11,11 +11,51 @@ namespace climber {
 
 typedef __nv_bfloat16 bf16;
 
-// Model dimensions, passed by value to kernels.
+// Model dimensions, passed by value to kernels.  The relative-bias pointers
+// are ctx-lifetime device arrays (nullptr when rel_bias = 0, Eq. 3
+// f_b = 0): tables b_pos [L][Nb][R][h][NB_POS], b_time [L][Nb][R][h][NB_TIME];
+// hts [slot][Nb][nk] the event time of every extracted history token, treq
+// [slot] the request time; cbias [slot][L][Nb][h][nk] the candidate-row bias
+// over the history keys (the same for every candidate of a request).
 struct Dims {
   int d, h, dh, L, Nb, nk, F, Dse, Hse, V, A, R, Mmax, causal, ppb;
   float eps;
+  const float* bpos;
+  const float* btime;
+  long long* hts;
+  long long* treq;
+  float* cbias;
 };
+
+// ---- relative attention bias buckets (Eq. 3 f_b^{p,t}; G6c) ----
+constexpr int NB_POS = 128;   // 64 position-offset buckets per sign
+constexpr int NB_TIME = 14;   // 7 time-delta buckets per sign
+__host__ __device__ __forceinline__ int bucket_pos(int delta) {
+  const int a = delta < 0 ? -delta : delta;
+  int b;
+  if (a < 16) {
+    b = a;
+  } else {
+#ifdef __CUDA_ARCH__
+    const int e = 31 - __clz(a);  // floor(log2 a)
+#else
+    int e = 31;
+    while (!((a >> e) & 1)) --e;
+#endif
+    b = 16 + 4 * (e - 4) + ((a >> (e - 2)) & 3);
+    b = b < 63 ? b : 63;
+  }
+  return b + (delta < 0 ? 64 : 0);
+}
+__host__ __device__ __forceinline__ int bucket_time(long long dt) {
+  const long long a = dt < 0 ? -dt : dt;
+  const int b = a == 0 ? 0 : a < 60 ? 1 : a < 3600 ? 2 : a < 86400 ? 3 : a < 604800 ? 4 : a < 2592000 ? 5 : 6;
+  return b + (dt < 0 ? 7 : 0);
+}
+// the (layer, block, scenario, head) row of a bias table
+__host__ __device__ __forceinline__ long long bias_row(const Dims& D, int l, int k, int r, int head) {
+  return (((long long)l * D.Nb + k) * D.R + r) * D.h + head;
+}
 
 // Device error word bits (climber_stream_status maps them to statuses).
 enum : int { ERR_RANGE = 1, ERR_UNSORTED = 2, ERR_CONFIG = 4 };

@@ -58,7 +58,40 @@ __global__ void k_extract(const int32_t* __restrict__ item, const uint8_t* __res
     int v = min(cnt, D.nk);
     for (int p = lane; p < D.nk - v; p += 32) idx[p] = -1;
     if (lane == 0) vlen_all[(long long)slot * D.Nb + k] = v;
+    if (D.hts) {  // relative bias: the event time of history token p (chronological)
+      __syncwarp();
+      long long* hts = D.hts + ((long long)slot * D.Nb + k) * D.nk;
+      for (int p = lane; p < v; p += 32) hts[p] = ts[s + idx[D.nk - v + p]];
+    }
   }
+  // G6e: the request (= candidate) time is the last event's timestamp
+  if (D.treq && threadIdx.x == 0) D.treq[slot] = e > s ? ts[e - 1] : 0;
+}
+
+// Relative bias of the candidate rows (Eq. 3 f_b, NEXT-1): a candidate sits at
+// position v and time t_req, so its bias over history key j,
+// b_pos[bucket_pos(v - j)] + b_time[bucket_time(t_req - t_j)], is the same for
+// every candidate of the request: computed once per (user, layer, block, head)
+// at encode.  grid (U, L * Nb * h), block 128 over the keys.
+__global__ void k_cand_bias(const int* __restrict__ wave_slot, const int* __restrict__ wave_r,
+                            const int* __restrict__ vlen_all, Dims D) {
+  const int u = blockIdx.x;
+  const int head = blockIdx.y % D.h, k = (blockIdx.y / D.h) % D.Nb, l = blockIdx.y / (D.h * D.Nb);
+  const int slot = wave_slot[u], r = wave_r[u];
+  const int v = vlen_all[(long long)slot * D.Nb + k];
+  const long long tq = D.treq[slot];
+  const long long row = bias_row(D, l, k, r, head);
+  const float* bp = D.bpos + row * NB_POS;
+  const float* bt = D.btime + row * NB_TIME;
+  const long long* ht = D.hts + ((long long)slot * D.Nb + k) * D.nk;
+  float* out = D.cbias + ((((long long)slot * D.L + l) * D.Nb + k) * D.h + head) * D.nk;
+  for (int j = threadIdx.x; j < D.nk; j += blockDim.x)
+    out[j] = j < v ? bp[bucket_pos(v - j)] + bt[bucket_time(tq - ht[j])] : 0.f;
+}
+
+void launch_cand_bias(const int* wave_slot, const int* wave_r, int U, const int* vlen_all, const Dims& D,
+                      cudaStream_t s) {
+  k_cand_bias<<<dim3(U, D.L * D.Nb * D.h), 128, 0, s>>>(wave_slot, wave_r, vlen_all, D);
 }
 
 // ===========================================================================
@@ -264,9 +297,10 @@ __device__ __forceinline__ void load_kv_chunk(float (*Ks)[DH + 1], float (*Vs)[D
   }
 }
 
-template <int DH>
-__device__ __forceinline__ void online_chunk(const float (*Ks)[DH + 1], const float (*Vs)[DH + 1],
-                                             const float* q, float* o, float& m, float& l, int jmax) {
+// with a relative bias: bias(j) is the (already log2-scaled) bias of key j of the chunk
+template <int DH, typename FB>
+__device__ __forceinline__ void online_chunk_b(const float (*Ks)[DH + 1], const float (*Vs)[DH + 1],
+                                               const float* q, float* o, float& m, float& l, int jmax, FB bias) {
   // keys j < jmax of the staged chunk are visible to this thread
   if (jmax <= 0) return;
   float s[KC];
@@ -276,7 +310,7 @@ __device__ __forceinline__ void online_chunk(const float (*Ks)[DH + 1], const fl
     float acc = 0.f;
 #pragma unroll
     for (int c = 0; c < DH; ++c) acc = fmaf(q[c], Ks[j][c], acc);
-    s[j] = (j < jmax) ? acc : -INFINITY;
+    s[j] = (j < jmax) ? acc + bias(j) : -INFINITY;
     cmax = fmaxf(cmax, s[j]);
   }
   float mn = fmaxf(m, cmax);
@@ -293,6 +327,13 @@ __device__ __forceinline__ void online_chunk(const float (*Ks)[DH + 1], const fl
   }
   m = mn;
 }
+
+template <int DH>
+__device__ __forceinline__ void online_chunk(const float (*Ks)[DH + 1], const float (*Vs)[DH + 1],
+                                             const float* q, float* o, float& m, float& l, int jmax) {
+  online_chunk_b<DH>(Ks, Vs, q, o, m, l, jmax, [](int) { return 0.f; });
+}
+
 
 // SUMI candidate attention: candidate (u, m) of block k,
 // layer l attends to the v cached history keys of its user/block/layer and to
@@ -333,18 +374,26 @@ __global__ void __launch_bounds__(128) k_attn_sumi(const T* __restrict__ QKV, co
       q[c] *= sc;
       ss = fmaf(q[c], ks[c], ss);
     }
+    if (D.bpos) {  // self: position offset 0, time delta 0
+      const long long br = bias_row(D, l, k, r, head);
+      ss += sc * (D.bpos[br * NB_POS + bucket_pos(0)] + D.btime[br * NB_TIME + bucket_time(0)]);
+    }
     m = ss;      // self term first: weight exp2(0) = 1 on v_self
     lsum = 1.f;
   } else {
 #pragma unroll
     for (int c = 0; c < DH; ++c) q[c] = o[c] = 0.f;
   }
+  const float* cb = D.cbias ? D.cbias + ((((long long)slot * D.L + l) * D.Nb + k) * D.h + head) * D.nk : nullptr;
   for (int t0 = 0; t0 < v; t0 += KC) {
     int nkeys = min(KC, v - t0);
     __syncthreads();
     load_kv_chunk<T, DH>(Ks, Vs, pool, pages, t0, nkeys, head, D.d);
     __syncthreads();
-    if (active) online_chunk<DH>(Ks, Vs, q, o, m, lsum, nkeys);
+    if (active) {
+      if (cb) online_chunk_b<DH>(Ks, Vs, q, o, m, lsum, nkeys, [&](int j) { return sc * cb[t0 + j]; });
+      else online_chunk<DH>(Ks, Vs, q, o, m, lsum, nkeys);
+    }
   }
   if (active) {
     float inv = 1.f / lsum;
@@ -401,7 +450,18 @@ __global__ void __launch_bounds__(128) k_attn_hist(const T* __restrict__ Q, cons
     __syncthreads();
     if (active) {
       int jmax = D.causal ? min(nkeys, t - t0 + 1) : nkeys;
-      online_chunk<DH>(Ks, Vs, q, o, m, lsum, jmax);
+      if (D.bpos) {  // relative bias of (row t, key t0 + j): offset and time delta
+        const long long br = bias_row(D, l, k, r, head);
+        const float* bp = D.bpos + br * NB_POS;
+        const float* bt = D.btime + br * NB_TIME;
+        const long long* ht = D.hts + ((long long)slot * D.Nb + k) * D.nk;
+        const long long tt = ht[t];
+        online_chunk_b<DH>(Ks, Vs, q, o, m, lsum, jmax, [&](int j) {
+          return sc * (bp[bucket_pos(t - (t0 + j))] + bt[bucket_time(tt - ht[t0 + j])]);
+        });
+      } else {
+        online_chunk<DH>(Ks, Vs, q, o, m, lsum, jmax);
+      }
     }
   }
   T* out = O + row * D.d + head * DH;

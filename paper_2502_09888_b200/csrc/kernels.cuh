@@ -11,6 +11,9 @@ struct EventsDev {
   const int64_t* ts;
 };
 
+// relative bias (rel_bias = 1): candidate-row bias over the history keys, per (user, layer, block, head)
+void launch_cand_bias(const int* wave_slot, const int* wave_r, int U, const int* vlen_all, const Dims& D,
+                      cudaStream_t s);
 void launch_extract(const EventsDev& ev, const int64_t* ev_off, const int* wave_slot, int U,
                     const unsigned long long* amask, const unsigned long long* smask, int* idx_all,
                     int* vlen_all, int* bad_all, int* err, const Dims& D, cudaStream_t s);

@@ -38,9 +38,10 @@ def test_struct_layout_matches_header():
 #include <stddef.h>
 #include "climber.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(climber_config), offsetof(climber_config, rms_eps),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(climber_config), offsetof(climber_config, rms_eps),
          offsetof(climber_config, kv_pages), sizeof(climber_weights), offsetof(climber_weights, b_head),
-         sizeof(climber_events), sizeof(climber_strategy));
+         sizeof(climber_events), sizeof(climber_strategy), offsetof(climber_config, rel_bias),
+         offsetof(climber_weights, b_pos), offsetof(climber_weights, b_time));
   return 0;
 }
 '''
@@ -52,14 +53,15 @@ int main(void) {
         got = list(map(int, subprocess.check_output([exe]).split()))
     exp = [C.sizeof(climber._Config), climber._Config.rms_eps.offset, climber._Config.kv_pages.offset,
            C.sizeof(climber._Weights), climber._Weights.b_head.offset, C.sizeof(climber._Events),
-           C.sizeof(climber._Strategy)]
+           C.sizeof(climber._Strategy), climber._Config.rel_bias.offset, climber._Weights.b_pos.offset,
+           climber._Weights.b_time.offset]
     assert got == exp
 
 
 def _cfg(**kw):
     from paper_2502_09888_b200 import climber
     c = climber._Config()
-    vals = dict(abi_version=1, d=128, n_heads=4, n_layers=2, n_blocks=4, n_k=64, ffn_mult=4, se_reduction=4,
+    vals = dict(abi_version=climber.ABI_VERSION, d=128, n_heads=4, n_layers=2, n_blocks=4, n_k=64, ffn_mult=4, se_reduction=4,
                 vocab=1000, n_actions=6, n_scenarios=4, max_candidates=128, hist_causal=1, dtype=0, page_tokens=64,
                 rms_eps=1e-6, max_batch_users=8, max_wave_users=8, max_wave_pairs=1024, kv_pages=64)
     vals.update(kw)
@@ -75,9 +77,11 @@ def test_arena_bytes_and_config_validation_on_host():
     assert n > 0
     # more pages -> more bytes, exactly page_bytes per page (page = 2 * 64 * d bf16)
     n2 = L.climber_arena_bytes(C.byref(_cfg(kv_pages=128)))
+    assert L.climber_arena_bytes(C.byref(_cfg(rel_bias=1, dtype=1))) > n   # fp32: any n_k, + bias state
     assert n2 - n >= 64 * 2 * 64 * 128 * 2
     for bad in (dict(d=100), dict(n_heads=3), dict(n_k=48), dict(n_blocks=9), dict(page_tokens=32),
-                dict(abi_version=2), dict(dtype=7), dict(max_wave_pairs=10)):
+                dict(abi_version=1), dict(dtype=7), dict(max_wave_pairs=10), dict(rel_bias=2),
+                dict(rel_bias=1)):   # rel_bias on bf16 needs n_k % 128 == 0 (here 64)
         assert L.climber_arena_bytes(C.byref(_cfg(**bad))) == 0, bad
     # create rejects a bad config synchronously, before touching the device
     h = C.c_void_p()

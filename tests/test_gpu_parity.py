@@ -234,3 +234,35 @@ def test_latency_mode_cuda_graph(name):
     c0, c1 = int(batch.cand_offsets[1]), int(batch.cand_offsets[2])
     ab, rel = parity_err(cl.rank_host(*_one_user(batch, 1)), ref)
     assert ab <= tolerance(cfg) and rel <= tolerance(cfg)
+
+
+# ---------------------------------------------------------------------------
+# Eq. 3 relative attention bias f_b^{p,t}(a_k, r)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("causal", [1, 0])
+def test_rel_bias_fp32_tiny(causal):
+    cfg = synth.preset("tiny", L=2, B=3, hist_causal=causal, rel_bias=1)
+    _check_cfg(cfg, B=3, users=[0, 1, 2])
+
+
+@pytest.mark.parametrize("name,users", [("medium", [0, 3]), ("large", [0])])
+def test_rel_bias_bf16(name, users):
+    cfg = synth.preset(name, rel_bias=1)
+    _check_cfg(cfg, B=4, users=users, max_wave_pairs=4 * cfg.M)
+    # the bias is live on this path: the same inputs without it score differently
+    batch = synth.make_batch(cfg, 1, B=2)
+    w = synth.make_weights(cfg, 0)
+    with_b = gpu_scores(make_gpu(cfg, w, 2), batch)
+    cfg0 = cfg.replace(rel_bias=0)
+    without = gpu_scores(make_gpu(cfg0, w, 2), batch)
+    assert np.max(np.abs(with_b - without)) > 0.05
+
+
+def test_rel_bias_bf16_latency_mode_and_config_errors():
+    from paper_2502_09888_b200 import ClimberError
+    cfg = synth.preset("medium", rel_bias=1)
+    _check_cfg(cfg, B=1, users=[0])           # single request: small-launch GEMM tiles
+    bad = synth.preset("small", rel_bias=1)   # n_k = 64: no tcgen05 history attention
+    with pytest.raises(ClimberError) as ei:
+        make_gpu(bad, synth.make_weights(bad, 0), 1)
+    assert ei.value.name == "E_CONFIG"
