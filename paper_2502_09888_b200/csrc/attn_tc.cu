@@ -186,6 +186,13 @@ __global__ void __launch_bounds__(THREADS, 2)
   }
   const int n_chunks = (key_end + KEYS - 1) / KEYS;
 
+  // page ids of this (user, block, layer), requested before the setup so the
+  // global-load latency overlaps barrier init and TMEM allocation
+  int pg0 = 0, pg1 = 0;
+  if (warp == 0) {
+    if (lane < n_chunks) pg0 = pages[lane];
+    if (lane + 32 < n_chunks) pg1 = pages[lane + 32];
+  }
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmQ) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmKV) : "memory");
@@ -201,6 +208,17 @@ __global__ void __launch_bounds__(THREADS, 2)
       mbar_init(&o_done[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the query-side tiles go out first: their TMA round trip (~3k cycles
+    // under load) is the head of every CTA's critical path
+    if (MODE == MODE_SUMI) {  // q, k_self, v_self of the tile's candidates
+      mbar_expect_tx(bar_q, 3 * Ly::Q_BYTES);
+      tma_load_2d(smem + Ly::Q_OFF, &tmQ, bar_q, head * DH, (int)row_base);
+      tma_load_2d(smem + Ly::KS_OFF, &tmQ, bar_q, D.d + head * DH, (int)row_base);
+      tma_load_2d(smem + Ly::VS_OFF, &tmQ, bar_q, 2 * D.d + head * DH, (int)row_base);
+    } else if (n_chunks > 0) {
+      mbar_expect_tx(bar_q, Ly::Q_BYTES);
+      tma_load_2d(smem + Ly::Q_OFF, &tmQ, bar_q, head * DH, (int)row_base);
+    }
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -228,19 +246,11 @@ __global__ void __launch_bounds__(THREADS, 2)
     // page ids of this (user, block, layer): one warp-wide load into smem (up
     // to 64 pages), so the producer never waits on a global load per chunk
     int* spg = reinterpret_cast<int*>(smem + Ly::BAR_OFF + 256);
-    for (int j = lane; j < n_chunks && j < 64; j += 32) spg[j] = pages[j];
+    if (lane < n_chunks) spg[lane] = pg0;
+    if (lane + 32 < n_chunks) spg[lane + 32] = pg1;
     __syncwarp();
-    if (lane == 0 && (n_chunks > 0 || MODE == MODE_SUMI)) {
-      // ---------------- TMA producer ----------------
-      if (MODE == MODE_SUMI) {  // q, k_self, v_self of the tile's candidates
-        mbar_expect_tx(bar_q, 3 * Ly::Q_BYTES);
-        tma_load_2d(smem + Ly::Q_OFF, &tmQ, bar_q, head * DH, (int)row_base);
-        tma_load_2d(smem + Ly::KS_OFF, &tmQ, bar_q, D.d + head * DH, (int)row_base);
-        tma_load_2d(smem + Ly::VS_OFF, &tmQ, bar_q, 2 * D.d + head * DH, (int)row_base);
-      } else {
-        mbar_expect_tx(bar_q, Ly::Q_BYTES);
-        tma_load_2d(smem + Ly::Q_OFF, &tmQ, bar_q, head * DH, (int)row_base);
-      }
+    if (lane == 0 && n_chunks > 0) {
+      // ---------------- TMA producer (K/V pages; q tiles were issued at init) ----------------
       for (int j = 0; j < n_chunks; ++j) {
         const int st = j % STAGES;
         const int page = (j < 64) ? spg[j] : pages[j];
