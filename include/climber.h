@@ -214,6 +214,42 @@ climber_status climber_rank_host(climber_ctx_t ctx, int32_t B, const int64_t* ev
                                  const int64_t* cand_offsets, const int32_t* items, float* scores,
                                  climber_stream_t stream);
 
+/* ---- Block-parallel serving (PAPER.md L155
+ * "block-parallel KV cache", L203: the N_b blocks are independent until the
+ * fusion step).  G processes each own a block range [k0, k1) (G divides N_b):
+ * each encodes and scores only its blocks, the block outputs E(S_k) (the
+ * candidate rows after the last layer, G13) are exchanged with one
+ * all-gather, and one process fuses (BGF + head).  Every block runs the same
+ * kernels as the single-GPU path, and the fusion input is rebuilt in the
+ * same summation order, so the scores are bit-identical to climber_score_items.
+ * These calls need the bf16 grouped tcgen05 path (d_h in {32, 64}, n_k %
+ * 128 == 0), else CLIMBER_E_UNSUPPORTED. */
+
+/* climber_encode_users restricted to blocks [k0, k1): extraction, embedding
+ * and the layer stacks of those blocks only; the handle holds their K/V and
+ * can only be scored on a sub-range (else CLIMBER_E_INVALID_ARG). */
+climber_status climber_encode_users_blocks(climber_ctx_t ctx, int32_t B, const int64_t* ev_offsets,
+                                           const climber_events* events, const int32_t* scenario_r,
+                                           int32_t k0, int32_t k1, climber_stream_t stream,
+                                           climber_kv_t* out);
+
+/* The candidate stacks of blocks [k0, k1) (layouts as climber_score_items_batched):
+ * E is a DEVICE float [P][k1 - k0][d] (P = cand_offsets[B] - cand_offsets[0]),
+ * E[p][k - k0] = block k's output row of pair p. */
+climber_status climber_score_blocks(climber_ctx_t ctx, int32_t B, const climber_kv_t* kvs,
+                                    const int64_t* cand_offsets, const int32_t* items, int32_t k0, int32_t k1,
+                                    float* E, climber_stream_t stream);
+
+/* BGF (Eq. 4) + squeeze-and-excitation gate + head from gathered block outputs.
+ * E: DEVICE float [n_slices][P][N_b / n_slices][d] (slice g = blocks
+ * [g N_b / n_slices, (g + 1) N_b / n_slices), i.e. the rank-major result of an
+ * all-gather of climber_score_blocks outputs); scenario_r: HOST int32[B] (the
+ * request scenarios, G4); cand_offsets: HOST int64[B + 1]; scores: DEVICE
+ * float[P].  No handle is needed. */
+climber_status climber_fuse_scores(climber_ctx_t ctx, int32_t B, const int64_t* cand_offsets,
+                                   const int32_t* scenario_r, int32_t n_slices, const float* E, float* scores,
+                                   climber_stream_t stream);
+
 /* Return a handle's pages to the pool.  The caller must ensure no enqueued
  * work still reads it.  Double release -> CLIMBER_E_STALE. */
 climber_status climber_kv_release(climber_ctx_t ctx, climber_kv_t kv);

@@ -89,6 +89,9 @@ def lib() -> C.CDLL:
             "climber_kv_export": (I32, [VP, VP, VP, VP]),
             "climber_kv_import": (I32, [VP, VP, I32, VP, P]),
             "climber_profile_read": (I32, [VP, P]),
+            "climber_encode_users_blocks": (I32, [VP, I32, P, P, P, I32, I32, VP, P]),
+            "climber_score_blocks": (I32, [VP, I32, P, P, VP, I32, I32, VP, VP]),
+            "climber_fuse_scores": (I32, [VP, I32, P, P, I32, VP, VP, VP]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -103,7 +106,8 @@ EXPORTED_SYMBOLS = ("climber_arena_bytes", "climber_create", "climber_destroy", 
                     "climber_rank_host", "climber_kv_release", "climber_kv_broadcast", "climber_stream_status",
                     "climber_last_error", "climber_debug_extract", "climber_debug_mask", "climber_debug_kv",
                     "climber_launch_count", "climber_debug_gemm", "climber_profile", "climber_profile_read",
-                    "climber_kv_slab_bytes", "climber_kv_export", "climber_kv_import")
+                    "climber_kv_slab_bytes", "climber_kv_export", "climber_kv_import",
+                    "climber_encode_users_blocks", "climber_score_blocks", "climber_fuse_scores")
 
 KERNEL_CLASSES = ("extract", "embed", "rmsnorm", "gemm_qkv", "gemm_o", "gemm_ffn_up", "gemm_ffn_down", "gemm_se",
                   "attn_hist", "attn_sumi", "attn_fusion", "head", "other")
@@ -281,6 +285,42 @@ class Climber:
             scores = self.torch.empty(items.numel(), dtype=self.torch.float32, device=items.device)
         _check(lib().climber_score_items(self.h, C.c_void_p(handle), C.c_void_p(items.data_ptr()), int(items.numel()),
                                          C.c_void_p(scores.data_ptr()), self._stream(stream)))
+        return scores
+
+    # -- block-parallel serving (NEXT-2): blocks [k0, k1) per process --------
+    def encode_users_blocks(self, ev_offsets, item, action, scenario, ts, r, k0: int, k1: int,
+                            stream=None) -> List[int]:
+        ev_offsets = np.ascontiguousarray(ev_offsets, np.int64)
+        r = np.ascontiguousarray(r, np.int32)
+        B = len(r)
+        ev = _Events(item.data_ptr(), action.data_ptr(), scenario.data_ptr(), ts.data_ptr())
+        out = (C.c_void_p * B)()
+        _check(lib().climber_encode_users_blocks(self.h, B, _ptr(ev_offsets), C.byref(ev), _ptr(r), int(k0), int(k1),
+                                                 self._stream(stream), out))
+        return [out[i] for i in range(B)]
+
+    def score_blocks(self, handles, cand_offsets, items, k0: int, k1: int, E=None, stream=None):
+        """Block outputs E [P][k1 - k0][d] (fp32 CUDA tensor) of blocks [k0, k1)."""
+        cand_offsets = np.ascontiguousarray(cand_offsets, np.int64)
+        B = len(handles)
+        P = int(cand_offsets[-1] - cand_offsets[0])
+        if E is None:
+            E = self.torch.empty((P, k1 - k0, self.cfg.d), dtype=self.torch.float32, device=items.device)
+        hs = (C.c_void_p * B)(*handles)
+        _check(lib().climber_score_blocks(self.h, B, hs, _ptr(cand_offsets), C.c_void_p(items.data_ptr()), int(k0),
+                                          int(k1), C.c_void_p(E.data_ptr()), self._stream(stream)))
+        return E
+
+    def fuse_scores(self, cand_offsets, r, E, n_slices: int = 1, scores=None, stream=None):
+        """BGF + head from E [n_slices][P][N_b / n_slices][d] (fp32 CUDA tensor)."""
+        cand_offsets = np.ascontiguousarray(cand_offsets, np.int64)
+        r = np.ascontiguousarray(r, np.int32)
+        P = int(cand_offsets[-1] - cand_offsets[0])
+        if scores is None:
+            scores = self.torch.empty(P, dtype=self.torch.float32, device=E.device)
+        _check(lib().climber_fuse_scores(self.h, len(r), _ptr(cand_offsets), _ptr(r), int(n_slices),
+                                         C.c_void_p(E.data_ptr()), C.c_void_p(scores.data_ptr()),
+                                         self._stream(stream)))
         return scores
 
     def release(self, handles):

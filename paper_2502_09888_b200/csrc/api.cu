@@ -53,6 +53,7 @@ struct SlotState {
   uint32_t gen = 1;
   bool live = false;
   int r = 0;
+  int kb0 = 0, kb1 = 0;  // blocks whose K/V this handle holds (all, unless encoded block-parallel)
   std::vector<int> pages;
 };
 
@@ -912,8 +913,12 @@ static bool grouped_ok(const climber_ctx_s* c) {
   return c->fused && c->attn_mode == 2 && attn_tc_supported(c->D.dh, c->D.nk, false) && !(g && atoi(g) == 0);
 }
 
+// blocks [k0, k0 + nbk) only (block-parallel serving, NEXT-2); the layouts
+// keep absolute block indices, so a partial encode writes the same bytes as
+// the corresponding part of a full one
 static void encode_wave_grouped(climber_ctx_s* c, const EventsDev& ev, int u0, int U, long long n_events,
-                                cudaStream_t s) {
+                                cudaStream_t s, int k0 = 0, int nbk = -1) {
+  if (nbk < 0) nbk = c->D.Nb;
   const Dims& D = c->D;
   const long long rows = (long long)U * D.nk;  // per block
   const long long d = D.d, F = D.F, pld = c->pld, Nb = D.Nb, Lk = D.L;
@@ -933,8 +938,13 @@ static void encode_wave_grouped(climber_ctx_s* c, const EventsDev& ev, int u0, i
   bf16* O = (bf16*)c->O;     // [Nb][rows][d]
   bf16* Fh = (bf16*)c->Fh;   // [Nb][rows][F]
   float* X = c->X;           // [Nb][rows][d]
+  // the grouped launches below see blocks k0 .. k0 + nbk - 1 as batch 0 .. nbk - 1
+  bf16 *gXb = Xb + k0 * rows * d, *gQb = Qb + k0 * rows * d, *gO = O + k0 * rows * d, *gFh = Fh + k0 * rows * F;
+  float* gX = X + k0 * rows * d;
+  float* gpart = c->part + k0 * rows * pld;
+  const size_t wk = (size_t)k0 * Lk;  // first weight slice of block k0
   const double causal_pairs = D.causal ? (double)D.nk * (D.nk + 1) / 2 : (double)D.nk * D.nk;
-  for (int k = 0; k < D.Nb; ++k) {
+  for (int k = k0; k < k0 + nbk; ++k) {
     Prof p(c, CLIMBER_K_EMBED, s, 0, (double)rows * d * (3 * 2 + 4 + 2));
     launch_embed_hist<bf16>(ev, c->d_ev_off + u0, wslot, U, c->idx_all, c->vlen_all, c->bad_all,
                             (const bf16*)c->e_item, (const bf16*)c->e_act, (const bf16*)c->e_scn, X + k * rows * d,
@@ -942,83 +952,104 @@ static void encode_wave_grouped(climber_ctx_s* c, const EventsDev& ev, int u0, i
   }
   for (int l = 0; l < D.L; ++l) {
     Epilogue e{};
-    e.kind = EPI_QKV_PAGES; e.out = Qb; e.ldo = d; e.out_bs = rows * d; e.pool = c->pool; e.ptab = c->ptab;
+    e.kind = EPI_QKV_PAGES; e.out = gQb; e.ldo = d; e.out_bs = rows * d; e.pool = c->pool; e.ptab = c->ptab;
     e.wave_slot = wslot; e.pool_rows = c->n_pages * 2 * PAGE; e.blk_from_batch = 1;
-    e.blk = 0; e.layer = l; e.d = D.d; e.h = D.h; e.dh = D.dh; e.nk = D.nk; e.Nb = D.Nb; e.L = D.L; e.ppb = D.ppb;
-    e = with_rs(e, c, c->part, pld);
+    e.blk = k0; e.layer = l; e.d = D.d; e.h = D.h; e.dh = D.dh; e.nk = D.nk; e.Nb = D.Nb; e.L = D.L; e.ppb = D.ppb;
+    e = with_rs(e, c, gpart, pld);
     e.rs_bs = rows * pld;
-    const bf16* Wqkv = (const bf16*)c->w_qkv + (size_t)l * 3 * d * d;  // block k at + k * L * 3d * d
+    const bf16* Wqkv = (const bf16*)c->w_qkv + (wk + l) * 3 * d * d;  // block k at + k * L * 3d * d
     if (l < D.L - 1) {
       e.col_off = 0;
-      gemm_g(c, CLIMBER_K_GEMM_QKV, Xb, d, rows * d, Wqkv, d, Lk * 3 * d * d, rows, 3 * D.d, D.d, D.Nb, e, s);
+      gemm_g(c, CLIMBER_K_GEMM_QKV, gXb, d, rows * d, Wqkv, d, Lk * 3 * d * d, rows, 3 * D.d, D.d, nbk, e, s);
       {
-        Prof p(c, CLIMBER_K_ATTN_HIST, s, 4.0 * U * causal_pairs * d * Nb, (double)rows * d * 2 * 4 * Nb);
-        launch_attn_hist_tc(Qb, wslot, wr, U, (const bf16*)c->pool, c->n_pages * 2 * PAGE, c->ptab, c->vlen_all,
-                            c->tau, O, 0, l, D, s, D.Nb);
+        Prof p(c, CLIMBER_K_ATTN_HIST, s, 4.0 * U * causal_pairs * d * nbk, (double)rows * d * 2 * 4 * nbk);
+        launch_attn_hist_tc(gQb, wslot, wr, U, (const bf16*)c->pool, c->n_pages * 2 * PAGE, c->ptab, c->vlen_all,
+                            c->tau, gO, k0, l, D, s, nbk);
       }
-      Epilogue eo = epi_resid_norm(X, d, Xb, c->part, pld);
+      Epilogue eo = epi_resid_norm(gX, d, gXb, gpart, pld);
       eo.out_bs = rows * d; eo.out_b16_bs = rows * d; eo.part_bs = rows * pld;
-      gemm_g(c, CLIMBER_K_GEMM_O, O, d, rows * d, (const bf16*)c->w_o + (size_t)l * d * d, d, Lk * d * d, rows,
-             D.d, D.d, D.Nb, eo, s);
-      Epilogue eu = with_rs(epi_store(Fh, F, ACT_SILU), c, c->part, pld);
+      gemm_g(c, CLIMBER_K_GEMM_O, gO, d, rows * d, (const bf16*)c->w_o + (wk + l) * d * d, d, Lk * d * d, rows,
+             D.d, D.d, nbk, eo, s);
+      Epilogue eu = with_rs(epi_store(gFh, F, ACT_SILU), c, gpart, pld);
       eu.out_bs = rows * F; eu.rs_bs = rows * pld;
-      gemm_g(c, CLIMBER_K_GEMM_FFN_UP, Xb, d, rows * d, (const bf16*)c->w1 + (size_t)l * F * d, d, Lk * F * d, rows,
-             D.F, D.d, D.Nb, eu, s);
-      gemm_g(c, CLIMBER_K_GEMM_FFN_DOWN, Fh, F, rows * F, (const bf16*)c->w2 + (size_t)l * d * F, F, Lk * d * F,
-             rows, D.d, D.F, D.Nb, eo, s);
+      gemm_g(c, CLIMBER_K_GEMM_FFN_UP, gXb, d, rows * d, (const bf16*)c->w1 + (wk + l) * F * d, d, Lk * F * d, rows,
+             D.F, D.d, nbk, eu, s);
+      gemm_g(c, CLIMBER_K_GEMM_FFN_DOWN, gFh, F, rows * F, (const bf16*)c->w2 + (wk + l) * d * F, F, Lk * d * F,
+             rows, D.d, D.F, nbk, eo, s);
     } else {
       e.col_off = D.d;  // last layer: only K/V of the history are ever read
-      gemm_g(c, CLIMBER_K_GEMM_QKV, Xb, d, rows * d, Wqkv + d * d, d, Lk * 3 * d * d, rows, 2 * D.d, D.d, D.Nb, e,
+      gemm_g(c, CLIMBER_K_GEMM_QKV, gXb, d, rows * d, Wqkv + d * d, d, Lk * 3 * d * d, rows, 2 * D.d, D.d, nbk, e,
              s);
     }
   }
 }
 
-static void score_wave_grouped(climber_ctx_s* c, const int32_t* items, const int64_t* wcand, int u0, int U,
-                               long long P, int Mmax_wave, float* scores, cudaStream_t s) {
+// blocks [k0, k0 + nbk) of the candidate stacks (all of them for a full
+// score; a slice for block-parallel serving, NEXT-2): candidate rows
+// C [p][N_b][d] hold every block's residual, the launches see the slice
+static void score_blocks_grouped(climber_ctx_s* c, const int32_t* items, const int64_t* wcand, int u0, int U,
+                                 long long P, int Mmax_wave, cudaStream_t s, int k0, int nbk) {
   const Dims& D = c->D;
   const long long d = D.d, F = D.F, Nb = D.Nb, ldC = Nb * d, pld = c->pld, Lk = D.L;
   const int* wslot = c->d_slots + u0;
   const int* wr = c->d_r + u0;
   bf16* Cb = (bf16*)c->Xb;   // [p][k][d] (interleaved blocks)
-  bf16* QKV = (bf16*)c->QKV; // [k][p][3d]
-  bf16* O = (bf16*)c->O;     // [k][p][d]
-  bf16* Fh = (bf16*)c->Fh;   // [k][p][F]
+  bf16* QKV = (bf16*)c->QKV; // [k - k0][p][3d]
+  bf16* O = (bf16*)c->O;     // [k - k0][p][d]
+  bf16* Fh = (bf16*)c->Fh;   // [k - k0][p][F]
   float* C = c->X;           // [p][k][d]
   {
     Prof p(c, CLIMBER_K_EMBED, s, 0, (double)P * d * (2 * 2 + 6 * Nb));
     launch_embed_cand<bf16>(items, wcand, wr, U, P, (const bf16*)c->e_item, (const bf16*)c->e_scn, C, Cb, c->part,
                             c->pld, c->err, D, s);
   }
+  bf16* gCb = Cb + k0 * d;
+  float* gC = C + k0 * d;
+  float* gpart = c->part + k0 * pld;
+  const size_t wk = (size_t)k0 * Lk;
   // candidate rows of block k: row p at (p * Nb + k) -> batch stride d (elements), partials stride pld
   for (int l = 0; l < D.L; ++l) {
-    Epilogue eq = with_rs(epi_store(QKV, 3 * d), c, c->part, Nb * pld);
+    Epilogue eq = with_rs(epi_store(QKV, 3 * d), c, gpart, Nb * pld);
     eq.out_bs = P * 3 * d; eq.rs_bs = pld;
-    gemm_stage(c, 1, CLIMBER_K_GEMM_QKV, Cb, ldC, d, (const bf16*)c->w_qkv + (size_t)l * 3 * d * d, d, Lk * 3 * d * d, P,
-           3 * D.d, D.d, D.Nb, eq, s);
+    gemm_stage(c, 1, CLIMBER_K_GEMM_QKV, gCb, ldC, d, (const bf16*)c->w_qkv + (wk + l) * 3 * d * d, d, Lk * 3 * d * d,
+               P, 3 * D.d, D.d, nbk, eq, s);
     {
-      Prof p(c, CLIMBER_K_ATTN_SUMI, s, 4.0 * P * (D.nk + 1) * d * Nb,
-             ((double)P * d * 2 * 4 + (double)U * D.nk * d * 4) * Nb);
+      Prof p(c, CLIMBER_K_ATTN_SUMI, s, 4.0 * P * (D.nk + 1) * d * nbk,
+             ((double)P * d * 2 * 4 + (double)U * D.nk * d * 4) * nbk);
       if (grouped_mask() & 2) {
         launch_attn_sumi_tc(QKV, P, wcand, wslot, wr, U, Mmax_wave, (const bf16*)c->pool, c->n_pages * 2 * PAGE,
-                            c->ptab, c->vlen_all, c->tau, O, 0, l, D, s, D.Nb);
+                            c->ptab, c->vlen_all, c->tau, O, k0, l, D, s, nbk);
       } else {
-        for (int k = 0; k < D.Nb; ++k)
+        for (int k = 0; k < nbk; ++k)
           launch_attn_sumi_tc(QKV + k * P * 3 * d, P, wcand, wslot, wr, U, Mmax_wave, (const bf16*)c->pool,
-                              c->n_pages * 2 * PAGE, c->ptab, c->vlen_all, c->tau, O + k * P * d, k, l, D, s, 1);
+                              c->n_pages * 2 * PAGE, c->ptab, c->vlen_all, c->tau, O + k * P * d, k0 + k, l, D, s, 1);
       }
     }
-    Epilogue eo = epi_resid_norm(C, ldC, Cb, c->part, Nb * pld);
+    Epilogue eo = epi_resid_norm(gC, ldC, gCb, gpart, Nb * pld);
     eo.out_bs = d; eo.out_b16_bs = d; eo.part_bs = pld;
-    gemm_stage(c, 4, CLIMBER_K_GEMM_O, O, d, P * d, (const bf16*)c->w_o + (size_t)l * d * d, d, Lk * d * d, P, D.d, D.d,
-           D.Nb, eo, s);
-    Epilogue eu = with_rs(epi_store(Fh, F, ACT_SILU), c, c->part, Nb * pld);
+    gemm_stage(c, 4, CLIMBER_K_GEMM_O, O, d, P * d, (const bf16*)c->w_o + (wk + l) * d * d, d, Lk * d * d, P, D.d,
+               D.d, nbk, eo, s);
+    Epilogue eu = with_rs(epi_store(Fh, F, ACT_SILU), c, gpart, Nb * pld);
     eu.out_bs = P * F; eu.rs_bs = pld;
-    gemm_stage(c, 8, CLIMBER_K_GEMM_FFN_UP, Cb, ldC, d, (const bf16*)c->w1 + (size_t)l * F * d, d, Lk * F * d, P, D.F, D.d,
-           D.Nb, eu, s);
-    gemm_stage(c, 16, CLIMBER_K_GEMM_FFN_DOWN, Fh, F, P * F, (const bf16*)c->w2 + (size_t)l * d * F, F, Lk * d * F, P, D.d,
-           D.F, D.Nb, eo, s);
+    gemm_stage(c, 8, CLIMBER_K_GEMM_FFN_UP, gCb, ldC, d, (const bf16*)c->w1 + (wk + l) * F * d, d, Lk * F * d, P,
+               D.F, D.d, nbk, eu, s);
+    gemm_stage(c, 16, CLIMBER_K_GEMM_FFN_DOWN, Fh, F, P * F, (const bf16*)c->w2 + (wk + l) * d * F, F, Lk * d * F, P,
+               D.d, D.F, nbk, eo, s);
   }
+}
+
+// a5/a6 on the candidate rows C [p][N_b][d] (fp32 residual, bf16 copy and
+// per-128-column partial sums of squares already in place)
+static void fuse_grouped(climber_ctx_s* c, const int64_t* wcand, int u0, int U, long long P, float* scores,
+                         cudaStream_t s) {
+  const Dims& D = c->D;
+  const long long d = D.d, F = D.F, Nb = D.Nb, pld = c->pld;
+  const int* wr = c->d_r + u0;
+  bf16* Cb = (bf16*)c->Xb;
+  bf16* QKV = (bf16*)c->QKV;
+  bf16* O = (bf16*)c->O;
+  bf16* Fh = (bf16*)c->Fh;
+  float* C = c->X;
   // ---- BGF (Eq. 4) + SE gate + head: identical to the per-block fused path
   const long long R = P * Nb;
   gemm<bf16>(c, CLIMBER_K_GEMM_QKV, Cb, d, (const bf16*)c->fw_qkv, d, R, 3 * D.d, D.d,
@@ -1044,6 +1075,12 @@ static void score_wave_grouped(climber_ctx_s* c, const int32_t* items, const int
     Prof p(c, CLIMBER_K_HEAD, s, 3.0 * P * D.Dse, (double)P * D.Dse * 8 + P * 4);
     launch_head(C, gate, c->w_head, c->b_head, scores, P, D.Dse, s);
   }
+}
+
+static void score_wave_grouped(climber_ctx_s* c, const int32_t* items, const int64_t* wcand, int u0, int U,
+                               long long P, int Mmax_wave, float* scores, cudaStream_t s) {
+  score_blocks_grouped(c, items, wcand, u0, U, P, Mmax_wave, s, 0, c->D.Nb);
+  fuse_grouped(c, wcand, u0, U, P, scores, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -1098,9 +1135,9 @@ static climber_status check_launch(climber_ctx_s* c, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 // encode
 // ---------------------------------------------------------------------------
-extern "C" climber_status climber_encode_users(climber_ctx_t c, int32_t B, const int64_t* ev_offsets,
-                                               const climber_events* events, const int32_t* scenario_r,
-                                               climber_stream_t stream, climber_kv_t* out) {
+static climber_status encode_users_range(climber_ctx_t c, int32_t B, const int64_t* ev_offsets,
+                                         const climber_events* events, const int32_t* scenario_r,
+                                         climber_stream_t stream, climber_kv_t* out, int k0, int k1) {
   try {
     if (!c || !ev_offsets || !events || !scenario_r || !out) return fail(CLIMBER_E_INVALID_ARG, "null argument");
     if (B < 1 || B > c->cfg.max_batch_users) return fail(CLIMBER_E_INVALID_ARG, "B=%d outside [1, max_batch_users]", B);
@@ -1125,6 +1162,8 @@ extern "C" climber_status climber_encode_users(climber_ctx_t c, int32_t B, const
         SlotState& st = c->slots[slot];
         st.live = true;
         st.r = scenario_r[b];
+        st.kb0 = k0;
+        st.kb1 = k1;
         st.pages.resize(c->per_slot);
         for (int i = 0; i < c->per_slot; ++i) {
           st.pages[i] = c->free_pages.back();
@@ -1146,7 +1185,7 @@ extern "C" climber_status climber_encode_users(climber_ctx_t c, int32_t B, const
       int U = B - u0 < c->cfg.max_wave_users ? B - u0 : c->cfg.max_wave_users;
       long long nev = ev_offsets[u0 + U] - ev_offsets[u0];
       if (c->fused && grouped_ok(c) && attn_tc_supported(c->D.dh, c->D.nk, true))
-        encode_wave_grouped(c, ev, u0, U, nev, s);
+        encode_wave_grouped(c, ev, u0, U, nev, s, k0, k1 - k0);
       else if (c->fused) encode_wave_fused(c, ev, u0, U, nev, s);
       else if (c->cfg.dtype == CLIMBER_BF16) encode_wave<bf16>(c, ev, u0, U, nev, s);
       else encode_wave<float>(c, ev, u0, U, nev, s);
@@ -1159,6 +1198,26 @@ extern "C" climber_status climber_encode_users(climber_ctx_t c, int32_t B, const
   }
 }
 
+extern "C" climber_status climber_encode_users(climber_ctx_t c, int32_t B, const int64_t* ev_offsets,
+                                               const climber_events* events, const int32_t* scenario_r,
+                                               climber_stream_t stream, climber_kv_t* out) {
+  return encode_users_range(c, B, ev_offsets, events, scenario_r, stream, out, 0, c ? c->D.Nb : 0);
+}
+
+static bool block_parallel_ok(const climber_ctx_s* c) {
+  return c->fused && grouped_ok(c) && attn_tc_supported(c->D.dh, c->D.nk, true);
+}
+
+extern "C" climber_status climber_encode_users_blocks(climber_ctx_t c, int32_t B, const int64_t* ev_offsets,
+                                                      const climber_events* events, const int32_t* scenario_r,
+                                                      int32_t k0, int32_t k1, climber_stream_t stream,
+                                                      climber_kv_t* out) {
+  if (!c) return fail(CLIMBER_E_INVALID_ARG, "null ctx");
+  if (k0 < 0 || k1 > c->D.Nb || k0 >= k1) return fail(CLIMBER_E_INVALID_ARG, "block range [%d, %d) invalid", k0, k1);
+  if (!block_parallel_ok(c)) return fail(CLIMBER_E_UNSUPPORTED, "block ranges need the bf16 grouped tcgen05 path");
+  return encode_users_range(c, B, ev_offsets, events, scenario_r, stream, out, k0, k1);
+}
+
 extern "C" climber_status climber_encode_user(climber_ctx_t c, const climber_events* events, int64_t n_s,
                                               int32_t scenario_r, climber_stream_t stream, climber_kv_t* out) {
   if (n_s < 0) return fail(CLIMBER_E_INVALID_ARG, "n_s < 0");
@@ -1169,11 +1228,16 @@ extern "C" climber_status climber_encode_user(climber_ctx_t c, const climber_eve
 // ---------------------------------------------------------------------------
 // score
 // ---------------------------------------------------------------------------
-extern "C" climber_status climber_score_items_batched(climber_ctx_t c, int32_t B, const climber_kv_t* kvs,
-                                                      const int64_t* cand_offsets, const int32_t* items,
-                                                      float* scores, climber_stream_t stream) {
+// mode 0: full score (blocks + BGF + head) -> scores; mode 1: blocks [k0, k1)
+// only -> E [P][k1 - k0][d]; mode 2: BGF + head from E ([n_slices][P][N_b /
+// n_slices][d]) with the per-user scenarios given (no handles) -> scores
+static climber_status score_common(climber_ctx_t c, int32_t B, const climber_kv_t* kvs, const int64_t* cand_offsets,
+                                   const int32_t* items, const int32_t* scen, int mode, int k0, int k1,
+                                   int n_slices, float* E, float* scores, climber_stream_t stream) {
   try {
-    if (!c || !kvs || !cand_offsets || !items || !scores) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+    if (!c || !cand_offsets || (mode != 2 && (!kvs || !items)) || (mode == 2 && (!scen || !E)) ||
+        (mode != 1 && !scores) || (mode == 1 && !E))
+      return fail(CLIMBER_E_INVALID_ARG, "null argument");
     if (B < 1 || B > c->cfg.max_batch_users) return fail(CLIMBER_E_INVALID_ARG, "B=%d outside [1, max_batch_users]", B);
     for (int b = 0; b < B; ++b) {
       long long m = cand_offsets[b + 1] - cand_offsets[b];
@@ -1186,10 +1250,15 @@ extern "C" climber_status climber_score_items_batched(climber_ctx_t c, int32_t B
     std::vector<Wave> waves;
     {
       std::lock_guard<std::mutex> g(c->mu);
-      std::vector<int> slots(B);
-      for (int b = 0; b < B; ++b) {
-        climber_status rs = resolve(c, kvs[b], &slots[b]);
-        if (rs != CLIMBER_OK) return rs;
+      std::vector<int> slots(B, 0);
+      if (mode != 2) {
+        for (int b = 0; b < B; ++b) {
+          climber_status rs = resolve(c, kvs[b], &slots[b]);
+          if (rs != CLIMBER_OK) return rs;
+          const SlotState& ss = c->slots[slots[b]];
+          if (k0 < ss.kb0 || k1 > ss.kb1)
+            return fail(CLIMBER_E_INVALID_ARG, "handle %d holds blocks [%d, %d), not [%d, %d)", b, ss.kb0, ss.kb1, k0, k1);
+        }
       }
       CU(cudaEventSynchronize(c->stage_evt));
       Stage h = stage_layout(c, c->h_stage);
@@ -1210,17 +1279,34 @@ extern "C" climber_status climber_score_items_batched(climber_ctx_t c, int32_t B
       }
       for (int b = 0; b < B; ++b) {
         h.slots[b] = slots[b];
-        h.r[b] = c->slots[slots[b]].r;
+        h.r[b] = mode == 2 ? scen[b] : c->slots[slots[b]].r;
+        if (h.r[b] < 0 || h.r[b] >= c->D.R) return fail(CLIMBER_E_OUT_OF_RANGE, "scenario_r[%d] out of range", b);
       }
       h.ev_off[0] = 0;
       climber_status rs = stage_upload(c, B, false, s);
       if (rs != CLIMBER_OK) return rs;
     }
+    const long long d = c->D.d, Nb = c->D.Nb;
     for (const Wave& w : waves) {
-      const int32_t* it = items + cand_offsets[w.u0];
-      float* sc = scores + cand_offsets[w.u0];
+      const int32_t* it = items ? items + cand_offsets[w.u0] : nullptr;
+      float* sc = scores ? scores + cand_offsets[w.u0] : nullptr;
       const int64_t* wc = c->d_cand_off + w.coff;
-      if (c->fused && grouped_ok(c)) score_wave_grouped(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
+      const long long q0 = cand_offsets[w.u0] - cand_offsets[0];  // first pair of the wave
+      if (mode == 1) {  // block stacks of [k0, k1), then E = C[:, k0:k1, :]
+        score_blocks_grouped(c, it, wc, w.u0, w.U, w.P, w.Mmax, s, k0, k1 - k0);
+        CU(cudaMemcpy2DAsync(E + q0 * (k1 - k0) * d, (k1 - k0) * d * 4, c->X + k0 * d, Nb * d * 4, (k1 - k0) * d * 4,
+                             w.P, cudaMemcpyDeviceToDevice, s));
+      } else if (mode == 2) {  // C = E (slices rank-major), recompute the bf16 copy + norm partials, fuse
+        const long long ns = Nb / n_slices, Ptot = cand_offsets[B] - cand_offsets[0];
+        for (int g = 0; g < n_slices; ++g)
+          CU(cudaMemcpy2DAsync(c->X + g * ns * d, Nb * d * 4, E + ((long long)g * Ptot + q0) * ns * d, ns * d * 4,
+                               ns * d * 4, w.P, cudaMemcpyDeviceToDevice, s));
+        {
+          Prof p(c, CLIMBER_K_OTHER, s, 0, (double)w.P * Nb * d * 6);
+          launch_row_prep(c->X, (bf16*)c->Xb, c->part, w.P * Nb, c->D.d, c->pld, s);
+        }
+        fuse_grouped(c, wc, w.u0, w.U, w.P, sc, s);
+      } else if (c->fused && grouped_ok(c)) score_wave_grouped(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
       else if (c->fused) score_wave_fused(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
       else if (c->cfg.dtype == CLIMBER_BF16) score_wave<bf16>(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
       else score_wave<float>(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
@@ -1231,6 +1317,31 @@ extern "C" climber_status climber_score_items_batched(climber_ctx_t c, int32_t B
   } catch (...) {
     return fail(CLIMBER_E_CUDA, "score: exception");
   }
+}
+
+extern "C" climber_status climber_score_items_batched(climber_ctx_t c, int32_t B, const climber_kv_t* kvs,
+                                                      const int64_t* cand_offsets, const int32_t* items,
+                                                      float* scores, climber_stream_t stream) {
+  return score_common(c, B, kvs, cand_offsets, items, nullptr, 0, 0, c ? c->D.Nb : 0, 1, nullptr, scores, stream);
+}
+
+extern "C" climber_status climber_score_blocks(climber_ctx_t c, int32_t B, const climber_kv_t* kvs,
+                                               const int64_t* cand_offsets, const int32_t* items, int32_t k0,
+                                               int32_t k1, float* E, climber_stream_t stream) {
+  if (!c) return fail(CLIMBER_E_INVALID_ARG, "null ctx");
+  if (k0 < 0 || k1 > c->D.Nb || k0 >= k1) return fail(CLIMBER_E_INVALID_ARG, "block range [%d, %d) invalid", k0, k1);
+  if (!block_parallel_ok(c)) return fail(CLIMBER_E_UNSUPPORTED, "block ranges need the bf16 grouped tcgen05 path");
+  return score_common(c, B, kvs, cand_offsets, items, nullptr, 1, k0, k1, 1, E, nullptr, stream);
+}
+
+extern "C" climber_status climber_fuse_scores(climber_ctx_t c, int32_t B, const int64_t* cand_offsets,
+                                              const int32_t* scenario_r, int32_t n_slices, const float* E,
+                                              float* scores, climber_stream_t stream) {
+  if (!c) return fail(CLIMBER_E_INVALID_ARG, "null ctx");
+  if (n_slices < 1 || c->D.Nb % n_slices) return fail(CLIMBER_E_INVALID_ARG, "n_slices must divide N_b");
+  if (!block_parallel_ok(c)) return fail(CLIMBER_E_UNSUPPORTED, "block ranges need the bf16 grouped tcgen05 path");
+  return score_common(c, B, nullptr, cand_offsets, nullptr, scenario_r, 2, 0, c->D.Nb, n_slices,
+                      const_cast<float*>(E), scores, stream);
 }
 
 extern "C" climber_status climber_score_items(climber_ctx_t c, climber_kv_t kv, const int32_t* items, int32_t M,
@@ -1306,6 +1417,8 @@ extern "C" climber_status climber_kv_import(climber_ctx_t c, const void* slab, i
     SlotState& st = c->slots[slot];
     st.live = true;
     st.r = scenario_r;
+    st.kb0 = 0;
+    st.kb1 = c->D.Nb;
     st.pages.resize(c->per_slot);
     for (int i = 0; i < c->per_slot; ++i) {
       st.pages[i] = c->free_pages.back();
@@ -1366,6 +1479,8 @@ static climber_status rank_one_graph(climber_ctx_s* c, long long E, long long P,
     SlotState& st = c->slots[slot];
     st.live = true;
     st.r = r;
+    st.kb0 = 0;
+    st.kb1 = c->D.Nb;
     st.pages.resize(c->per_slot);
     for (int i = 0; i < c->per_slot; ++i) {
       st.pages[i] = c->free_pages.back();

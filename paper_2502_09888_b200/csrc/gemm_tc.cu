@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
                 const int cc = cg - e.d * (1 + kv);
                 const int u = (int)(row0 / e.nk), tt = (int)(row0 % e.nk);
                 const int slot = e.wave_slot[u];
-                const int blk = e.blk_from_batch ? bt : e.blk;
+                const int blk = e.blk_from_batch ? e.blk + bt : e.blk;
                 const int page = e.ptab[(((long long)slot * e.Nb + blk) * e.L + e.layer) * e.ppb + tt / PAGE];
                 tma_store_3d(&tmP, buf, cc, (int)page_row(page, kv, tt % PAGE), 0);
               }

@@ -89,6 +89,36 @@ __global__ void k_cand_bias(const int* __restrict__ wave_slot, const int* __rest
     out[j] = j < v ? bp[bucket_pos(v - j)] + bt[bucket_time(tq - ht[j])] : 0.f;
 }
 
+// Block-parallel fusion input (NEXT-2): from the gathered fp32 block outputs
+// C [rows][d], the bf16 copy and the per-128-column partial sums of squares
+// that the RESID_NORM GEMM epilogue would have written, in the same order
+// (32-column chunks, each 4 columns as fma(c3, fma(c2, fma(c1, fma(c0 ...)))))
+// so the fused scores are bit-identical to the single-GPU path.
+__global__ void k_row_prep(const float* __restrict__ C, bf16* __restrict__ Cb, float* __restrict__ part,
+                           long long rows, int d, int pld) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // (row, 128-column group)
+  if (t >= rows * pld) return;
+  const long long row = t / pld;
+  const int g = (int)(t % pld);
+  const int w = d < 128 ? d : 128;
+  const float* x = C + row * d + g * w;
+  bf16* xb = Cb + row * d + g * w;
+  float ss = 0.f;
+  for (int c = 0; c < w; c += 4) {
+    const float4 v = *reinterpret_cast<const float4*>(x + c);
+    ss = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, ss))));
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    *reinterpret_cast<__nv_bfloat162*>(xb + c) = a;
+    *reinterpret_cast<__nv_bfloat162*>(xb + c + 2) = b;
+  }
+  part[row * pld + g] = ss;
+}
+
+void launch_row_prep(const float* C, bf16* Cb, float* part, long long rows, int d, int pld, cudaStream_t s) {
+  const long long n = rows * pld;
+  k_row_prep<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(C, Cb, part, rows, d, pld);
+}
+
 void launch_cand_bias(const int* wave_slot, const int* wave_r, int U, const int* vlen_all, const Dims& D,
                       cudaStream_t s) {
   k_cand_bias<<<dim3(U, D.L * D.Nb * D.h), 128, 0, s>>>(wave_slot, wave_r, vlen_all, D);

@@ -1,4 +1,5 @@
-"""Multi-GPU candidate sharding for one request (latency mode).
+"""Multi-GPU serving of one request (latency mode): candidate sharding
+ and block-parallel serving.
 
 The paper's serving statement has one exchange step when a
 request is spread over G GPUs: the user's multi-layer K/V cache must reach the
@@ -58,6 +59,27 @@ class ClimberBackend:
     def release(self, handle):
         self.cl.release(handle)
 
+    # block-parallel
+    @property
+    def n_blocks(self) -> int:
+        return self.cl.cfg.N_b
+
+    def encode_blocks(self, events, r, k0, k1):
+        import numpy as np
+        item, action, scenario, ts = events
+        n = int(item.numel())
+        return self.cl.encode_users_blocks(np.array([0, n], np.int64), item, action, scenario, ts,
+                                           np.array([r], np.int32), k0, k1)[0]
+
+    def score_blocks(self, handle, items, k0, k1, out=None):
+        import numpy as np
+        return self.cl.score_blocks([handle], np.array([0, int(items.numel())], np.int64), items, k0, k1, E=out)
+
+    def fuse(self, E_all, r, n_slices):
+        import numpy as np
+        M = int(E_all.shape[1])
+        return self.cl.fuse_scores(np.array([0, M], np.int64), np.array([r], np.int32), E_all, n_slices=n_slices)
+
 
 def rank_request_sharded(backend, dist, events, r: int, items, root: int = 0):
     """Score one request's candidates across the process group.
@@ -92,3 +114,49 @@ def rank_request_sharded(backend, dist, events, r: int, items, root: int = 0):
         a, b = shard_bounds(M, G, g)
         out[a:b] = parts[g][:b - a]
     return out
+
+
+# ---------------------------------------------------------------------------
+# block-parallel serving ("block-parallel
+# KV cache", L203: the N_b blocks are independent until the fusion step)
+# ---------------------------------------------------------------------------
+def block_bounds(N_b: int, G: int, rank: int) -> Tuple[int, int]:
+    """Blocks [k0, k1) of `rank` (G must divide N_b)."""
+    if N_b % G:
+        raise ValueError(f"G={G} must divide N_b={N_b}")
+    n = N_b // G
+    return rank * n, (rank + 1) * n
+
+
+def rank_request_block_parallel(backend, dist, events, r: int, items, root: int = 0):
+    """Score one request with its N_b blocks spread over the process group.
+
+    Every rank encodes and scores only its blocks (no K/V moves at all); the
+    block outputs E [M][N_b / G][d] are all-gathered rank-major into one
+    [G][M][N_b / G][d] buffer, which is exactly the layout the fusion call
+    reads; `root` fuses (BGF + head).  events: the user's events on `root`
+    (broadcast here, ~14 B per event); items: the M candidates (every rank).
+    Returns the M scores on `root`, None elsewhere."""
+    torch = backend.torch
+    G, rank = dist.get_world_size(), dist.get_rank()
+    k0, k1 = block_bounds(backend.n_blocks, G, rank)
+    # the request's events reach every rank: one broadcast of n_s, one of the packed arrays
+    n = torch.zeros(1, dtype=torch.int64, device=backend.device)
+    if rank == root:
+        n[0] = int(events[0].numel())
+    dist.broadcast(n, src=root)
+    n_s = int(n.item())
+    packed = torch.empty((4, n_s), dtype=torch.int64, device=backend.device)
+    if rank == root:
+        for i, a in enumerate(events):
+            packed[i] = a.to(torch.int64)
+    dist.broadcast(packed, src=root)
+    ev = (packed[0].to(torch.int32), packed[1].to(torch.uint8), packed[2].to(torch.uint8), packed[3].contiguous())
+    handle = backend.encode_blocks(ev, r, k0, k1)
+    E = backend.score_blocks(handle, items, k0, k1)                   # [M][N_b / G][d]
+    E_all = torch.empty((G,) + tuple(E.shape), dtype=E.dtype, device=E.device)
+    dist.all_gather(list(E_all.unbind(0)), E)
+    backend.release(handle)
+    if rank != root:
+        return None
+    return backend.fuse(E_all, r, G)

@@ -85,3 +85,66 @@ def test_sharded_driver_world1_nccl():
         cl.release(h)
     finally:
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# block-parallel serving (NEXT-2): every block range run in-process, block
+# outputs stacked rank-major, fused: bit-identical to the single-GPU path
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,G,rel_bias", [("medium", 2, 0), ("medium", 4, 1), ("large", 2, 0)])
+def test_block_parallel_bitwise(name, G, rel_bias):
+    import torch
+    from paper_2502_09888_b200 import ClimberError
+    from paper_2502_09888_b200.sharded import block_bounds
+    cfg = synth.preset(name, rel_bias=rel_bias)
+    B = 3
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 8, B=B)
+    cl = make_gpu(cfg, w, B, kv_users=B * (G + 1))
+    item, action, scenario, ts, cand = to_dev(batch)
+    hs = cl.encode_users(batch.ev_offsets, item, action, scenario, ts, batch.r)
+    ref = cl.score_batched(hs, batch.cand_offsets, cand)
+    P = int(batch.cand_offsets[-1])
+    E_all = torch.empty((G, P, cfg.N_b // G, cfg.d), dtype=torch.float32, device=cand.device)
+    parts = []
+    for g in range(G):
+        k0, k1 = block_bounds(cfg.N_b, G, g)
+        hg = cl.encode_users_blocks(batch.ev_offsets, item, action, scenario, ts, batch.r, k0, k1)
+        cl.score_blocks(hg, batch.cand_offsets, cand, k0, k1, E=E_all[g])
+        parts.append(hg)
+    got = cl.fuse_scores(batch.cand_offsets, batch.r, E_all, n_slices=G)
+    cl.stream_status()
+    assert torch.equal(got, ref)
+    # a partial handle cannot be scored outside its blocks
+    with pytest.raises(ClimberError) as ei:
+        cl.score_batched(parts[0], batch.cand_offsets, cand)
+    assert ei.value.name == "E_INVALID_ARG"
+    for hg in parts:
+        cl.release(hg)
+    cl.release(hs)
+
+
+def test_block_parallel_driver_world1_nccl():
+    import torch
+    import torch.distributed as dist
+    from paper_2502_09888_b200.sharded import ClimberBackend, rank_request_block_parallel
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        cfg = synth.preset("medium")
+        w = synth.make_weights(cfg, 0)
+        batch = synth.make_batch(cfg, 6, B=1)
+        cl = make_gpu(cfg, w, 1, kv_users=2)
+        item, action, scenario, ts, cand = to_dev(batch)
+        out = rank_request_block_parallel(ClimberBackend(cl), dist, (item, action, scenario, ts),
+                                          int(batch.r[0]), cand)
+        h = cl.encode_user(item, action, scenario, ts, int(batch.r[0]))
+        ref = cl.score_items(h, cand)
+        assert torch.equal(out, ref)
+        cl.release(h)
+    finally:
+        dist.destroy_process_group()

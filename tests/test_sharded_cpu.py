@@ -102,3 +102,99 @@ def test_two_rank_candidate_sharding_matches_single_process():
     u = synth.make_user(cfg, np.random.default_rng(3), n_s=120, M=7)
     ref = O.sumi_scores(cfg, w, synth.strategies_for(cfg.N_b, cfg.R), u, 0)
     np.testing.assert_allclose(res[0], ref, rtol=0, atol=1e-6)   # fp32 transport of fp64 scores
+
+
+# ---------------------------------------------------------------------------
+# block-parallel serving (NEXT-2): blocks [k0, k1) per rank, E all-gathered
+# ---------------------------------------------------------------------------
+def test_block_bounds():
+    from paper_2502_09888_b200.sharded import block_bounds
+    for N_b in (1, 2, 4, 8):
+        for G in (1, 2, 4, 8):
+            if N_b % G:
+                with pytest.raises(ValueError):
+                    block_bounds(N_b, G, 0)
+                continue
+            cover = []
+            for g in range(G):
+                k0, k1 = block_bounds(N_b, G, g)
+                cover += list(range(k0, k1))
+            assert cover == list(range(N_b))
+
+
+class OracleBlockBackend:
+    """The oracle behind the block-parallel interface: block outputs E(S_k)
+    of the rank's blocks only, fusion = BGF + head."""
+
+    def __init__(self, cfg, w, strats):
+        import torch
+        self.torch, self.cfg, self.w, self.strats = torch, cfg, w, strats
+        self.device = torch.device("cpu")
+        self.n_blocks = cfg.N_b
+
+    def encode_blocks(self, events, r, k0, k1):
+        import oracle as O
+        item, action, scenario, ts = (a.numpy() for a in events)
+        return (O.encode_user(self.cfg, self.w, self.strats, item, action, scenario, r, ts), k0, k1)
+
+    def score_blocks(self, handle, items, k0, k1):
+        import oracle as O
+        cache, a, b = handle
+        assert (a, b) == (k0, k1)
+        E = O.block_outputs(self.cfg, self.w, cache, items.numpy())
+        return self.torch.tensor(E[:, k0:k1, :], dtype=self.torch.float64).contiguous()
+
+    def fuse(self, E_all, r, n_slices):
+        import oracle as O
+        G, M, nb, d = E_all.shape
+        E = E_all.permute(1, 0, 2, 3).reshape(M, G * nb, d).numpy()
+        return self.torch.tensor(O.head(self.cfg, self.w, O.bgf(self.cfg, self.w, E, r)))
+
+    def release(self, handle):
+        pass
+
+
+def _block_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    import synth
+    from paper_2502_09888_b200.sharded import rank_request_block_parallel
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = synth.preset("tiny", N_b=4, L=2, M=5, rel_bias=1)
+    w = synth.make_weights(cfg, 1)
+    u = synth.make_user(cfg, np.random.default_rng(4), n_s=150, M=5)
+    item, action, scenario, ts = u.user_events(0)
+    be = OracleBlockBackend(cfg, w, synth.strategies_for(cfg.N_b, cfg.R))
+    t = torch.from_numpy
+    events = (t(item), t(action), t(scenario), t(ts)) if rank == 0 else None
+    out = rank_request_block_parallel(be, dist, events, int(u.r[0]), torch.from_numpy(u.user_cands(0)))
+    q.put((rank, None if out is None else out.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_block_parallel_matches_single_process():
+    sys.path.insert(0, ROOT)
+    import oracle as O
+    import synth
+    port = socket.socket()
+    port.bind(("127.0.0.1", 0))
+    p = port.getsockname()[1]
+    port.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_block_worker, args=(r, 2, p, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=180) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert res[1] is None
+    cfg = synth.preset("tiny", N_b=4, L=2, M=5, rel_bias=1)
+    w = synth.make_weights(cfg, 1)
+    u = synth.make_user(cfg, np.random.default_rng(4), n_s=150, M=5)
+    ref = O.sumi_scores(cfg, w, synth.strategies_for(cfg.N_b, cfg.R), u, 0)
+    np.testing.assert_allclose(res[0], ref, rtol=0, atol=1e-12)     # fp64 transport: exact
