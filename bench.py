@@ -203,6 +203,7 @@ def aggregate_rate(units_per_rank, world, ms_max):
 def workload_cfg(cfg):
     return {"workload": cfg.name, "B": cfg.B, "M": cfg.M, "n": cfg.n, "N_b": cfg.N_b, "n_k": cfg.n_k, "L": cfg.L,
             "d": cfg.d, "h": cfg.h, "n_s": cfg.n_s if not cfg.n_s_max else [cfg.n_s, cfg.n_s_max],
+            "rel_bias": int(cfg.rel_bias),
             "parallelism": "request-sharded replicas (no data-path collective)",
             "l2": "no flush: per-step K/V cache + activations far exceed the 126 MB L2"}
 
@@ -265,6 +266,12 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="large", choices=sorted(synth.PRESETS))
+    ap.add_argument("--L", type=int, default=0, help="override layers per block (sweep axis)")
+    ap.add_argument("--n-k", type=int, default=0, help="override the per-block budget n_k (sweep axis; n_s = 3 n)")
+    ap.add_argument("--M", type=int, default=0, help="override candidates per user (sweep axis)")
+    ap.add_argument("--rel-bias", type=int, default=0, help="1: Eq. 3 relative attention bias on")
+    ap.add_argument("--reuse", type=int, default=0,
+                    help="warm K/V reuse: score R fresh candidate sets per cached user (SURVEY §8(d) medium)")
     ap.add_argument("--impl", default="climber", choices=["climber", "reference"])
     ap.add_argument("--users", type=int, default=0, help="override B (users per rank per step)")
     ap.add_argument("--latency-requests", type=int, default=30)
@@ -273,6 +280,17 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     cfg = synth.preset(args.config)
+    over = {}
+    if args.L:
+        over["L"] = args.L
+    if args.n_k:
+        over.update(n_k=args.n_k, n_s=3 * args.n_k * cfg.N_b, n_s_max=0)
+    if args.M:
+        over["M"] = args.M
+    if args.rel_bias:
+        over["rel_bias"] = 1
+    if over:
+        cfg = cfg.replace(**over)
     if args.users:
         cfg = cfg.replace(B=args.users)
     if args.impl == "reference":
@@ -357,6 +375,31 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(out.nbytes), "steps": ksteps,
                "api": "climber_rank_host (pinned host buffers)"}
 
+    # ---- warm K/V reuse: every cached user is scored with
+    # R fresh candidate sets; the reused cache must give bit-identical scores ----
+    warm = None
+    if args.reuse > 0:
+        hs = cl.encode_users(batch.ev_offsets, item, action, scenario, ts, batch.r)
+        cl.score_batched(hs, batch.cand_offsets, cand, scores)
+        fresh = scores.clone()
+        rng = np.random.default_rng(1000 + rank)
+        sets = [dev(synth.zipf_draw(rng, cfg.V, cfg.zipf_s, len(batch.cand))) for _ in range(args.reuse)]
+        out = torch.empty_like(scores)
+        torch.cuda.synchronize()
+        w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0.record(stream)
+        for cs in sets:
+            cl.score_batched(hs, batch.cand_offsets, cs, out)
+        w1.record(stream)
+        torch.cuda.synchronize()
+        cl.score_batched(hs, batch.cand_offsets, cand, out)
+        same = bool(torch.equal(out, fresh))
+        cl.release(hs)
+        wms = max_over_ranks(dist, w0.elapsed_time(w1), "cuda")
+        warm = {"value": aggregate_rate(int(batch.cand_offsets[-1]) * args.reuse, world, wms), "unit": "pairs/s",
+                "reuse": args.reuse, "bitwise_equal_fresh": same,
+                "mode": "K/V cached once per user, score-only steps with fresh candidate sets"}
+
     # ---- per-request latency: one user, M candidates, host call to host scores ----
     lat = None
     if args.latency_requests > 0 and world == 1:
@@ -390,6 +433,27 @@ def main():
             lat = {"p50": float(np.percentile(tl, 50)), "p99": float(np.percentile(tl, 99)), "requests": len(tl),
                    "mode": f"candidate-sharded over {world} GPUs: owner encodes, K/V slab broadcast (NCCL), "
                            f"scores all_gather; host call to host scores"}
+        if cfg.N_b % world == 0:
+            # block-parallel: each rank encodes + scores N_b / G blocks,
+            # block outputs all-gathered, rank 0 fuses; no K/V moves
+            from paper_2502_09888_b200.sharded import rank_request_block_parallel
+            tb = []
+            for i in range(args.latency_requests + 5):
+                u = batch.subset([i % B])
+                items = dev(u.cand)
+                dist.barrier()
+                t0 = time.perf_counter()
+                ev = (dev(u.item), dev(u.action), dev(u.scenario), dev(u.ts)) if rank == 0 else None
+                out = rank_request_block_parallel(be, dist, ev, int(u.r[0]), items)
+                if rank == 0:
+                    out.cpu()
+                    if i >= 5:
+                        tb.append((time.perf_counter() - t0) * 1e3)
+            if rank == 0:
+                lat["block_parallel"] = {
+                    "p50": float(np.percentile(tb, 50)), "p99": float(np.percentile(tb, 99)), "requests": len(tb),
+                    "mode": f"block-parallel over {world} GPUs: N_b / G blocks per rank (encode + score), "
+                            f"block outputs all_gather (NCCL), rank 0 fuses; host call to host scores"}
 
     if rank == 0:
         pk, pk_src = peaks()
@@ -401,6 +465,7 @@ def main():
                 "data": "synthetic", "config": workload_cfg(cfg), "roofline": roof,
                 "step_tflops": tot_flops / (ms_max * 1e-3) / 1e12,
                 "e2e": e2e, "latency_ms": lat, "gpu_launches": int(launches), "clocks": clk,
+                **({"warm_reuse": warm} if warm else {}),
                 "kernel_ms": {k: round(v["ms"], 3) for k, v in prof.items() if v["launches"]},
                 # per-class achieved rate over the timed steps: TFLOP/s where the class
                 # has algorithmic FLOPs, else GB/s of algorithmic bytes
