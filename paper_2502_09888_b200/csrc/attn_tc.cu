@@ -560,17 +560,18 @@ __global__ void __launch_bounds__(THREADS, 2)
 }
 
 // ===========================================================================
-// Persistent two-tile attention (default).  One CTA per SM (all 512 TMEM
+// Persistent two-tile attention (CLIMBER_ATTN_KERNEL=2).  One CTA per SM (all 512 TMEM
 // columns) loops over work items; an item = two adjacent 128-row query tiles
 // of one (user, block, head), so every K/V page loaded serves 256 query rows.
 //   warp 0     K/V producer: streams 64-key pages of every item into a ring
 //              that runs across items (the warp holds the item's page ids)
-//   warp 1     MMA issuer (one thread) for both tiles: S = Q K^T two chunks
-//              ahead, interleaved with O += P V (P from TMEM, V MN-major)
-//   warp 2     TMEM allocator
-//   warp 3     item decoder + Q / k_self / v_self producer: writes the item's
-//              descriptor to smem and loads its q tiles into one of two
-//              buffers while the previous item still runs
+//   warp 1     MMA issuer of tile 0, warp 3 of tile 1 (one thread each): S =
+//              Q K^T two chunks ahead, issued as soon as its TMEM buffer is
+//              free, and O += P V (P from TMEM, V MN-major); the two tiles share
+//              only the K/V ring (each stage is released by both threads)
+//   warp 2     TMEM allocator, then item decoder + Q / k_self / v_self
+//              producer: writes the item's descriptor to smem and loads its q
+//              tiles into one of two buffers while the previous item still runs
 //   warps 4-7  softmax + epilogue of tile 0, warps 8-11 of tile 1; each
 //              warpgroup owns half of TMEM (3 x 64 score/P columns + d_h
 //              output columns); the two ping-pong on the MUFU
@@ -689,13 +690,13 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmKV) : "memory");
     for (int b = 0; b < 2; ++b) {
       mbar_init(&q_full[b], 1);
-      mbar_init(&q_empty[b], 1 + 256);
+      mbar_init(&q_empty[b], 2 + 256);  // both MMA threads + every softmax thread
     }
     mbar_init(self_full, 1);
     mbar_init(self_empty, 256);
     for (int s = 0; s < ST; ++s) {
       mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+      mbar_init(&kv_empty[s], 2);  // released by both tiles' MMA threads
     }
     for (int b = 0; b < PT_WT * NSB; ++b) {
       mbar_init(&s_full[b], 1);
@@ -736,8 +737,8 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
       }
       __syncwarp();
     }
-  } else if (warp == 3) {
-    // ---------------- item decoder + q / self producer ----------------
+  } else if (warp == 2) {
+    // ---------------- item decoder + q / self producer (after the TMEM alloc) ----------------
     if (lane == 0) {
       long long seq = 0;
       for (long long it = blockIdx.x;; it += gridDim.x) {
@@ -780,22 +781,22 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
         ++seq;
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || warp == 3) {
     if (lane == 0) {
-      // ---------------- MMA issuer for both tiles ----------------
+      // ---------------- MMA issuer of one tile (warp 1: tile 0, warp 3: tile 1) ----------------
+      // The two tiles share only the K/V ring (kv_empty needs both threads) and
+      // the q buffers; each runs its own S -> P -> PV chain.
+      const int w = warp == 1 ? 0 : 1;
       constexpr uint32_t idesc_qk = idesc_bf16_major(ROWS, KEYS, 0, 0);
       constexpr uint32_t idesc_pv = idesc_bf16_major(ROWS, DH, 0, 1);
-      long long gk = 0;
-      long long cs[PT_WT] = {0, 0};
+      long long gk = 0, cs = 0;
       for (long long seq = 0;; ++seq) {
         const int b = (int)(seq & 1);
         MBW(&q_full[b], (uint32_t)((seq >> 1) & 1));
         fence_after();
         const PDesc& I = desc[b];
         if (I.end) break;
-        int nch[PT_WT];
-#pragma unroll
-        for (int w = 0; w < PT_WT; ++w) nch[w] = I.nch[w];
+        const int nch = I.nch[w];
         const int nkv = I.nkv;
         auto kv_wait = [&](int j) {
           MBW(&kv_full[(gk + j) % ST], (uint32_t)(((gk + j) / ST) & 1));
@@ -804,97 +805,52 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
         auto kdesc = [&](int j) {
           return make_sdesc(smem_u32(smem + Ly::KV_OFF + (int)((gk + j) % ST) * 2 * Ly::KVB), 16, 8 * Ly::RB, Ly::SWZ);
         };
-        auto qdesc = [&](int w) {
-          return make_sdesc(smem_u32(smem + Ly::Q_OFF + (b * PT_WT + w) * Ly::QB), 16, 8 * Ly::RB, Ly::SWZ);
-        };
-        auto sbuf = [&](int w, long long c) { return tmem_base + w * 256 + (uint32_t)(c % NSB) * KEYS; };
-        for (int j = 0; j < 2 && j < nkv; ++j) {
+        const uint64_t qd = make_sdesc(smem_u32(smem + Ly::Q_OFF + (b * PT_WT + w) * Ly::QB), 16, 8 * Ly::RB, Ly::SWZ);
+        auto sbuf = [&](long long c) { return tmem_base + w * 256 + (uint32_t)(c % NSB) * KEYS; };
+        const uint32_t tO = tmem_base + w * 256 + NSB * KEYS;
+        for (int j = 0; j < 2 && j < nch; ++j) {
           kv_wait(j);
           const uint64_t kd = kdesc(j);
+          const long long c = cs + j;  // score buffer c % 3 was last read by PV(c - 3)
+          if (c >= 3) MBW(&o_done[w * NSB + (int)((c - 3) % NSB)], (uint32_t)(((c - 3) / NSB) & 1));
 #pragma unroll
-          for (int w = 0; w < PT_WT; ++w) {
-            if (j >= nch[w]) continue;
-            const long long c = cs[w] + j;  // score buffer c % 3 was last read by PV(c - 3)
-            if (c >= 3) MBW(&o_done[w * NSB + (int)((c - 3) % NSB)], (uint32_t)(((c - 3) / NSB) & 1));
-            const uint64_t qd = qdesc(w);
-            const uint32_t tS = sbuf(w, c);
-#pragma unroll
-            for (int s = 0; s < DH / 16; ++s) mma_bf16(tS, qd + 2 * s, kd + 2 * s, idesc_qk, s > 0 ? 1u : 0u);
-            mma_commit(&s_full[w * NSB + (int)(c % NSB)]);
-          }
+          for (int s = 0; s < DH / 16; ++s) mma_bf16(sbuf(c), qd + 2 * s, kd + 2 * s, idesc_qk, s > 0 ? 1u : 0u);
+          mma_commit(&s_full[w * NSB + (int)(c % NSB)]);
         }
-        if (nkv <= 2) mma_commit(&q_empty[b]);
+        if (nch <= 2) mma_commit(&q_empty[b]);
         for (int j = 0; j < nkv; ++j) {
-          const int jq = j + 2;
-          uint64_t kq = 0;
-          if (jq < nkv) {
-            kv_wait(jq);
-            kq = kdesc(jq);
-          }
-          const uint64_t vd = kdesc(j) + (uint64_t)(Ly::KVB >> 4);
-          if (EARLY_S) {
-            // S(j+2) as soon as its buffer is free (PV(j-1) done), ahead of
-            // waiting for P(j): the score chain gets a full softmax period more slack
-#pragma unroll
-            for (int w = 0; w < PT_WT; ++w) {
-              if (jq >= nch[w]) continue;
-              const long long c = cs[w] + j;
-              if (c >= 1) MBW(&o_done[w * NSB + (int)((c - 1) % NSB)], (uint32_t)(((c - 1) / NSB) & 1));
-              fence_after();
-              const uint64_t qd = qdesc(w);
-              const uint32_t tSq = sbuf(w, c + 2);
-#pragma unroll
-              for (int s = 0; s < DH / 16; ++s) mma_bf16(tSq, qd + 2 * s, kq + 2 * s, idesc_qk, s > 0 ? 1u : 0u);
-              mma_commit(&s_full[w * NSB + (int)((c + 2) % NSB)]);
-            }
-#pragma unroll
-            for (int w = 0; w < PT_WT; ++w) {
-              if (j >= nch[w]) continue;
-              const long long c = cs[w] + j;
-              MBW(&p_full[w * NSB + (int)(c % NSB)], (uint32_t)((c / NSB) & 1));
-              fence_after();
-              const uint32_t tO = tmem_base + w * 256 + NSB * KEYS;
-              const uint32_t tP = sbuf(w, c);
-#pragma unroll
-              for (int s = 0; s < KEYS / 16; ++s) {
-                const uint64_t vds = vd + (uint64_t)((16 * Ly::RB) >> 4) * s;
-                const uint32_t acc = (MODE == MODE_SUMI || j > 0 || s > 0) ? 1u : 0u;
-                mma_bf16_ts(tO, tP + 8 * s, vds, idesc_pv, acc);
-              }
-              mma_commit(&o_done[w * NSB + (int)(c % NSB)]);
-            }
-            mma_commit(&kv_empty[(gk + j) % ST]);
-            if (jq == nkv - 1) mma_commit(&q_empty[b]);
+          if (j >= nch) {  // chunk unused by this tile: release the stage once it has landed
+            kv_wait(j);
+            mbar_arrive(&kv_empty[(gk + j) % ST]);
             continue;
           }
-#pragma unroll
-          for (int w = 0; w < PT_WT; ++w) {
-            if (j >= nch[w]) continue;
-            const bool q = jq < nch[w];
-            const long long c = cs[w] + j;
-            if (q && c >= 1) MBW(&o_done[w * NSB + (int)((c - 1) % NSB)], (uint32_t)(((c - 1) / NSB) & 1));
-            MBW(&p_full[w * NSB + (int)(c % NSB)], (uint32_t)((c / NSB) & 1));
+          const int jq = j + 2;
+          const long long c = cs + j;
+          if (jq < nch) {  // S(j+2) as soon as its buffer is free (PV(j-1) done)
+            kv_wait(jq);
+            const uint64_t kq = kdesc(jq);
+            if (c >= 1) MBW(&o_done[w * NSB + (int)((c - 1) % NSB)], (uint32_t)(((c - 1) / NSB) & 1));
             fence_after();
-            const uint64_t qd = qdesc(w);
-            const uint32_t tO = tmem_base + w * 256 + NSB * KEYS;
-            const uint32_t tP = sbuf(w, c);
-            const uint32_t tSq = sbuf(w, c + 2);
 #pragma unroll
-            for (int s = 0; s < KEYS / 16; ++s) {
-              const uint64_t vds = vd + (uint64_t)((16 * Ly::RB) >> 4) * s;
-              const uint32_t acc = (MODE == MODE_SUMI || j > 0 || s > 0) ? 1u : 0u;
-              mma_bf16_ts(tO, tP + 8 * s, vds, idesc_pv, acc);
-              if (q && s < DH / 16) mma_bf16(tSq, qd + 2 * s, kq + 2 * s, idesc_qk, s > 0 ? 1u : 0u);
-            }
-            mma_commit(&o_done[w * NSB + (int)(c % NSB)]);
-            if (q) mma_commit(&s_full[w * NSB + (int)((c + 2) % NSB)]);
+            for (int s = 0; s < DH / 16; ++s) mma_bf16(sbuf(c + 2), qd + 2 * s, kq + 2 * s, idesc_qk, s > 0 ? 1u : 0u);
+            mma_commit(&s_full[w * NSB + (int)((c + 2) % NSB)]);
+            if (jq == nch - 1) mma_commit(&q_empty[b]);  // this tile's last QK has been issued
           }
+          if (j < 2) kv_wait(j);  // (chunks >= 2 were waited for when their S was issued)
+          const uint64_t vd = kdesc(j) + (uint64_t)(Ly::KVB >> 4);
+          MBW(&p_full[w * NSB + (int)(c % NSB)], (uint32_t)((c / NSB) & 1));
+          fence_after();
+#pragma unroll
+          for (int s = 0; s < KEYS / 16; ++s) {
+            const uint64_t vds = vd + (uint64_t)((16 * Ly::RB) >> 4) * s;
+            const uint32_t acc = (MODE == MODE_SUMI || j > 0 || s > 0) ? 1u : 0u;
+            mma_bf16_ts(tO, sbuf(c) + 8 * s, vds, idesc_pv, acc);
+          }
+          mma_commit(&o_done[w * NSB + (int)(c % NSB)]);
           mma_commit(&kv_empty[(gk + j) % ST]);
-          if (jq == nkv - 1) mma_commit(&q_empty[b]);  // the item's last QK has been issued
         }
         gk += nkv;
-#pragma unroll
-        for (int w = 0; w < PT_WT; ++w) cs[w] += nch[w];
+        cs += nch;
       }
     }
   } else if (warp >= 4) {
