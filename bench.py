@@ -270,6 +270,7 @@ def main():
     ap.add_argument("--n-k", type=int, default=0, help="override the per-block budget n_k (sweep axis; n_s = 3 n)")
     ap.add_argument("--M", type=int, default=0, help="override candidates per user (sweep axis)")
     ap.add_argument("--rel-bias", type=int, default=0, help="1: Eq. 3 relative attention bias on")
+    ap.add_argument("--susi", type=int, default=1, help="1: also time the SUSI baseline (one record per pair)")
     ap.add_argument("--reuse", type=int, default=0,
                     help="warm K/V reuse: score R fresh candidate sets per cached user (SURVEY §8(d) medium)")
     ap.add_argument("--impl", default="climber", choices=["climber", "reference"])
@@ -375,6 +376,29 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(out.nbytes), "steps": ksteps,
                "api": "climber_rank_host (pinned host buffers)"}
 
+    # ---- SUSI baseline: the same pairs as "single user, single
+    # item" records, i.e. every pair pays its user's full history pass; one
+    # record per user here (its first candidate), through climber_forward ----
+    susi = None
+    if args.susi:
+        one = np.arange(B + 1, dtype=np.int64)
+        first = dev(batch.cand[batch.cand_offsets[:-1]])
+        out1 = torch.empty(B, dtype=torch.float32, device="cuda")
+        cl.forward(batch.ev_offsets, item, action, scenario, ts, batch.r, one, first, out1)
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        cl.forward(batch.ev_offsets, item, action, scenario, ts, batch.r, one, first, out1)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        sms = max_over_ranks(dist, s0.elapsed_time(s1), "cuda")
+        # compression is lossless: each SUSI score equals the SUMI score of that pair
+        same = bool(torch.equal(out1, scores[torch.from_numpy(batch.cand_offsets[:-1]).cuda()]))
+        sv = aggregate_rate(B, world, sms)
+        susi = {"value": sv, "unit": "pairs/s", "sumi_over_susi": value / sv, "bitwise_equal_sumi": same,
+                "mode": "single user, single item records (P:L253): one full history pass per scored pair, "
+                        "climber_forward; paper's training-side gain from the SUMI pattern: 5.15x (context)"}
+
     # ---- warm K/V reuse: every cached user is scored with
     # R fresh candidate sets; the reused cache must give bit-identical scores ----
     warm = None
@@ -465,7 +489,7 @@ def main():
                 "data": "synthetic", "config": workload_cfg(cfg), "roofline": roof,
                 "step_tflops": tot_flops / (ms_max * 1e-3) / 1e12,
                 "e2e": e2e, "latency_ms": lat, "gpu_launches": int(launches), "clocks": clk,
-                **({"warm_reuse": warm} if warm else {}),
+                **({"warm_reuse": warm} if warm else {}), **({"susi": susi} if susi else {}),
                 "kernel_ms": {k: round(v["ms"], 3) for k, v in prof.items() if v["launches"]},
                 # per-class achieved rate over the timed steps: TFLOP/s where the class
                 # has algorithmic FLOPs, else GB/s of algorithmic bytes

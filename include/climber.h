@@ -204,6 +204,21 @@ climber_status climber_score_items_batched(climber_ctx_t ctx, int32_t B, const c
                                            const int64_t* cand_offsets, const int32_t* items,
                                            float* scores, climber_stream_t stream);
 
+/* SUMI forward of compressed training records (SURVEY
+ * §8(f) NEXT-3): each user's "single user, multiple items" record — the
+ * history plus its items, causal history, items full-visible to the history
+ * and isolated from each other (diagonal) — is scored in one call without
+ * keeping a cache (encode + score with transient handles, released when the
+ * call returns).  Layouts as climber_encode_users + climber_score_items_batched
+ * (DEVICE events / items / scores, HOST offsets and scenarios).  The pages
+ * return to the pool on return: a later call on the SAME stream is ordered
+ * after this one; on another stream, synchronise first.  Backward is out of
+ * scope. */
+climber_status climber_forward(climber_ctx_t ctx, int32_t B, const int64_t* ev_offsets,
+                               const climber_events* events, const int32_t* scenario_r,
+                               const int64_t* cand_offsets, const int32_t* items, float* scores,
+                               climber_stream_t stream);
+
 /* End-to-end convenience call with HOST buffers: copies the events and the
  * candidates to the device, encodes, scores, copies the scores back to
  * `scores` (HOST float[cand_offsets[B]]), releases the handles and

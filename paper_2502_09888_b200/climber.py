@@ -92,6 +92,7 @@ def lib() -> C.CDLL:
             "climber_encode_users_blocks": (I32, [VP, I32, P, P, P, I32, I32, VP, P]),
             "climber_score_blocks": (I32, [VP, I32, P, P, VP, I32, I32, VP, VP]),
             "climber_fuse_scores": (I32, [VP, I32, P, P, I32, VP, VP, VP]),
+            "climber_forward": (I32, [VP, I32, P, P, P, P, VP, VP, VP]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -107,7 +108,7 @@ EXPORTED_SYMBOLS = ("climber_arena_bytes", "climber_create", "climber_destroy", 
                     "climber_last_error", "climber_debug_extract", "climber_debug_mask", "climber_debug_kv",
                     "climber_launch_count", "climber_debug_gemm", "climber_profile", "climber_profile_read",
                     "climber_kv_slab_bytes", "climber_kv_export", "climber_kv_import",
-                    "climber_encode_users_blocks", "climber_score_blocks", "climber_fuse_scores")
+                    "climber_encode_users_blocks", "climber_score_blocks", "climber_fuse_scores", "climber_forward")
 
 KERNEL_CLASSES = ("extract", "embed", "rmsnorm", "gemm_qkv", "gemm_o", "gemm_ffn_up", "gemm_ffn_down", "gemm_se",
                   "attn_hist", "attn_sumi", "attn_fusion", "head", "other")
@@ -285,6 +286,20 @@ class Climber:
             scores = self.torch.empty(items.numel(), dtype=self.torch.float32, device=items.device)
         _check(lib().climber_score_items(self.h, C.c_void_p(handle), C.c_void_p(items.data_ptr()), int(items.numel()),
                                          C.c_void_p(scores.data_ptr()), self._stream(stream)))
+        return scores
+
+    def forward(self, ev_offsets, item, action, scenario, ts, r, cand_offsets, items, scores=None, stream=None):
+        """SUMI forward of compressed training records (no cache kept): CUDA
+        tensors for events / items, numpy offsets and scenarios."""
+        ev_offsets = np.ascontiguousarray(ev_offsets, np.int64)
+        cand_offsets = np.ascontiguousarray(cand_offsets, np.int64)
+        r = np.ascontiguousarray(r, np.int32)
+        if scores is None:
+            scores = self.torch.empty(int(cand_offsets[-1]), dtype=self.torch.float32, device=items.device)
+        ev = _Events(item.data_ptr(), action.data_ptr(), scenario.data_ptr(), ts.data_ptr())
+        _check(lib().climber_forward(self.h, len(r), _ptr(ev_offsets), C.byref(ev), _ptr(r), _ptr(cand_offsets),
+                                     C.c_void_p(items.data_ptr()), C.c_void_p(scores.data_ptr()),
+                                     self._stream(stream)))
         return scores
 
     # -- block-parallel serving (NEXT-2): blocks [k0, k1) per process --------

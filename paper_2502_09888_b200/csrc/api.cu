@@ -1557,6 +1557,28 @@ static climber_status rank_one_graph(climber_ctx_s* c, long long E, long long P,
 }
 
 // ---------------------------------------------------------------------------
+// SUMI forward of compressed training records:
+// one "single user, multiple items" record per user = history + its items in
+// one pass (causal history, items full-visible to the history, diagonal among
+// items), no cache kept: encode + score with transient handles.
+// ---------------------------------------------------------------------------
+extern "C" climber_status climber_forward(climber_ctx_t c, int32_t B, const int64_t* ev_offsets,
+                                          const climber_events* events, const int32_t* scenario_r,
+                                          const int64_t* cand_offsets, const int32_t* items, float* scores,
+                                          climber_stream_t stream) {
+  if (!c || !cand_offsets || !items || !scores) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+  if (B < 1 || B > c->cfg.max_batch_users) return fail(CLIMBER_E_INVALID_ARG, "B out of range");
+  std::vector<climber_kv_t> kvs(B);
+  climber_status st = climber_encode_users(c, B, ev_offsets, events, scenario_r, stream, kvs.data());
+  if (st != CLIMBER_OK) return st;
+  st = climber_score_items_batched(c, B, kvs.data(), cand_offsets, items, scores, stream);
+  // the pages return to the pool now; later calls on this stream are ordered
+  // after this one (other streams: synchronise first)
+  for (int b = 0; b < B; ++b) climber_kv_release(c, kvs[b]);
+  return st;
+}
+
+// ---------------------------------------------------------------------------
 // end-to-end call with host buffers
 // ---------------------------------------------------------------------------
 extern "C" climber_status climber_rank_host(climber_ctx_t c, int32_t B, const int64_t* ev_offsets,

@@ -266,3 +266,31 @@ def test_rel_bias_bf16_latency_mode_and_config_errors():
     with pytest.raises(ClimberError) as ei:
         make_gpu(bad, synth.make_weights(bad, 0), 1)
     assert ei.value.name == "E_CONFIG"
+
+
+# ---------------------------------------------------------------------------
+# SUMI forward of compressed training records (NEXT-3)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["small", "medium"])
+def test_forward_sumi_record_equals_susi_records(name):
+    # one "single user, multiple items" record scores every item exactly as the
+    # "single user, single item" records of the same pairs do (bitwise), and as
+    # the cached serving path
+    import torch
+    cfg = synth.preset(name)
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 4, B=2, M=24)
+    cl = make_gpu(cfg, w, 24, M_max=24)
+    item, action, scenario, ts, cand = to_dev(batch)
+    sumi = cl.forward(batch.ev_offsets, item, action, scenario, ts, batch.r, batch.cand_offsets, cand)
+    serve = gpu_scores(cl, batch)
+    assert np.array_equal(sumi.cpu().numpy(), serve)
+    for b in range(batch.B):
+        u = batch.subset([b] * 24)                       # 24 records of user b, one item each
+        c0 = int(batch.cand_offsets[b])
+        items = torch.from_numpy(batch.cand[c0:c0 + 24].copy()).cuda()
+        dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        susi = cl.forward(u.ev_offsets, dv(u.item), dv(u.action), dv(u.scenario), dv(u.ts), u.r,
+                          np.arange(25, dtype=np.int64), items)
+        assert torch.equal(susi, sumi[c0:c0 + 24])
+    cl.stream_status()
