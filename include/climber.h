@@ -269,6 +269,35 @@ climber_status climber_fuse_scores(climber_ctx_t ctx, int32_t B, const int64_t* 
  * work still reads it.  Double release -> CLIMBER_E_STALE. */
 climber_status climber_kv_release(climber_ctx_t ctx, climber_kv_t kv);
 
+/* ---- serving cache store ("concurrent
+ * readers, atomic cache build"; PAPER.md L161 on static caches) ----
+ * Handles keyed by (user_key, scenario r) with the caller's digest of the
+ * event log (e.g. a hash of ids + timestamps; "digest mismatch ->
+ * staleness").  An entry is pinned while any caller holds it; unpinned
+ * entries are evicted least-recently-used when an encode needs pages.  The
+ * store owns its handles: never climber_kv_release one; call
+ * climber_cache_release to unpin.  Thread-safe (one mutex; a miss encodes
+ * under it, so concurrent acquires of one key build the cache once). */
+typedef enum {
+  CLIMBER_CACHE_HIT = 0,        /* same key, same digest: the cached K/V is returned */
+  CLIMBER_CACHE_ENCODED = 1,    /* miss or stale digest: encoded now and cached */
+  CLIMBER_CACHE_UNCACHED = 2    /* stale, but the old entry is pinned by another caller:
+                                 * encoded now, returned pinned, dropped on release */
+} climber_cache_result;
+
+/* Pin (and build if needed) the cache of one user.  events: DEVICE arrays of
+ * n_s events (as climber_encode_user); result: HOST out, climber_cache_result.
+ * CLIMBER_E_CAPACITY when every page is held by pinned entries. */
+climber_status climber_cache_acquire(climber_ctx_t ctx, uint64_t user_key, int32_t scenario_r, uint64_t digest,
+                                     const climber_events* events, int64_t n_s, climber_stream_t stream,
+                                     climber_kv_t* out, int32_t* result);
+
+/* Unpin a handle returned by climber_cache_acquire. */
+climber_status climber_cache_release(climber_ctx_t ctx, climber_kv_t kv);
+
+/* Entries, pinned entries, hits, misses and evictions so far (HOST int64[5]). */
+climber_status climber_cache_stats(climber_ctx_t ctx, int64_t* stats);
+
 /* ---- multi-GPU candidate sharding (latency mode) ----
  * The owner rank encodes the user, exports the handle's K/V pages into one
  * contiguous DEVICE slab, the slab is replicated with a collective of the

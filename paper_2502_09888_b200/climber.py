@@ -93,6 +93,9 @@ def lib() -> C.CDLL:
             "climber_score_blocks": (I32, [VP, I32, P, P, VP, I32, I32, VP, VP]),
             "climber_fuse_scores": (I32, [VP, I32, P, P, I32, VP, VP, VP]),
             "climber_forward": (I32, [VP, I32, P, P, P, P, VP, VP, VP]),
+            "climber_cache_acquire": (I32, [VP, C.c_uint64, I32, C.c_uint64, P, I64, VP, P, P]),
+            "climber_cache_release": (I32, [VP, VP]),
+            "climber_cache_stats": (I32, [VP, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -108,7 +111,8 @@ EXPORTED_SYMBOLS = ("climber_arena_bytes", "climber_create", "climber_destroy", 
                     "climber_last_error", "climber_debug_extract", "climber_debug_mask", "climber_debug_kv",
                     "climber_launch_count", "climber_debug_gemm", "climber_profile", "climber_profile_read",
                     "climber_kv_slab_bytes", "climber_kv_export", "climber_kv_import",
-                    "climber_encode_users_blocks", "climber_score_blocks", "climber_fuse_scores", "climber_forward")
+                    "climber_encode_users_blocks", "climber_score_blocks", "climber_fuse_scores", "climber_forward",
+                    "climber_cache_acquire", "climber_cache_release", "climber_cache_stats")
 
 KERNEL_CLASSES = ("extract", "embed", "rmsnorm", "gemm_qkv", "gemm_o", "gemm_ffn_up", "gemm_ffn_down", "gemm_se",
                   "attn_hist", "attn_sumi", "attn_fusion", "head", "other")
@@ -301,6 +305,25 @@ class Climber:
                                      C.c_void_p(items.data_ptr()), C.c_void_p(scores.data_ptr()),
                                      self._stream(stream)))
         return scores
+
+    # -- serving cache store (NEXT-4) ---------------------------------------
+    CACHE_RESULT = {0: "hit", 1: "encoded", 2: "uncached"}
+
+    def cache_acquire(self, user_key: int, r: int, digest: int, item, action, scenario, ts, stream=None):
+        """(handle, "hit" | "encoded" | "uncached"); events are CUDA tensors."""
+        ev = _Events(item.data_ptr(), action.data_ptr(), scenario.data_ptr(), ts.data_ptr())
+        out, res = C.c_void_p(), C.c_int32()
+        _check(lib().climber_cache_acquire(self.h, C.c_uint64(user_key), int(r), C.c_uint64(digest), C.byref(ev),
+                                           int(item.numel()), self._stream(stream), C.byref(out), C.byref(res)))
+        return out.value, self.CACHE_RESULT[res.value]
+
+    def cache_release(self, handle):
+        _check(lib().climber_cache_release(self.h, C.c_void_p(handle)))
+
+    def cache_stats(self) -> dict:
+        st = np.zeros(5, np.int64)
+        _check(lib().climber_cache_stats(self.h, _ptr(st)))
+        return dict(zip(("entries", "pinned", "hits", "misses", "evictions"), map(int, st)))
 
     # -- block-parallel serving (NEXT-2): blocks [k0, k1) per process --------
     def encode_users_blocks(self, ev_offsets, item, action, scenario, ts, r, k0: int, k1: int,

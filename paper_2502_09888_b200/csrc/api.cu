@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -118,6 +119,19 @@ struct climber_ctx_s {
   void* g_io = nullptr;
   long long g_launches = 0;
   long long g_seen_E = -1, g_seen_P = -1;  // last shape run eagerly
+  // serving cache store (NEXT-4): (user_key, r) -> entry; LRU by tick
+  struct CacheEntry {
+    climber_kv_t kv;
+    uint64_t digest;
+    int pins;
+    unsigned long long tick;
+    bool dropped;  // stale while pinned: released on the last unpin
+  };
+  std::mutex store_mu;
+  std::map<std::pair<uint64_t, int>, CacheEntry> store;
+  std::vector<CacheEntry> orphans;  // uncached (stale-while-pinned) handles still held by callers
+  unsigned long long store_tick = 0;
+  long long st_hits = 0, st_miss = 0, st_evict = 0;
   cudaStream_t g_stream = nullptr;          // capture stream
   bool graphs = true;
 };
@@ -1554,6 +1568,95 @@ static climber_status rank_one_graph(climber_ctx_s* c, long long E, long long P,
   }
   climber_kv_release(c, kv);
   return st;
+}
+
+// ---------------------------------------------------------------------------
+// serving cache store (NEXT-4)
+// ---------------------------------------------------------------------------
+static bool pool_has_room(climber_ctx_s* c) {
+  std::lock_guard<std::mutex> g(c->mu);
+  return !c->free_slots.empty() && (long long)c->free_pages.size() >= c->per_slot;
+}
+
+// evict the least-recently-used unpinned entry; false if none
+static bool store_evict_one(climber_ctx_s* c) {
+  auto victim = c->store.end();
+  for (auto it = c->store.begin(); it != c->store.end(); ++it)
+    if (it->second.pins == 0 && (victim == c->store.end() || it->second.tick < victim->second.tick)) victim = it;
+  if (victim == c->store.end()) return false;
+  climber_kv_release(c, victim->second.kv);
+  c->store.erase(victim);
+  ++c->st_evict;
+  return true;
+}
+
+extern "C" climber_status climber_cache_acquire(climber_ctx_t c, uint64_t user_key, int32_t scenario_r,
+                                                uint64_t digest, const climber_events* events, int64_t n_s,
+                                                climber_stream_t stream, climber_kv_t* out, int32_t* result) {
+  if (!c || !events || !out || !result) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+  std::lock_guard<std::mutex> g(c->store_mu);
+  const auto key = std::make_pair(user_key, (int)scenario_r);
+  auto it = c->store.find(key);
+  if (it != c->store.end() && it->second.digest == digest && !it->second.dropped) {
+    it->second.pins++;
+    it->second.tick = ++c->store_tick;
+    ++c->st_hits;
+    *out = it->second.kv;
+    *result = CLIMBER_CACHE_HIT;
+    return CLIMBER_OK;
+  }
+  ++c->st_miss;
+  bool uncached = false;
+  if (it != c->store.end()) {  // stale digest
+    if (it->second.pins == 0) {
+      climber_kv_release(c, it->second.kv);
+      c->store.erase(it);
+    } else {  // another caller still reads the old K/V: hand out an uncached build
+      uncached = true;
+    }
+  }
+  while (!pool_has_room(c))
+    if (!store_evict_one(c)) return fail(CLIMBER_E_CAPACITY, "every cached handle is pinned");
+  climber_kv_t kv;
+  climber_status st = climber_encode_user(c, events, n_s, scenario_r, stream, &kv);
+  if (st != CLIMBER_OK) return st;
+  climber_ctx_s::CacheEntry e{kv, digest, 1, ++c->store_tick, uncached};
+  if (uncached) c->orphans.push_back(e);
+  else c->store[key] = e;
+  *out = kv;
+  *result = uncached ? CLIMBER_CACHE_UNCACHED : CLIMBER_CACHE_ENCODED;
+  return CLIMBER_OK;
+}
+
+extern "C" climber_status climber_cache_release(climber_ctx_t c, climber_kv_t kv) {
+  if (!c) return fail(CLIMBER_E_INVALID_ARG, "null ctx");
+  std::lock_guard<std::mutex> g(c->store_mu);
+  for (auto& kvp : c->store)
+    if (kvp.second.kv == kv) {
+      if (kvp.second.pins <= 0) return fail(CLIMBER_E_STALE, "cache handle is not pinned");
+      kvp.second.pins--;
+      return CLIMBER_OK;
+    }
+  for (size_t i = 0; i < c->orphans.size(); ++i)
+    if (c->orphans[i].kv == kv) {
+      climber_kv_release(c, kv);
+      c->orphans.erase(c->orphans.begin() + i);
+      return CLIMBER_OK;
+    }
+  return fail(CLIMBER_E_STALE, "handle is not held by the cache store");
+}
+
+extern "C" climber_status climber_cache_stats(climber_ctx_t c, int64_t* stats) {
+  if (!c || !stats) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+  std::lock_guard<std::mutex> g(c->store_mu);
+  long long pinned = 0;
+  for (auto& kvp : c->store) pinned += kvp.second.pins > 0;
+  stats[0] = (int64_t)c->store.size();
+  stats[1] = pinned + (int64_t)c->orphans.size();
+  stats[2] = c->st_hits;
+  stats[3] = c->st_miss;
+  stats[4] = c->st_evict;
+  return CLIMBER_OK;
 }
 
 // ---------------------------------------------------------------------------

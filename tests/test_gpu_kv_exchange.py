@@ -148,3 +148,68 @@ def test_block_parallel_driver_world1_nccl():
         cl.release(h)
     finally:
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# serving cache store (NEXT-4): hits, staleness, LRU eviction, pinning
+# ---------------------------------------------------------------------------
+def test_cache_store_hits_staleness_and_lru():
+    import torch
+    from paper_2502_09888_b200 import ClimberError
+    cfg = synth.preset("small")
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 9, B=3)
+    cl = make_gpu(cfg, w, 3, kv_users=2)           # room for two cached users
+    dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    ev = [tuple(dv(a) for a in batch.user_events(b)) for b in range(3)]
+    cands = [dv(batch.user_cands(b)) for b in range(3)]
+    def score(h, b):
+        return cl.score_items(h, cands[b]).cpu().numpy()
+
+    fresh = []
+    for b in range(3):                              # one user at a time (the pool holds two)
+        h = cl.encode_user(*ev[b], int(batch.r[b]))
+        fresh.append(score(h, b))
+        cl.release(h)
+    fresh = np.concatenate(fresh)
+    off = batch.cand_offsets
+
+    h0, res = cl.cache_acquire(100, int(batch.r[0]), 7, *ev[0])
+    assert res == "encoded" and np.array_equal(score(h0, 0), fresh[off[0]:off[1]])
+    h0b, res = cl.cache_acquire(100, int(batch.r[0]), 7, *ev[0])
+    assert res == "hit" and h0b == h0                               # same K/V, no encode
+    cl.cache_release(h0b)
+    cl.cache_release(h0)
+    h1, res = cl.cache_acquire(101, int(batch.r[1]), 7, *ev[1])
+    assert res == "encoded"
+    cl.cache_release(h1)
+    # a third user: the pool holds two handles -> the LRU unpinned entry (user 100) goes
+    h2, res = cl.cache_acquire(102, int(batch.r[2]), 7, *ev[2])
+    assert res == "encoded" and np.array_equal(score(h2, 2), fresh[off[2]:off[3]])
+    cl.cache_release(h2)
+    st = cl.cache_stats()
+    assert st["entries"] == 2 and st["evictions"] == 1 and st["hits"] == 1
+    # user 101 is still cached; a new digest (the log changed) while the old
+    # K/V is pinned builds an uncached handle (evicting the unpinned user 102)
+    h1b, res = cl.cache_acquire(101, int(batch.r[1]), 7, *ev[1])
+    assert res == "hit"
+    h1c, res = cl.cache_acquire(101, int(batch.r[1]), 8, *ev[1])
+    assert res == "uncached"
+    assert np.array_equal(score(h1c, 1), fresh[off[1]:off[2]])
+    cl.cache_release(h1c)
+    cl.cache_release(h1b)
+    assert cl.cache_stats()["evictions"] == 2
+    h2b, res = cl.cache_acquire(102, int(batch.r[2]), 7, *ev[2])
+    assert res == "encoded"
+    h1d, res = cl.cache_acquire(101, int(batch.r[1]), 8, *ev[1])   # stale, unpinned: rebuilt in place
+    assert res == "encoded"
+    # every handle pinned -> capacity error, nothing evicted
+    with pytest.raises(ClimberError) as ei:
+        cl.cache_acquire(100, int(batch.r[0]), 7, *ev[0])
+    assert ei.value.name == "E_CAPACITY"
+    with pytest.raises(ClimberError):
+        cl.cache_release(12345)
+    cl.cache_release(h2b)
+    cl.cache_release(h1d)
+    assert cl.cache_stats()["pinned"] == 0
+    cl.stream_status()
