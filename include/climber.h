@@ -281,8 +281,9 @@ climber_status climber_kv_release(climber_ctx_t ctx, climber_kv_t kv);
 typedef enum {
   CLIMBER_CACHE_HIT = 0,        /* same key, same digest: the cached K/V is returned */
   CLIMBER_CACHE_ENCODED = 1,    /* miss or stale digest: encoded now and cached */
-  CLIMBER_CACHE_UNCACHED = 2    /* stale, but the old entry is pinned by another caller:
+  CLIMBER_CACHE_UNCACHED = 2,   /* stale, but the old entry is pinned by another caller:
                                  * encoded now, returned pinned, dropped on release */
+  CLIMBER_CACHE_APPENDED = 3    /* incremental update in place (climber_cache_append) */
 } climber_cache_result;
 
 /* Pin (and build if needed) the cache of one user.  events: DEVICE arrays of
@@ -292,7 +293,23 @@ climber_status climber_cache_acquire(climber_ctx_t ctx, uint64_t user_key, int32
                                      const climber_events* events, int64_t n_s, climber_stream_t stream,
                                      climber_kv_t* out, int32_t* result);
 
-/* Unpin a handle returned by climber_cache_acquire. */
+/* Incremental update after the user's event log grew by appending
+ * (static caches go stale; NEXT-4).  If the cached entry's
+ * digest is `digest_prefix` (the caller's digest of the first events, i.e. the
+ * old log) and it is not pinned, only the blocks whose strategy a_k matches
+ * an appended event are recomputed in place (S_k of the others is unchanged,
+ * Eq. 2), extraction and the request-time bias rows are redone, and the entry
+ * takes `digest`; result = CLIMBER_CACHE_APPENDED, *blocks_recomputed = how
+ * many of the N_b stacks ran.  Otherwise it behaves as climber_cache_acquire
+ * with `digest` (*blocks_recomputed = N_b).  Scores from the updated handle
+ * are bit-identical to a full encode of the new log.  Synchronises `stream`
+ * once (to read which blocks changed). */
+climber_status climber_cache_append(climber_ctx_t ctx, uint64_t user_key, int32_t scenario_r,
+                                    uint64_t digest_prefix, uint64_t digest, const climber_events* events,
+                                    int64_t n_s, climber_stream_t stream, climber_kv_t* out, int32_t* result,
+                                    int32_t* blocks_recomputed);
+
+/* Unpin a handle returned by climber_cache_acquire / climber_cache_append. */
 climber_status climber_cache_release(climber_ctx_t ctx, climber_kv_t kv);
 
 /* Entries, pinned entries, hits, misses and evictions so far (HOST int64[5]). */

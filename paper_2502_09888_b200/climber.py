@@ -95,6 +95,7 @@ def lib() -> C.CDLL:
             "climber_forward": (I32, [VP, I32, P, P, P, P, VP, VP, VP]),
             "climber_cache_acquire": (I32, [VP, C.c_uint64, I32, C.c_uint64, P, I64, VP, P, P]),
             "climber_cache_release": (I32, [VP, VP]),
+            "climber_cache_append": (I32, [VP, C.c_uint64, I32, C.c_uint64, C.c_uint64, P, I64, VP, P, P, P]),
             "climber_cache_stats": (I32, [VP, P]),
         }
         for name, (res, args) in sig.items():
@@ -112,7 +113,8 @@ EXPORTED_SYMBOLS = ("climber_arena_bytes", "climber_create", "climber_destroy", 
                     "climber_launch_count", "climber_debug_gemm", "climber_profile", "climber_profile_read",
                     "climber_kv_slab_bytes", "climber_kv_export", "climber_kv_import",
                     "climber_encode_users_blocks", "climber_score_blocks", "climber_fuse_scores", "climber_forward",
-                    "climber_cache_acquire", "climber_cache_release", "climber_cache_stats")
+                    "climber_cache_acquire", "climber_cache_release", "climber_cache_stats",
+                    "climber_cache_append")
 
 KERNEL_CLASSES = ("extract", "embed", "rmsnorm", "gemm_qkv", "gemm_o", "gemm_ffn_up", "gemm_ffn_down", "gemm_se",
                   "attn_hist", "attn_sumi", "attn_fusion", "head", "other")
@@ -307,7 +309,7 @@ class Climber:
         return scores
 
     # -- serving cache store (NEXT-4) ---------------------------------------
-    CACHE_RESULT = {0: "hit", 1: "encoded", 2: "uncached"}
+    CACHE_RESULT = {0: "hit", 1: "encoded", 2: "uncached", 3: "appended"}
 
     def cache_acquire(self, user_key: int, r: int, digest: int, item, action, scenario, ts, stream=None):
         """(handle, "hit" | "encoded" | "uncached"); events are CUDA tensors."""
@@ -316,6 +318,16 @@ class Climber:
         _check(lib().climber_cache_acquire(self.h, C.c_uint64(user_key), int(r), C.c_uint64(digest), C.byref(ev),
                                            int(item.numel()), self._stream(stream), C.byref(out), C.byref(res)))
         return out.value, self.CACHE_RESULT[res.value]
+
+    def cache_append(self, user_key: int, r: int, digest_prefix: int, digest: int, item, action, scenario, ts,
+                     stream=None):
+        """(handle, result, blocks recomputed) after the user's log grew by appending."""
+        ev = _Events(item.data_ptr(), action.data_ptr(), scenario.data_ptr(), ts.data_ptr())
+        out, res, nb = C.c_void_p(), C.c_int32(), C.c_int32()
+        _check(lib().climber_cache_append(self.h, C.c_uint64(user_key), int(r), C.c_uint64(digest_prefix),
+                                          C.c_uint64(digest), C.byref(ev), int(item.numel()), self._stream(stream),
+                                          C.byref(out), C.byref(res), C.byref(nb)))
+        return out.value, self.CACHE_RESULT[res.value], nb.value
 
     def cache_release(self, handle):
         _check(lib().climber_cache_release(self.h, C.c_void_p(handle)))

@@ -126,7 +126,9 @@ struct climber_ctx_s {
     int pins;
     unsigned long long tick;
     bool dropped;  // stale while pinned: released on the last unpin
+    long long n_s;  // events the cached K/V was built from
   };
+  int* d_flags = nullptr;  // incremental append: per-block "a new event matches a_k"
   std::mutex store_mu;
   std::map<std::pair<uint64_t, int>, CacheEntry> store;
   std::vector<CacheEntry> orphans;  // uncached (stale-while-pinned) handles still held by callers
@@ -466,6 +468,7 @@ extern "C" climber_status climber_destroy(climber_ctx_t c) {
   if (c->io) cudaFree(c->io);
   if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
   if (c->g_stream) cudaStreamDestroy(c->g_stream);
+  if (c->d_flags) cudaFree(c->d_flags);
   cudaEventDestroy(c->stage_evt);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete c;
@@ -947,6 +950,7 @@ static void encode_wave_grouped(climber_ctx_s* c, const EventsDev& ev, int u0, i
     Prof p(c, CLIMBER_K_OTHER, s, 0, (double)U * D.L * D.Nb * D.h * D.nk * 12);
     launch_cand_bias(wslot, c->d_r + u0, U, c->vlen_all, D, s);
   }
+  if (nbk == 0) return;  // extraction (and the candidate bias rows) only: incremental append
   bf16* Xb = (bf16*)c->Xb;   // [Nb][rows][d]
   bf16* Qb = (bf16*)c->QKV;  // [Nb][rows][d]
   bf16* O = (bf16*)c->O;     // [Nb][rows][d]
@@ -1620,12 +1624,88 @@ extern "C" climber_status climber_cache_acquire(climber_ctx_t c, uint64_t user_k
   climber_kv_t kv;
   climber_status st = climber_encode_user(c, events, n_s, scenario_r, stream, &kv);
   if (st != CLIMBER_OK) return st;
-  climber_ctx_s::CacheEntry e{kv, digest, 1, ++c->store_tick, uncached};
+  climber_ctx_s::CacheEntry e{kv, digest, 1, ++c->store_tick, uncached, n_s};
   if (uncached) c->orphans.push_back(e);
   else c->store[key] = e;
   *out = kv;
   *result = uncached ? CLIMBER_CACHE_UNCACHED : CLIMBER_CACHE_ENCODED;
   return CLIMBER_OK;
+}
+
+// Incremental update of a cached user whose event log grew by appending
+// (PAPER.md L161's critique of static caches).  The
+// blocks are independent (Eq. 2: S_k is a filter of S), so only the blocks
+// whose strategy a_k matches an appended event change; their stacks are
+// recomputed in place, the others keep their K/V (bit-identical to a full
+// re-encode of the new log).  Extraction and the request-time bias rows are
+// always redone (the request time moved).
+extern "C" climber_status climber_cache_append(climber_ctx_t c, uint64_t user_key, int32_t scenario_r,
+                                               uint64_t digest_prefix, uint64_t digest, const climber_events* events,
+                                               int64_t n_s, climber_stream_t stream, climber_kv_t* out,
+                                               int32_t* result, int32_t* blocks_recomputed) {
+  if (!c || !events || !out || !result || !blocks_recomputed) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+  *blocks_recomputed = 0;
+  {
+    std::unique_lock<std::mutex> g(c->store_mu);
+    auto it = c->store.find(std::make_pair(user_key, (int)scenario_r));
+    const bool inplace = it != c->store.end() && it->second.digest == digest_prefix && !it->second.dropped &&
+                         it->second.pins == 0 && n_s >= it->second.n_s && grouped_ok(c) &&
+                         attn_tc_supported(c->D.dh, c->D.nk, true) && n_s > 0;
+    if (inplace) {
+      cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+      climber_ctx_s::CacheEntry& e = it->second;
+      int slot;
+      {
+        std::lock_guard<std::mutex> gm(c->mu);
+        climber_status rs = resolve(c, e.kv, &slot);
+        if (rs != CLIMBER_OK) return rs;
+      }
+      const int Nb = c->D.Nb;
+      if (!c->d_flags) CU(cudaMalloc(&c->d_flags, 64 * sizeof(int)));
+      CU(cudaMemsetAsync(c->d_flags, 0, Nb * sizeof(int), s));
+      if (n_s > e.n_s)
+        launch_append_flags(events->action, events->scenario, e.n_s, n_s, c->amask, c->smask, c->d_flags, c->D, s);
+      int flags[64];
+      CU(cudaMemcpyAsync(flags, c->d_flags, Nb * sizeof(int), cudaMemcpyDeviceToHost, s));
+      CU(cudaStreamSynchronize(s));
+      {
+        std::lock_guard<std::mutex> gm(c->mu);
+        CU(cudaEventSynchronize(c->stage_evt));
+        Stage h = stage_layout(c, c->h_stage);
+        h.slots[0] = slot;
+        h.r[0] = scenario_r;
+        h.ev_off[0] = 0;
+        h.ev_off[1] = n_s;
+        climber_status rs = stage_upload(c, 1, false, s);
+        if (rs != CLIMBER_OK) return rs;
+      }
+      EventsDev ev{events->item, events->action, events->scenario, events->ts};
+      int done = 0;
+      for (int k = 0; k < Nb;) {  // contiguous runs of changed blocks
+        if (!flags[k]) { ++k; continue; }
+        int k1 = k;
+        while (k1 < Nb && flags[k1]) ++k1;
+        encode_wave_grouped(c, ev, 0, 1, n_s, s, k, k1 - k);
+        done += k1 - k;
+        k = k1;
+      }
+      if (done == 0) encode_wave_grouped(c, ev, 0, 1, n_s, s, 0, 0);  // extraction + bias rows only
+      climber_status rs = check_launch(c, s);
+      if (rs != CLIMBER_OK) return rs;
+      e.digest = digest;
+      e.n_s = n_s;
+      e.pins = 1;
+      e.tick = ++c->store_tick;
+      ++c->st_hits;
+      *out = e.kv;
+      *result = CLIMBER_CACHE_APPENDED;
+      *blocks_recomputed = done;
+      return CLIMBER_OK;
+    }
+  }
+  // not incrementally updatable: a (re)build under the new digest
+  *blocks_recomputed = c->D.Nb;
+  return climber_cache_acquire(c, user_key, scenario_r, digest, events, n_s, stream, out, result);
 }
 
 extern "C" climber_status climber_cache_release(climber_ctx_t c, climber_kv_t kv) {

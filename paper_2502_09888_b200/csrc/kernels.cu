@@ -119,6 +119,26 @@ void launch_row_prep(const float* C, bf16* Cb, float* part, long long rows, int 
   k_row_prep<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(C, Cb, part, rows, d, pld);
 }
 
+// Incremental cache update: flags[k] = 1 if an appended event e in [n0, n1)
+// passes strategy a_k's filter (Eq. 2), i.e. S_k changed.
+__global__ void k_append_flags(const uint8_t* __restrict__ action, const uint8_t* __restrict__ scenario, long long n0,
+                               long long n1, const unsigned long long* __restrict__ amask,
+                               const unsigned long long* __restrict__ smask, int* __restrict__ flags, Dims D) {
+  for (long long i = n0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n1; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned a = action[i], sc = scenario[i];
+    for (int k = 0; k < D.Nb; ++k)
+      if (a < 64 && sc < 64 && ((amask[k] >> a) & 1ull) && ((smask[k] >> sc) & 1ull)) flags[k] = 1;
+  }
+}
+
+void launch_append_flags(const uint8_t* action, const uint8_t* scenario, long long n0, long long n1,
+                         const unsigned long long* amask, const unsigned long long* smask, int* flags, const Dims& D,
+                         cudaStream_t s) {
+  const long long n = n1 - n0;
+  const int blocks = (int)((n + 255) / 256 < 148 ? (n + 255) / 256 : 148);
+  k_append_flags<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(action, scenario, n0, n1, amask, smask, flags, D);
+}
+
 void launch_cand_bias(const int* wave_slot, const int* wave_r, int U, const int* vlen_all, const Dims& D,
                       cudaStream_t s) {
   k_cand_bias<<<dim3(U, D.L * D.Nb * D.h), 128, 0, s>>>(wave_slot, wave_r, vlen_all, D);

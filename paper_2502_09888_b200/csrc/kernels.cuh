@@ -16,6 +16,10 @@ void launch_cand_bias(const int* wave_slot, const int* wave_r, int U, const int*
                       cudaStream_t s);
 // block-parallel fusion input: bf16 copy + norm partials of gathered fp32 rows
 void launch_row_prep(const float* C, bf16* Cb, float* part, long long rows, int d, int pld, cudaStream_t s);
+// incremental cache update: which strategies an appended event range matches
+void launch_append_flags(const uint8_t* action, const uint8_t* scenario, long long n0, long long n1,
+                         const unsigned long long* amask, const unsigned long long* smask, int* flags, const Dims& D,
+                         cudaStream_t s);
 void launch_extract(const EventsDev& ev, const int64_t* ev_off, const int* wave_slot, int U,
                     const unsigned long long* amask, const unsigned long long* smask, int* idx_all,
                     int* vlen_all, int* bad_all, int* err, const Dims& D, cudaStream_t s);

@@ -213,3 +213,51 @@ def test_cache_store_hits_staleness_and_lru():
     cl.cache_release(h1d)
     assert cl.cache_stats()["pinned"] == 0
     cl.stream_status()
+
+
+@pytest.mark.parametrize("rel_bias", [0, 1])
+def test_cache_incremental_append_bitwise(rel_bias):
+    # the log grows by appending; only the blocks whose strategy matches an
+    # appended event are recomputed, and the scores equal a full re-encode
+    import torch
+    cfg = synth.preset("medium", rel_bias=rel_bias)      # N_b = 4: {play_full}, {like}, {share, comment}, {click}
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 12, B=1)
+    cl = make_gpu(cfg, w, 1, kv_users=3)
+    item, action, scenario, ts = (np.array(a) for a in batch.user_events(0))
+    r = int(batch.r[0])
+    cand = torch.from_numpy(batch.user_cands(0).copy()).cuda()
+    dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    n1 = len(item)
+    n0 = n1 - 12
+    action = action.copy()
+    action[n0:] = synth.A_SKIP                            # matches no strategy
+
+    def fresh(n, act):
+        h = cl.encode_user(dv(item[:n]), dv(act[:n]), dv(scenario[:n]), dv(ts[:n]), r)
+        s = cl.score_items(h, cand).cpu().numpy()
+        cl.release(h)
+        return s
+
+    h, res = cl.cache_acquire(7, r, 1000, dv(item[:n0]), dv(action[:n0]), dv(scenario[:n0]), dv(ts[:n0]))
+    assert res == "encoded"
+    cl.cache_release(h)
+    steps = [(n0 + 4, None, 0),                      # only skips appended: no block changes
+             (n0 + 8, (n0 + 5, synth.A_LIKE), 1),    # one 'like': block 1 only
+             (n1, (n1 - 1, synth.A_PLAY), 1)]        # one 'play_full': block 0 (full -> its window slides)
+    dig = 1000
+    for n, change, expect in steps:
+        if change:
+            action[change[0]] = change[1]
+        h, res, nb = cl.cache_append(7, r, dig, dig + 1, dv(item[:n]), dv(action[:n]), dv(scenario[:n]),
+                                     dv(ts[:n]))
+        dig += 1
+        assert res == "appended" and nb == expect, (res, nb)
+        got = cl.score_items(h, cand).cpu().numpy()
+        cl.cache_release(h)
+        assert np.array_equal(got, fresh(n, action)), n
+    # a digest that is not the cached one falls back to a full build
+    h, res, nb = cl.cache_append(7, r, 999, 5000, dv(item), dv(action), dv(scenario), dv(ts))
+    assert res == "encoded" and nb == cfg.N_b
+    cl.cache_release(h)
+    cl.stream_status()
