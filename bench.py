@@ -436,6 +436,20 @@ def main():
                 tl.append((time.perf_counter() - t0) * 1e3)
         lat = {"p50": float(np.percentile(tl, 50)), "p99": float(np.percentile(tl, 99)), "requests": len(tl),
                "mode": "single GPU per request (B=1, M candidates), climber_rank_host: H2D + one CUDA graph (encode + score, captured once per shape) + D2H"}
+        # where one request's device time goes: the same request eagerly with the
+        # per-launch profiler on (CUDA events around every launch; graphs are off
+        # while profiling), summed per kernel class, ms
+        u = one[0]
+        ud = [dev(a) for a in (u.item, u.action, u.scenario, u.ts, u.cand)]
+        cl.profile(True)
+        hs1 = cl.encode_users(u.ev_offsets, ud[0], ud[1], ud[2], ud[3], u.r)
+        cl.score_batched(hs1, u.cand_offsets, ud[4])
+        torch.cuda.synchronize()
+        cl.release(hs1)
+        cl.profile(False)
+        br = cl.profile_read()
+        lat["device_ms_by_class"] = {k: round(v["ms"], 4) for k, v in br.items() if v["launches"]}
+        lat["device_ms_total"] = round(sum(v["ms"] for v in br.values()), 4)
     elif args.latency_requests > 0:
         # candidate sharding: owner encodes, K/V slab broadcast over
         # the NCCL group, every rank scores floor(m G / M) == rank, scores gathered
