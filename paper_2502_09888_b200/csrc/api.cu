@@ -69,7 +69,7 @@ struct climber_ctx_s {
   void *e_item, *e_act, *e_scn;
   float *g1, *g2, *tau, *fg1, *fg2, *tau_f, *b_se1, *b_se2, *w_head;
   float *bpos = nullptr, *btime = nullptr, *cbias = nullptr;  // relative bias (rel_bias = 1)
-  long long *hts = nullptr, *treq = nullptr;
+  int* hage = nullptr;
   void *w_qkv, *w_o, *w1, *w2, *fw_qkv, *fw_o, *fw1, *fw2, *w_se1, *w_se2;
   float b_head;
   unsigned long long *amask, *smask;
@@ -181,7 +181,7 @@ static bool dims_from(const climber_config* cfg, Dims* D, std::string* why) {
   D->F = cfg->ffn_mult * cfg->d; D->Dse = cfg->n_blocks * cfg->d; D->Hse = D->Dse / cfg->se_reduction;
   D->V = cfg->vocab; D->A = cfg->n_actions; D->R = cfg->n_scenarios; D->Mmax = cfg->max_candidates;
   D->causal = cfg->hist_causal ? 1 : 0; D->ppb = (cfg->n_k + PAGE - 1) / PAGE; D->eps = cfg->rms_eps;
-  D->bpos = D->btime = nullptr; D->hts = D->treq = nullptr; D->cbias = nullptr;
+  D->bpos = D->btime = nullptr; D->hage = nullptr; D->cbias = nullptr;
   if (cfg->rel_bias != 0 && cfg->rel_bias != 1) { *why = "rel_bias must be 0 or 1"; return false; }
   if (cfg->rel_bias && cfg->dtype == CLIMBER_BF16 && !((dh == 32 || dh == 64) && cfg->n_k % 128 == 0)) {
     *why = "rel_bias on the bf16 path needs d_h in {32, 64} and n_k % 128 == 0 (tcgen05 attention)";
@@ -233,9 +233,8 @@ static void carve(climber_ctx_s* c, Carver& cv) {
   cv.take(c->idx_all, S * Nb * D.nk * 4);
   cv.take(c->bad_all, S * 4);
   cv.take(c->err, 256);
-  if (c->cfg.rel_bias) {  // per handle: history token times, request time, candidate bias rows
-    cv.take(c->hts, S * Nb * D.nk * 8);
-    cv.take(c->treq, S * 8);
+  if (c->cfg.rel_bias) {  // per handle: history token ages at the request time, candidate bias rows
+    cv.take(c->hage, S * Nb * D.nk * 4);
     cv.take(c->cbias, S * L * Nb * D.h * D.nk * 4);
   }
   // per-call metadata
@@ -423,8 +422,7 @@ extern "C" climber_status climber_create(const climber_config* cfg, const climbe
       up.put(c->btime, w->b_time, 1, 1, (size_t)L * Nb * D.R * D.h * NB_TIME, false, false);
       c->D.bpos = c->bpos;
       c->D.btime = c->btime;
-      c->D.hts = c->hts;
-      c->D.treq = c->treq;
+      c->D.hage = c->hage;
       c->D.cbias = c->cbias;
     }
     if (up.st != CLIMBER_OK) {

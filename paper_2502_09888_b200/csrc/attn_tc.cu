@@ -333,18 +333,21 @@ __global__ void __launch_bounds__(THREADS, 2)
     // head)'s tables staged in smem; history token times / candidate-row bias
     float* sbp = reinterpret_cast<float*>(smem + Ly::BAR_OFF + 512);
     float* sbt = sbp + NB_POS;
-    const long long* ht = nullptr;
+    float* lut = sbt + 16;  // causal history: lut[bp * 7 + bt] = b_pos[bp] + b_time[bt], bp < 64, bt < 7
+    const int* hag = nullptr;
     const float* cbr = nullptr;
-    long long t_time = 0;
+    int t_age = 0;
     if constexpr (BIAS) {
       const long long br = bias_row(D, a.l, kblk, r, head);
       const int i = ew * 32 + lane;
       sbp[i] = D.bpos[br * NB_POS + i];
       if (i < NB_TIME) sbt[i] = D.btime[br * NB_TIME + i];
+      if (MODE == MODE_HIST && D.causal)
+        for (int e = i; e < 64 * 7; e += 128) lut[e] = D.bpos[br * NB_POS + e / 7] + D.btime[br * NB_TIME + e % 7];
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      ht = D.hts + ((long long)slot * D.Nb + kblk) * D.nk;
+      hag = D.hage + ((long long)slot * D.Nb + kblk) * D.nk;
       cbr = D.cbias + ((((long long)slot * D.L + a.l) * D.Nb + kblk) * D.h + head) * D.nk;
-      if (MODE == MODE_HIST && t_row < v) t_time = ht[t_row];
+      if (MODE == MODE_HIST && t_row < v) t_age = hag[t_row];
     }
     float m_used, l;
     if (MODE == MODE_SUMI) {
@@ -415,14 +418,31 @@ __global__ void __launch_bounds__(THREADS, 2)
             sr[i + 3] = __float_as_uint(__uint_as_float(sr[i + 3]) + b.w);
           }
         } else {
-          const longlong2* h2 = reinterpret_cast<const longlong2*>(ht + key0);
+          // t_row - t_key = age_key - age_row; key ages 4 per 16-byte load
+          const int4* a4 = reinterpret_cast<const int4*>(hag + key0);
+          if (D.causal) {  // offsets >= 0 and time deltas >= 0 on every visible key: one 2-D lookup
 #pragma unroll
-          for (int i = 0; i < KEYS; i += 2) {
-            const longlong2 tk = h2[i >> 1];
-            const float b0 = sbp[bucket_pos(t_row - (key0 + i))] + sbt[bucket_time(t_time - tk.x)];
-            const float b1 = sbp[bucket_pos(t_row - (key0 + i + 1))] + sbt[bucket_time(t_time - tk.y)];
-            sr[i] = __float_as_uint(__uint_as_float(sr[i]) + b0);
-            sr[i + 1] = __float_as_uint(__uint_as_float(sr[i + 1]) + b1);
+            for (int i = 0; i < KEYS; i += 4) {
+              const int4 ka = a4[i >> 2];
+              const int kv4[4] = {ka.x, ka.y, ka.z, ka.w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int bp = bucket_pos(t_row - (key0 + i + q)) & 63;   // masked keys (offset < 0) stay in range
+                const int bt = bucket_time32(kv4[q] - t_age) % 7;
+                sr[i + q] = __float_as_uint(__uint_as_float(sr[i + q]) + lut[bp * 7 + bt]);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < KEYS; i += 4) {
+              const int4 ka = a4[i >> 2];
+              const int kv4[4] = {ka.x, ka.y, ka.z, ka.w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float b = sbp[bucket_pos(t_row - (key0 + i + q))] + sbt[bucket_time32(kv4[q] - t_age)];
+                sr[i + q] = __float_as_uint(__uint_as_float(sr[i + q]) + b);
+              }
+            }
           }
         }
       }
@@ -1080,7 +1100,7 @@ template <int DH, int MODE, int PE8>
 static void launch_pe(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s) {
   // CLIMBER_ATTN_1CTA=1 (measurement knob): request enough smem for 1 CTA/SM
   static const int smem = getenv("CLIMBER_ATTN_1CTA") ? 150 * 1024 : Lay<DH>::TOTAL;
-  constexpr int smem_b = Lay<DH>::TOTAL + 1024;  // + the staged relative-bias tables
+  constexpr int smem_b = Lay<DH>::TOTAL + 3072;  // + the staged relative-bias tables and 2-D lookup
   static bool attr = false;
   static const bool es = [] { const char* e = getenv("CLIMBER_ATTN_EARLY_S"); return !(e && atoi(e) == 0); }();
   if (!attr) {

@@ -14,16 +14,16 @@ typedef __nv_bfloat16 bf16;
 // Model dimensions, passed by value to kernels.  The relative-bias pointers
 // are ctx-lifetime device arrays (nullptr when rel_bias = 0, Eq. 3
 // f_b = 0): tables b_pos [L][Nb][R][h][NB_POS], b_time [L][Nb][R][h][NB_TIME];
-// hts [slot][Nb][nk] the event time of every extracted history token, treq
-// [slot] the request time; cbias [slot][L][Nb][h][nk] the candidate-row bias
-// over the history keys (the same for every candidate of a request).
+// hage [slot][Nb][nk] the age of every extracted history token at the request
+// time, t_req - t_j in seconds (int32, saturating at 2^31 - 1 s ~ 68 years;
+// t_i - t_j = age_j - age_i); cbias [slot][L][Nb][h][nk] the candidate-row
+// bias over the history keys (the same for every candidate of a request).
 struct Dims {
   int d, h, dh, L, Nb, nk, F, Dse, Hse, V, A, R, Mmax, causal, ppb;
   float eps;
   const float* bpos;
   const float* btime;
-  long long* hts;
-  long long* treq;
+  int* hage;
   float* cbias;
 };
 
@@ -50,6 +50,12 @@ __host__ __device__ __forceinline__ int bucket_pos(int delta) {
 __host__ __device__ __forceinline__ int bucket_time(long long dt) {
   const long long a = dt < 0 ? -dt : dt;
   const int b = a == 0 ? 0 : a < 60 ? 1 : a < 3600 ? 2 : a < 86400 ? 3 : a < 604800 ? 4 : a < 2592000 ? 5 : 6;
+  return b + (dt < 0 ? 7 : 0);
+}
+// the same buckets for a 32-bit delta (branch-free compares)
+__host__ __device__ __forceinline__ int bucket_time32(int dt) {
+  const int a = dt < 0 ? -dt : dt;
+  const int b = (a > 0) + (a >= 60) + (a >= 3600) + (a >= 86400) + (a >= 604800) + (a >= 2592000);
   return b + (dt < 0 ? 7 : 0);
 }
 // the (layer, block, scenario, head) row of a bias table

@@ -58,14 +58,16 @@ __global__ void k_extract(const int32_t* __restrict__ item, const uint8_t* __res
     int v = min(cnt, D.nk);
     for (int p = lane; p < D.nk - v; p += 32) idx[p] = -1;
     if (lane == 0) vlen_all[(long long)slot * D.Nb + k] = v;
-    if (D.hts) {  // relative bias: the event time of history token p (chronological)
-      __syncwarp();
-      long long* hts = D.hts + ((long long)slot * D.Nb + k) * D.nk;
-      for (int p = lane; p < v; p += 32) hts[p] = ts[s + idx[D.nk - v + p]];
+    if (D.hage && v > 0) {  // relative bias: age of history token p at the request time (G6e:
+      __syncwarp();  // the request time is the last event's timestamp)
+      int* hage = D.hage + ((long long)slot * D.Nb + k) * D.nk;
+      const long long t_req = ts[e - 1];  // v > 0 implies e > s
+      for (int p = lane; p < v; p += 32) {
+        const long long age = t_req - ts[s + idx[D.nk - v + p]];
+        hage[p] = age < 0 ? 0 : (age > 2147483647LL ? 2147483647 : (int)age);
+      }
     }
   }
-  // G6e: the request (= candidate) time is the last event's timestamp
-  if (D.treq && threadIdx.x == 0) D.treq[slot] = e > s ? ts[e - 1] : 0;
 }
 
 // Relative bias of the candidate rows (Eq. 3 f_b, NEXT-1): a candidate sits at
@@ -79,14 +81,13 @@ __global__ void k_cand_bias(const int* __restrict__ wave_slot, const int* __rest
   const int head = blockIdx.y % D.h, k = (blockIdx.y / D.h) % D.Nb, l = blockIdx.y / (D.h * D.Nb);
   const int slot = wave_slot[u], r = wave_r[u];
   const int v = vlen_all[(long long)slot * D.Nb + k];
-  const long long tq = D.treq[slot];
   const long long row = bias_row(D, l, k, r, head);
   const float* bp = D.bpos + row * NB_POS;
   const float* bt = D.btime + row * NB_TIME;
-  const long long* ht = D.hts + ((long long)slot * D.Nb + k) * D.nk;
+  const int* age = D.hage + ((long long)slot * D.Nb + k) * D.nk;
   float* out = D.cbias + ((((long long)slot * D.L + l) * D.Nb + k) * D.h + head) * D.nk;
-  for (int j = threadIdx.x; j < D.nk; j += blockDim.x)
-    out[j] = j < v ? bp[bucket_pos(v - j)] + bt[bucket_time(tq - ht[j])] : 0.f;
+  for (int j = threadIdx.x; j < D.nk; j += blockDim.x)   // t_req - t_j = age_j
+    out[j] = j < v ? bp[bucket_pos(v - j)] + bt[bucket_time32(age[j])] : 0.f;
 }
 
 // Block-parallel fusion input (NEXT-2): from the gathered fp32 block outputs
@@ -504,10 +505,10 @@ __global__ void __launch_bounds__(128) k_attn_hist(const T* __restrict__ Q, cons
         const long long br = bias_row(D, l, k, r, head);
         const float* bp = D.bpos + br * NB_POS;
         const float* bt = D.btime + br * NB_TIME;
-        const long long* ht = D.hts + ((long long)slot * D.Nb + k) * D.nk;
-        const long long tt = ht[t];
+        const int* age = D.hage + ((long long)slot * D.Nb + k) * D.nk;
+        const int at = age[t];   // t_t - t_j = age_j - age_t
         online_chunk_b<DH>(Ks, Vs, q, o, m, lsum, jmax, [&](int j) {
-          return sc * (bp[bucket_pos(t - (t0 + j))] + bt[bucket_time(tt - ht[t0 + j])]);
+          return sc * (bp[bucket_pos(t - (t0 + j))] + bt[bucket_time32(age[t0 + j] - at)]);
         });
       } else {
         online_chunk<DH>(Ks, Vs, q, o, m, lsum, jmax);
