@@ -135,6 +135,11 @@ struct climber_ctx_s {
   unsigned long long store_tick = 0;
   long long st_hits = 0, st_miss = 0, st_evict = 0;
   cudaStream_t g_stream = nullptr;          // capture stream
+  // latency graph: score layer l starts its attention as soon as the encode
+  // wrote layer l's K/V (encode and score on two captured streams)
+  cudaStream_t g_stream2 = nullptr;
+  std::vector<cudaEvent_t> ov_evt;          // [L + 2]: per-layer K/V ready, fork, join
+  bool ov_record = false, ov_wait = false;
   bool graphs = true;
 };
 
@@ -466,6 +471,8 @@ extern "C" climber_status climber_destroy(climber_ctx_t c) {
   if (c->io) cudaFree(c->io);
   if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
   if (c->g_stream) cudaStreamDestroy(c->g_stream);
+  if (c->g_stream2) cudaStreamDestroy(c->g_stream2);
+  for (cudaEvent_t ev : c->ov_evt) cudaEventDestroy(ev);
   if (c->d_flags) cudaFree(c->d_flags);
   cudaEventDestroy(c->stage_evt);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -977,6 +984,7 @@ static void encode_wave_grouped(climber_ctx_s* c, const EventsDev& ev, int u0, i
     if (l < D.L - 1) {
       e.col_off = 0;
       gemm_g(c, CLIMBER_K_GEMM_QKV, gXb, d, rows * d, Wqkv, d, Lk * 3 * d * d, rows, 3 * D.d, D.d, nbk, e, s);
+      if (c->ov_record) cudaEventRecord(c->ov_evt[l], s);  // layer l's K/V pages written
       {
         Prof p(c, CLIMBER_K_ATTN_HIST, s, 4.0 * U * causal_pairs * d * nbk, (double)rows * d * 2 * 4 * nbk);
         launch_attn_hist_tc(gQb, wslot, wr, U, (const bf16*)c->pool, c->n_pages * 2 * PAGE, c->ptab, c->vlen_all,
@@ -996,6 +1004,7 @@ static void encode_wave_grouped(climber_ctx_s* c, const EventsDev& ev, int u0, i
       e.col_off = D.d;  // last layer: only K/V of the history are ever read
       gemm_g(c, CLIMBER_K_GEMM_QKV, gXb, d, rows * d, Wqkv + d * d, d, Lk * 3 * d * d, rows, 2 * D.d, D.d, nbk, e,
              s);
+      if (c->ov_record) cudaEventRecord(c->ov_evt[l], s);
     }
   }
 }
@@ -1029,6 +1038,7 @@ static void score_blocks_grouped(climber_ctx_s* c, const int32_t* items, const i
     eq.out_bs = P * 3 * d; eq.rs_bs = pld;
     gemm_stage(c, 1, CLIMBER_K_GEMM_QKV, gCb, ldC, d, (const bf16*)c->w_qkv + (wk + l) * 3 * d * d, d, Lk * 3 * d * d,
                P, 3 * D.d, D.d, nbk, eq, s);
+    if (c->ov_wait) cudaStreamWaitEvent(s, c->ov_evt[l], 0);  // the user's layer-l K/V
     {
       Prof p(c, CLIMBER_K_ATTN_SUMI, s, 4.0 * P * (D.nk + 1) * d * nbk,
              ((double)P * d * 2 * 4 + (double)U * D.nk * d * 4) * nbk);
@@ -1540,8 +1550,42 @@ static climber_status rank_one_graph(climber_ctx_s* c, long long E, long long P,
     // stream, which cannot capture); nothing executes during capture
     cudaError_t e = cudaSuccess;
     if (!c->g_stream) e = cudaStreamCreateWithFlags(&c->g_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess && !c->g_stream2) e = cudaStreamCreateWithFlags(&c->g_stream2, cudaStreamNonBlocking);
+    const int L = c->D.L;
+    while (e == cudaSuccess && (int)c->ov_evt.size() < L + 2) {
+      cudaEvent_t ev;
+      e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      if (e == cudaSuccess) c->ov_evt.push_back(ev);
+    }
+    // the score runs in its own scratch rows (after the encode's) so the two
+    // streams never share a buffer; without room, one stream
+    const long long enc_rows = (long long)c->D.nk * c->D.Nb;
+    const bool overlap = enc_rows + P * c->D.Nb <= c->rows_cap && !getenv("CLIMBER_LATENCY_SERIAL");
     if (e == cudaSuccess) e = cudaStreamBeginCapture(c->g_stream, cudaStreamCaptureModeThreadLocal);
-    if (e == cudaSuccess) {
+    if (e == cudaSuccess && overlap) {
+      const long long d = c->D.d;
+      float* X0 = c->X;
+      void *Xb0 = c->Xb, *QKV0 = c->QKV, *O0 = c->O, *Fh0 = c->Fh;
+      float* part0 = c->part;
+      cudaEventRecord(c->ov_evt[L], c->g_stream);  // fork
+      cudaStreamWaitEvent(c->g_stream2, c->ov_evt[L], 0);
+      c->ov_record = true;
+      encode_wave_grouped(c, evd, 0, 1, E, c->g_stream);
+      c->ov_record = false;
+      c->X = X0 + enc_rows * d;
+      c->Xb = (bf16*)Xb0 + enc_rows * d;
+      c->QKV = (bf16*)QKV0 + enc_rows * 3 * d;
+      c->O = (bf16*)O0 + enc_rows * d;
+      c->Fh = (bf16*)Fh0 + enc_rows * c->D.F;
+      c->part = part0 + enc_rows * c->pld;
+      c->ov_wait = true;
+      score_wave_grouped(c, d_items, c->d_cand_off, 0, 1, P, (int)P, d_scores, c->g_stream2);
+      c->ov_wait = false;
+      c->X = X0; c->Xb = Xb0; c->QKV = QKV0; c->O = O0; c->Fh = Fh0; c->part = part0;
+      cudaEventRecord(c->ov_evt[L + 1], c->g_stream2);  // join
+      cudaStreamWaitEvent(c->g_stream, c->ov_evt[L + 1], 0);
+      e = cudaStreamEndCapture(c->g_stream, &graph);
+    } else if (e == cudaSuccess) {
       encode_wave_grouped(c, evd, 0, 1, E, c->g_stream);
       score_wave_grouped(c, d_items, c->d_cand_off, 0, 1, P, (int)P, d_scores, c->g_stream);
       e = cudaStreamEndCapture(c->g_stream, &graph);
