@@ -533,10 +533,24 @@ void launch_gemm_tc_batched(const bf16* A, long long lda, long long a_bs, const 
     const char* c = getenv("CLIMBER_GEMM_CG");
     cg = c ? atoi(c) : 2;
   }
-  // small launches (one request in latency mode): 256-row pair tiles leave
-  // most SMs idle, so switch to 128 x 128 single-CTA tiles (4x the tiles)
+  // small launches: 128 x 128 single-CTA tiles (4x the tiles) below
+  // CLIMBER_GEMM_SMALL_WAVES (2) waves of pair CTAs and below
+  // CLIMBER_GEMM_SMALL_GFLOP (1.5) GFLOP per launch.  Measured on one request
+  // (latency graph with encode/score overlap): medium / small p50 0.54 / 0.44 ms
+  // with small tiles vs 0.66 / 0.49 with pairs (launches <= 1.1 GF); at large
+  // (launches >= 2.1 GF) pairs everywhere 1.51 ms vs 1.56-1.61 with small tiles
   const long long pair_ctas = ((M + 255) / 256) * (N / (N % 256 == 0 ? 256 : 128)) * batch * 2;
-  if (pair_ctas < 2LL * tc::num_sms()) {
+  // CLIMBER_GEMM_SMALL_WAVES (measurement knob): the threshold in waves of pair CTAs
+  static const long long small_waves = [] {
+    const char* e = getenv("CLIMBER_GEMM_SMALL_WAVES");
+    return e ? atoll(e) : 2LL;
+  }();
+  static const double small_gflop = [] {
+    const char* e = getenv("CLIMBER_GEMM_SMALL_GFLOP");
+    return e ? atof(e) : 1.5;
+  }();
+  const double gflop = 2.0 * (double)M * N * K * batch * 1e-9;
+  if (pair_ctas < small_waves * tc::num_sms() && gflop < small_gflop) {
     if (e.kind == EPI_RESID_NORM) {
       tc::launch<128, 4, 4, 2, 1>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
     } else {

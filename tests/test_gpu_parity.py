@@ -63,10 +63,23 @@ def test_large_bf16():
 
 @pytest.mark.parametrize("name", ["large", "medium"])
 def test_single_request_bf16(name):
-    # latency mode (B = 1): launches below two waves of CTA pairs take the
-    # 128 x 128 single-CTA GEMM tiles, whose RESID_NORM epilogue must write
-    # the same per-128-column norm partials as the 256-wide pair tiles
+    # latency mode (B = 1): small launches
     _check_cfg(synth.preset(name), B=1, users=[0])
+
+
+def test_single_request_small_gemm_tiles():
+    # the 128 x 128 single-CTA GEMM tiles on every small launch (knobs read once
+    # per process): their RESID_NORM epilogue must write the same per-128-column
+    # norm partials as the 256-wide pair tiles
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path[:0] = [%r, %r]; import synth, test_gpu_parity as t; "
+            "t._check_cfg(synth.preset('medium'), B=1, users=[0]); t._check_cfg(synth.preset('large'), B=1, users=[0])"
+            % (root, os.path.join(root, "tests")))
+    env = dict(os.environ, CLIMBER_GEMM_SMALL_WAVES="4", CLIMBER_GEMM_SMALL_GFLOP="1e9")
+    subprocess.run([sys.executable, "-c", code], env=env, check=True, cwd=root, timeout=600)
 
 
 def test_sweep_corner_bf16():
