@@ -446,8 +446,6 @@ __global__ void __launch_bounds__(THREADS, 2)
           }
         }
       }
-      const int tph = -1;
-      if (tph >= 0) tr[tph] = clock64();
       float mx8[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
@@ -485,7 +483,6 @@ __global__ void __launch_bounds__(THREADS, 2)
         }
       }
       // pass 2: P = exp2(s sc - m) as packed bf16, written over S_j in TMEM
-      if (tph >= 0) tr[tph + 1] = clock64();
       const float nb = (m_used == -INFINITY) ? 0.f : -m_used;
       float ls8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       uint32_t pk[KEYS / 2];
@@ -518,11 +515,9 @@ __global__ void __launch_bounds__(THREADS, 2)
           pk[i >> 1] = *reinterpret_cast<uint32_t*>(&pp);
         }
       }
-      if (tph >= 0) tr[tph + 2] = clock64();
       tmem_st16u(tSj, pk);
       tmem_st16u(tSj + 16, pk + 16);
       tmem_st_wait();
-      if (tph >= 0) tr[tph + 3] = clock64();
       l += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
       fence_before();
       mbar_arrive(&p_full[j % NSB]);
@@ -681,7 +676,7 @@ __device__ __forceinline__ bool pt_decode(const PArgs& pa, long long it, PDesc& 
   return live;
 }
 
-template <int DH, int MODE, int EARLY_S>
+template <int DH, int MODE>
 __global__ void __launch_bounds__(PT_THREADS, 1)
     k_attn_pt(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, PArgs pa) {
   using Ly = PLay<DH>;
@@ -1126,23 +1121,13 @@ static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a,
   }
 }
 
-// CLIMBER_ATTN_EARLY_S=0 interleaves S(j+2) with PV(j) after P(j) (measurement knob)
-static bool early_s() {
-  static bool v = [] {
-    const char* e = getenv("CLIMBER_ATTN_EARLY_S");
-    return !(e && atoi(e) == 0);
-  }();
-  return v;
-}
-
 template <int DH, int MODE>
 static void launch_pt(const CUtensorMap& mq, const CUtensorMap& mkv, const PArgs& pa, cudaStream_t s) {
   constexpr int smem = PLay<DH>::TOTAL;
   static bool attr = false;
   static int n_sm = 148;
   if (!attr) {
-    cudaFuncSetAttribute(k_attn_pt<DH, MODE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_attn_pt<DH, MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_attn_pt<DH, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
@@ -1150,12 +1135,11 @@ static void launch_pt(const CUtensorMap& mq, const CUtensorMap& mkv, const PArgs
   }
   if (pa.n_items <= 0) return;
   const int grid = (int)(pa.n_items < n_sm ? pa.n_items : n_sm);
-  if (early_s()) k_attn_pt<DH, MODE, 1><<<grid, PT_THREADS, smem, s>>>(mq, mkv, pa);
-  else k_attn_pt<DH, MODE, 0><<<grid, PT_THREADS, smem, s>>>(mq, mkv, pa);
+  k_attn_pt<DH, MODE><<<grid, PT_THREADS, smem, s>>>(mq, mkv, pa);
 }
 
-// CLIMBER_ATTN_KERNEL=2 selects the persistent two-tile kernel (measured
-// ~16% slower than two one-tile CTAs per SM at `large`; kept as a knob)
+// CLIMBER_ATTN_KERNEL=2 selects the persistent two-tile kernel (measured 2%
+// slower than two one-tile CTAs per SM at `large`; kept as a knob)
 static bool use_pt() {
   static bool v = [] {
     const char* e = getenv("CLIMBER_ATTN_KERNEL");
