@@ -14,7 +14,7 @@ $(OUT)/%.o: $(SRC)/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(OUT)/libclimber.so: $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -ldl
 
 clean:
 	rm -rf $(OUT)

@@ -164,9 +164,11 @@ size_t climber_arena_bytes(const climber_config* cfg);
 
 /* Create a context.  `arena` is a DEVICE buffer of >= climber_arena_bytes(cfg)
  * bytes, 256-byte aligned, borrowed for the ctx's lifetime (e.g. a torch
- * tensor).  `strategies` is a host array of n_blocks entries.  Multi-GPU
- * candidate sharding (rank/world/nccl_uid) is NEXT: world must be 1 and
- * nccl_uid NULL in this build, else CLIMBER_E_UNSUPPORTED.  Synchronous. */
+ * tensor).  `strategies` is a host array of n_blocks entries.  Multi-GPU:
+ * world > 1 needs `nccl_uid` (128 bytes from climber_nccl_unique_id on one
+ * rank); every rank then calls climber_create concurrently (collective) and
+ * the ctx holds an NCCL communicator for climber_kv_broadcast.  With world ==
+ * 1, nccl_uid may be NULL (no communicator).  Synchronous. */
 climber_status climber_create(const climber_config* cfg, const climber_strategy* strategies,
                               const climber_weights* weights, void* arena, size_t arena_bytes,
                               int32_t rank, int32_t world, const void* nccl_uid,
@@ -340,10 +342,20 @@ climber_status climber_kv_export(climber_ctx_t ctx, climber_kv_t kv, void* slab,
 climber_status climber_kv_import(climber_ctx_t ctx, const void* slab, int32_t scenario_r,
                                  climber_stream_t stream, climber_kv_t* out);
 
-/* In-library NCCL replication of a handle — not built: use kv_export + the
- * caller's collective + kv_import.  Returns CLIMBER_E_UNSUPPORTED. */
+/* In-library NCCL replication of one user's K/V: collective
+ * over the ctx's communicator (climber_create with world > 1 and an NCCL
+ * unique id).  On `root`, *kv is the handle to replicate (unchanged); on every
+ * other rank a new handle with identical pages is allocated in its pool and
+ * returned in *kv.  Root exports the pages into one slab, one ncclBroadcast
+ * (NVLink / NVSwitch) replicates it, the receivers import it; receivers
+ * synchronise `stream` once (to read the handle's scenario from the slab
+ * header).  A world-1 ctx without a communicator returns OK unchanged. */
 climber_status climber_kv_broadcast(climber_ctx_t ctx, climber_kv_t* kv, int32_t root,
                                     climber_stream_t stream);
+
+/* An NCCL unique id (128 bytes into `out`) for climber_create's nccl_uid:
+ * rank 0 calls it and shares the bytes with the other ranks. */
+climber_status climber_nccl_unique_id(void* out);
 
 /* Synchronise `stream` and report the first device-side error recorded since
  * the last call (then clear it): OK, E_OUT_OF_RANGE, E_UNSORTED, E_CUDA. */

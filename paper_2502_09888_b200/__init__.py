@@ -3,4 +3,4 @@
 The hot path lives in libclimber.so (hand-written sm_100a CUDA behind the C
 ABI of include/climber.h); ``climber`` is its thin ctypes binding.
 """
-from .climber import Climber, ClimberError, ModelConfig, lib, LIB_PATH  # noqa: F401
+from .climber import Climber, ClimberError, ModelConfig, lib, LIB_PATH, nccl_unique_id  # noqa: F401

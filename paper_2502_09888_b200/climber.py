@@ -96,6 +96,7 @@ def lib() -> C.CDLL:
             "climber_cache_acquire": (I32, [VP, C.c_uint64, I32, C.c_uint64, P, I64, VP, P, P]),
             "climber_cache_release": (I32, [VP, VP]),
             "climber_cache_append": (I32, [VP, C.c_uint64, I32, C.c_uint64, C.c_uint64, P, I64, VP, P, P, P]),
+            "climber_nccl_unique_id": (I32, [P]),
             "climber_cache_stats": (I32, [VP, P]),
         }
         for name, (res, args) in sig.items():
@@ -114,7 +115,7 @@ EXPORTED_SYMBOLS = ("climber_arena_bytes", "climber_create", "climber_destroy", 
                     "climber_kv_slab_bytes", "climber_kv_export", "climber_kv_import",
                     "climber_encode_users_blocks", "climber_score_blocks", "climber_fuse_scores", "climber_forward",
                     "climber_cache_acquire", "climber_cache_release", "climber_cache_stats",
-                    "climber_cache_append")
+                    "climber_cache_append", "climber_nccl_unique_id")
 
 KERNEL_CLASSES = ("extract", "embed", "rmsnorm", "gemm_qkv", "gemm_o", "gemm_ffn_up", "gemm_ffn_down", "gemm_se",
                   "attn_hist", "attn_sumi", "attn_fusion", "head", "other")
@@ -137,6 +138,13 @@ def debug_gemm(A, B, D, use_tc: bool = True, stream=None, epi: int = 0):
         N //= 2
     _check(lib().climber_debug_gemm(C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), C.c_void_p(D.data_ptr()),
                                     M, N, K, int(use_tc), int(epi), C.c_void_p(s.cuda_stream)))
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for Climber(..., rank, world, nccl_uid)."""
+    buf = (C.c_char * 128)()
+    _check(lib().climber_nccl_unique_id(buf))
+    return bytes(buf)
 
 
 def _ptr(a: np.ndarray):
@@ -179,7 +187,7 @@ class Climber:
 
     def __init__(self, cfg: ModelConfig, weights, strategies: Sequence[tuple], *, max_users: int = 64,
                  max_wave_users: int = 64, max_wave_pairs: Optional[int] = None, kv_users: Optional[int] = None,
-                 device=None):
+                 device=None, rank: int = 0, world: int = 1, nccl_uid: Optional[bytes] = None):
         import torch
         self.torch = torch
         self.cfg = cfg
@@ -222,8 +230,9 @@ class Climber:
                 setattr(w, n, a.ctypes.data)
         st = (_Strategy * cfg.N_b)(*[_Strategy(int(a), int(s)) for a, s in strategies])
         h = C.c_void_p()
-        _check(L.climber_create(C.byref(c), st, C.byref(w), C.c_void_p(self.arena.data_ptr()), nbytes, 0, 1, None,
-                                C.byref(h)))
+        uid = C.create_string_buffer(nccl_uid, 128) if nccl_uid is not None else None
+        _check(L.climber_create(C.byref(c), st, C.byref(w), C.c_void_p(self.arena.data_ptr()), nbytes, int(rank),
+                                int(world), uid, C.byref(h)))
         self._keep = []
         self.h = h
 
@@ -398,6 +407,12 @@ class Climber:
             slab = self.torch.empty(self.slab_bytes, dtype=self.torch.uint8, device=self.arena.device)
         _check(lib().climber_kv_export(self.h, C.c_void_p(handle), C.c_void_p(slab.data_ptr()), self._stream(stream)))
         return slab
+
+    def kv_broadcast(self, handle: Optional[int], root: int = 0, stream=None) -> int:
+        """Collective: replicate root's handle to every rank (NCCL inside the library)."""
+        kv = C.c_void_p(handle or 0)
+        _check(lib().climber_kv_broadcast(self.h, C.byref(kv), int(root), self._stream(stream)))
+        return kv.value
 
     def kv_import(self, slab, r: int, stream=None) -> int:
         out = C.c_void_p()

@@ -10,6 +10,9 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "../../include/climber.h"
 #include "kernels.cuh"
 
@@ -19,6 +22,33 @@ using namespace climber;
 // errors
 // ---------------------------------------------------------------------------
 static thread_local std::string g_last_error;
+
+// NCCL, resolved at run time from the process's libnccl.so.2 (the one torch
+// already loaded, else the system one): only multi-GPU contexts need it.
+struct NcclApi {
+  decltype(&ncclGetUniqueId) get_uid = nullptr;
+  decltype(&ncclCommInitRank) init = nullptr;
+  decltype(&ncclBroadcast) bcast = nullptr;
+  decltype(&ncclCommDestroy) destroy = nullptr;
+  decltype(&ncclGetErrorString) err = nullptr;
+  bool ok = false;
+};
+static NcclApi& nccl_api() {
+  static NcclApi a = [] {
+    NcclApi x;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return x;
+    x.get_uid = (decltype(x.get_uid))dlsym(h, "ncclGetUniqueId");
+    x.init = (decltype(x.init))dlsym(h, "ncclCommInitRank");
+    x.bcast = (decltype(x.bcast))dlsym(h, "ncclBroadcast");
+    x.destroy = (decltype(x.destroy))dlsym(h, "ncclCommDestroy");
+    x.err = (decltype(x.err))dlsym(h, "ncclGetErrorString");
+    x.ok = x.get_uid && x.init && x.bcast && x.destroy && x.err;
+    return x;
+  }();
+  return a;
+}
 
 static climber_status fail(climber_status st, const char* fmt, ...) {
   char buf[512];
@@ -138,6 +168,10 @@ struct climber_ctx_s {
   // latency graph: score layer l starts its attention as soon as the encode
   // wrote layer l's K/V (encode and score on two captured streams)
   cudaStream_t g_stream2 = nullptr;
+  // multi-GPU: this rank's NCCL communicator (climber_kv_broadcast)
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  void* bslab = nullptr;  // broadcast slab (device, slab_bytes)
   std::vector<cudaEvent_t> ov_evt;          // [L + 2]: per-layer K/V ready, fork, join
   bool ov_record = false, ov_wait = false;
   bool graphs = true;
@@ -319,8 +353,9 @@ extern "C" climber_status climber_create(const climber_config* cfg, const climbe
                                          int32_t world, const void* nccl_uid, climber_ctx_t* out) {
   try {
     if (!cfg || !strategies || !w || !arena || !out) return fail(CLIMBER_E_INVALID_ARG, "null argument");
-    if (world != 1 || rank != 0 || nccl_uid)
-      return fail(CLIMBER_E_UNSUPPORTED, "multi-GPU candidate sharding is not in this build (world must be 1)");
+    if (world < 1 || rank < 0 || rank >= world) return fail(CLIMBER_E_INVALID_ARG, "rank/world out of range");
+    if (world > 1 && !nccl_uid) return fail(CLIMBER_E_INVALID_ARG, "world > 1 needs an NCCL unique id");
+    if (nccl_uid && !nccl_api().ok) return fail(CLIMBER_E_UNSUPPORTED, "libnccl.so.2 not loadable");
     if (reinterpret_cast<uintptr_t>(arena) % 256) return fail(CLIMBER_E_INVALID_ARG, "arena must be 256-byte aligned");
     std::string why;
     Dims D;
@@ -455,6 +490,19 @@ extern "C" climber_status climber_create(const climber_config* cfg, const climbe
     CU(cudaEventCreateWithFlags(&c->stage_evt, cudaEventDisableTiming));
     CU(cudaEventRecord(c->stage_evt, 0));
     CU(cudaDeviceSynchronize());
+    c->rank = rank;
+    c->world = world;
+    if (nccl_uid) {  // collective: every rank of the group creates its ctx concurrently
+      ncclUniqueId id;
+      memcpy(&id, nccl_uid, sizeof(id));
+      ncclResult_t nr = nccl_api().init(&c->comm, world, id, rank);
+      if (nr != ncclSuccess) {
+        c->comm = nullptr;
+        const char* m = nccl_api().err(nr);
+        delete c;
+        return fail(CLIMBER_E_NCCL, "ncclCommInitRank: %s", m);
+      }
+    }
     *out = c;
     return CLIMBER_OK;
   } catch (const std::exception& ex) {
@@ -470,6 +518,8 @@ extern "C" climber_status climber_destroy(climber_ctx_t c) {
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->io) cudaFree(c->io);
   if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
+  if (c->comm) nccl_api().destroy(c->comm);
+  if (c->bslab) cudaFree(c->bslab);
   if (c->g_stream) cudaStreamDestroy(c->g_stream);
   if (c->g_stream2) cudaStreamDestroy(c->g_stream2);
   for (cudaEvent_t ev : c->ov_evt) cudaEventDestroy(ev);
@@ -1392,11 +1442,47 @@ extern "C" climber_status climber_kv_release(climber_ctx_t c, climber_kv_t kv) {
   return CLIMBER_OK;
 }
 
+static size_t page_bytes(const climber_ctx_s* c);
+
+// replicate one user's K/V to every rank of the ctx's NCCL
+// group.  The root exports its handle into one slab (256 B header: config
+// fingerprint, v_k per block, scenario r; then the pages), one ncclBroadcast
+// over NVLink/NVSwitch replicates it, every other rank imports it into its own
+// page pool and receives a new handle in *kv.  Collective; synchronises
+// `stream` on the receivers (they read r from the header).
 extern "C" climber_status climber_kv_broadcast(climber_ctx_t c, climber_kv_t* kv, int32_t root,
                                                climber_stream_t stream) {
-  (void)c; (void)kv; (void)root; (void)stream;
-  return fail(CLIMBER_E_UNSUPPORTED,
-              "climber_kv_broadcast: use climber_kv_export + the caller's collective + climber_kv_import");
+  if (!c || !kv) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+  if (root < 0 || root >= c->world) return fail(CLIMBER_E_INVALID_ARG, "root out of range");
+  if (c->world == 1 && !c->comm) return CLIMBER_OK;  // a single rank already holds it
+  if (!c->comm) return fail(CLIMBER_E_UNSUPPORTED, "ctx has no NCCL communicator");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t bytes = climber_kv_slab_bytes(c);
+  if (!c->bslab) CU(cudaMalloc(&c->bslab, bytes));
+  if (c->rank == root) {
+    climber_status st = climber_kv_export(c, *kv, c->bslab, stream);
+    if (st != CLIMBER_OK) return st;
+  }
+  ncclResult_t nr = nccl_api().bcast(c->bslab, c->bslab, bytes, ncclUint8, root, c->comm, s);
+  if (nr != ncclSuccess) return fail(CLIMBER_E_NCCL, "ncclBroadcast: %s", nccl_api().err(nr));
+  // CLIMBER_DEBUG_BCAST_SELF=1: the root also takes the receiver path (tests
+  // the whole export -> broadcast -> import chain on one GPU)
+  static const bool self_import = getenv("CLIMBER_DEBUG_BCAST_SELF") != nullptr;
+  if (c->rank == root && !self_import) return CLIMBER_OK;
+  int32_t r = 0;
+  CU(cudaMemcpyAsync(&r, (const char*)c->bslab + 28, 4, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return climber_kv_import(c, c->bslab, r, stream, kv);
+}
+
+extern "C" climber_status climber_nccl_unique_id(void* out) {
+  if (!out) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+  if (!nccl_api().ok) return fail(CLIMBER_E_UNSUPPORTED, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  ncclResult_t nr = nccl_api().get_uid(&id);
+  if (nr != ncclSuccess) return fail(CLIMBER_E_NCCL, "ncclGetUniqueId: %s", nccl_api().err(nr));
+  memcpy(out, &id, sizeof(id));
+  return CLIMBER_OK;
 }
 
 static size_t page_bytes(const climber_ctx_s* c) { return (size_t)2 * PAGE * c->D.d * c->esz; }
@@ -1409,17 +1495,18 @@ extern "C" climber_status climber_kv_export(climber_ctx_t c, climber_kv_t kv, vo
   if (!c || !slab) return fail(CLIMBER_E_INVALID_ARG, "null argument");
   if (c->cfg.rel_bias) return fail(CLIMBER_E_UNSUPPORTED, "K/V slabs do not carry the relative-bias state yet");
   if (reinterpret_cast<uintptr_t>(slab) % 16) return fail(CLIMBER_E_INVALID_ARG, "slab must be 16-byte aligned");
-  int slot;
+  int slot, r;
   {
     std::lock_guard<std::mutex> g(c->mu);
     climber_status rs = resolve(c, kv, &slot);
     if (rs != CLIMBER_OK) return rs;
+    r = c->slots[slot].r;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   {
     Prof p(c, CLIMBER_K_OTHER, s, 0, 2.0 * c->per_slot * page_bytes(c));
     launch_kv_export(c->pool, c->ptab, c->vlen_all, slot, c->per_slot, (long long)page_bytes(c), slab, c->D,
-                     c->cfg.dtype, s);
+                     c->cfg.dtype, r, s);
   }
   return check_launch(c, s);
 }

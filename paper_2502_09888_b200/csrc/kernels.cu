@@ -682,9 +682,10 @@ constexpr int SLAB_MAGIC = 0x4B56534C;  // "KVSL"
 
 __global__ void k_kv_export(const uint4* __restrict__ pool, const int* __restrict__ ptab, const int* __restrict__ vlen_all,
                             int slot, int per_slot, long long page_vec, int* __restrict__ hdr, uint4* __restrict__ body,
-                            Dims D, int dtype) {
+                            Dims D, int dtype, int r) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     hdr[0] = SLAB_MAGIC; hdr[1] = 1; hdr[2] = D.Nb; hdr[3] = D.L; hdr[4] = D.ppb; hdr[5] = D.d; hdr[6] = dtype;
+    hdr[7] = r;  // the handle's request scenario (for climber_kv_broadcast's receivers)
     for (int k = 0; k < D.Nb; ++k) hdr[8 + k] = vlen_all[(long long)slot * D.Nb + k];
   }
   const long long n = (long long)per_slot * page_vec;
@@ -715,9 +716,9 @@ __global__ void k_kv_import(uint4* __restrict__ pool, const int* __restrict__ pt
 }
 
 void launch_kv_export(const void* pool, const int* ptab, const int* vlen_all, int slot, int per_slot, long long page_bytes,
-                      void* slab, const Dims& D, int dtype, cudaStream_t s) {
+                      void* slab, const Dims& D, int dtype, int r, cudaStream_t s) {
   k_kv_export<<<592, 256, 0, s>>>((const uint4*)pool, ptab, vlen_all, slot, per_slot, page_bytes / 16, (int*)slab,
-                                  (uint4*)((char*)slab + 256), D, dtype);
+                                  (uint4*)((char*)slab + 256), D, dtype, r);
 }
 
 void launch_kv_import(void* pool, const int* ptab, int* vlen_all, int slot, int per_slot, long long page_bytes,

@@ -53,7 +53,7 @@ template <typename T>
 void launch_debug_kv(const T* pool, const int* ptab, const int* vlen_all, int slot, int k, int l, T* K, T* V,
                      const Dims& D, cudaStream_t s);
 void launch_kv_export(const void* pool, const int* ptab, const int* vlen_all, int slot, int per_slot, long long page_bytes,
-                      void* slab, const Dims& D, int dtype, cudaStream_t s);
+                      void* slab, const Dims& D, int dtype, int r, cudaStream_t s);
 void launch_kv_import(void* pool, const int* ptab, int* vlen_all, int slot, int per_slot, long long page_bytes,
                       const void* slab, int* err, const Dims& D, int dtype, cudaStream_t s);
 void launch_scatter_ptab(const int* staged, const int* slots, int B, int per, int* ptab, cudaStream_t s);

@@ -92,4 +92,6 @@ def test_arena_bytes_and_config_validation_on_host():
     st = L.climber_create(C.byref(_cfg(d=100)), strat, C.byref(w), C.c_void_p(256), 1 << 20, 0, 1, None, C.byref(h))
     assert st == 2 and L.climber_last_error().startswith(b"config:")
     st = L.climber_create(C.byref(_cfg()), strat, C.byref(w), C.c_void_p(256), 1 << 20, 0, 2, None, C.byref(h))
-    assert st == 10   # multi-GPU ctx not in this build
+    assert st == 1    # world > 1 without an NCCL unique id
+    st = L.climber_create(C.byref(_cfg()), strat, C.byref(w), C.c_void_p(256), 1 << 20, 2, 2, None, C.byref(h))
+    assert st == 1    # rank outside [0, world)

@@ -261,3 +261,44 @@ def test_cache_incremental_append_bitwise(rel_bias):
     assert res == "encoded" and nb == cfg.N_b
     cl.cache_release(h)
     cl.stream_status()
+
+
+def test_kv_broadcast_in_library_nccl():
+    # climber_kv_broadcast over the ctx's own NCCL communicator (world 1 on one
+    # GPU): the root keeps its handle; with CLIMBER_DEBUG_BCAST_SELF (a
+    # subprocess, the knob is read once) the root also runs the receiver path
+    # (export -> ncclBroadcast -> header scenario -> import): bitwise scores
+    import subprocess
+    import sys
+    import torch
+    from paper_2502_09888_b200 import nccl_unique_id
+    cfg = synth.preset("small")
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 5, B=1)
+    cl = make_gpu(cfg, w, 1, kv_users=2, rank=0, world=1, nccl_uid=nccl_unique_id())
+    item, action, scenario, ts, cand = to_dev(batch)
+    h = cl.encode_user(item, action, scenario, ts, int(batch.r[0]))
+    ref = cl.score_items(h, cand)
+    assert cl.kv_broadcast(h, root=0) == h
+    assert torch.equal(cl.score_items(h, cand), ref)
+    cl.release(h)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import sys, torch; sys.path[:0] = [%r, %r]
+import synth
+from helpers import make_gpu, to_dev
+from paper_2502_09888_b200 import nccl_unique_id
+cfg = synth.preset("small"); w = synth.make_weights(cfg, 0); batch = synth.make_batch(cfg, 5, B=1)
+cl = make_gpu(cfg, w, 1, kv_users=2, rank=0, world=1, nccl_uid=nccl_unique_id())
+item, action, scenario, ts, cand = to_dev(batch)
+h = cl.encode_user(item, action, scenario, ts, int(batch.r[0]))
+ref = cl.score_items(h, cand)
+h2 = cl.kv_broadcast(h, root=0)
+assert h2 != h
+assert torch.equal(cl.score_items(h2, cand), ref)
+cl.stream_status()
+print("ok")
+""" % (root, os.path.join(root, "tests"))
+    env = dict(os.environ, CLIMBER_DEBUG_BCAST_SELF="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
