@@ -1386,8 +1386,18 @@ static climber_status score_common(climber_ctx_t c, int32_t B, const climber_kv_
       else if (c->fused) score_wave_fused(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
       else if (c->cfg.dtype == CLIMBER_BF16) score_wave<bf16>(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
       else score_wave<float>(c, it, wc, w.u0, w.U, w.P, w.Mmax, sc, s);
+      if (c->sync_check && sc) launch_check_finite(sc, w.P, c->err, s);
       climber_status rs = check_launch(c, s);
       if (rs != CLIMBER_OK) return rs;
+      if (c->sync_check && sc) {  // synchronous numeric check (the header's E_NUMERIC contract)
+        int err = 0;
+        CU(cudaMemcpy(&err, c->err, 4, cudaMemcpyDeviceToHost));
+        if (err & ERR_NUMERIC) {
+          const int keep = err & ~ERR_NUMERIC;
+          CU(cudaMemcpy(c->err, &keep, 4, cudaMemcpyHostToDevice));
+          return fail(CLIMBER_E_NUMERIC, "non-finite score in users [%d, %d)", w.u0, w.u0 + w.U);
+        }
+      }
     }
     return CLIMBER_OK;
   } catch (...) {
@@ -1563,6 +1573,7 @@ extern "C" climber_status climber_stream_status(climber_ctx_t c, climber_stream_
   if (err & ERR_RANGE) return fail(CLIMBER_E_OUT_OF_RANGE, "an item/action/scenario id was out of range");
   if (err & ERR_UNSORTED) return fail(CLIMBER_E_UNSORTED, "a lifecycle sequence had decreasing timestamps");
   if (err & ERR_CONFIG) return fail(CLIMBER_E_CONFIG, "an imported K/V slab did not match this ctx's config");
+  if (err & ERR_NUMERIC) return fail(CLIMBER_E_NUMERIC, "a score was not finite");
   return CLIMBER_OK;
 }
 

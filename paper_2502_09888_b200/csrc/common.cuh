@@ -64,7 +64,7 @@ __host__ __device__ __forceinline__ long long bias_row(const Dims& D, int l, int
 }
 
 // Device error word bits (climber_stream_status maps them to statuses).
-enum : int { ERR_RANGE = 1, ERR_UNSORTED = 2, ERR_CONFIG = 4 };
+enum : int { ERR_RANGE = 1, ERR_UNSORTED = 2, ERR_CONFIG = 4, ERR_NUMERIC = 8 };
 
 constexpr int PAGE = 64;  // tokens per K/V page
 

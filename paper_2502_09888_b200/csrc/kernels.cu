@@ -140,6 +140,19 @@ void launch_append_flags(const uint8_t* action, const uint8_t* scenario, long lo
   k_append_flags<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(action, scenario, n0, n1, amask, smask, flags, D);
 }
 
+// CLIMBER_SYNC_CHECK=1: flag non-finite scores (climber_status E_NUMERIC)
+__global__ void k_check_finite(const float* __restrict__ x, long long n, int* __restrict__ err) {
+  bool bad = false;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(err, ERR_NUMERIC);
+}
+
+void launch_check_finite(const float* x, long long n, int* err, cudaStream_t s) {
+  const long long b = (n + 255) / 256;
+  k_check_finite<<<(unsigned)(b < 592 ? (b > 0 ? b : 1) : 592), 256, 0, s>>>(x, n, err);
+}
+
 void launch_cand_bias(const int* wave_slot, const int* wave_r, int U, const int* vlen_all, const Dims& D,
                       cudaStream_t s) {
   k_cand_bias<<<dim3(U, D.L * D.Nb * D.h), 128, 0, s>>>(wave_slot, wave_r, vlen_all, D);

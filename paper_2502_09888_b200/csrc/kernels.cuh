@@ -20,6 +20,8 @@ void launch_row_prep(const float* C, bf16* Cb, float* part, long long rows, int 
 void launch_append_flags(const uint8_t* action, const uint8_t* scenario, long long n0, long long n1,
                          const unsigned long long* amask, const unsigned long long* smask, int* flags, const Dims& D,
                          cudaStream_t s);
+// CLIMBER_SYNC_CHECK: flag non-finite values in the device error word
+void launch_check_finite(const float* x, long long n, int* err, cudaStream_t s);
 void launch_extract(const EventsDev& ev, const int64_t* ev_off, const int* wave_slot, int U,
                     const unsigned long long* amask, const unsigned long long* smask, int* idx_all,
                     int* vlen_all, int* bad_all, int* err, const Dims& D, cudaStream_t s);

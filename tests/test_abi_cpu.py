@@ -95,3 +95,10 @@ def test_arena_bytes_and_config_validation_on_host():
     assert st == 1    # world > 1 without an NCCL unique id
     st = L.climber_create(C.byref(_cfg()), strat, C.byref(w), C.c_void_p(256), 1 << 20, 2, 2, None, C.byref(h))
     assert st == 1    # rank outside [0, world)
+
+
+def test_nccl_unique_id_on_host():
+    # libnccl is resolved at run time (dlopen); the unique id needs no GPU
+    from paper_2502_09888_b200 import nccl_unique_id
+    a, b = nccl_unique_id(), nccl_unique_id()
+    assert len(a) == 128 and a != b

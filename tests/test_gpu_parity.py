@@ -307,3 +307,32 @@ def test_forward_sumi_record_equals_susi_records(name):
                           np.arange(25, dtype=np.int64), items)
         assert torch.equal(susi, sumi[c0:c0 + 24])
     cl.stream_status()
+
+
+def test_sync_check_reports_non_finite_scores():
+    # CLIMBER_SYNC_CHECK=1 (read at create): a score that is not finite fails
+    # the score call with E_NUMERIC.  An item embedding near the fp32 maximum
+    # overflows its candidate rows' projections (inf * 0 = NaN after the norm).
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import sys, numpy as np; sys.path[:0] = [%r, %r]
+import synth
+from helpers import make_gpu, gpu_scores
+from paper_2502_09888_b200 import ClimberError
+cfg = synth.preset("small"); w = synth.make_weights(cfg, 0); batch = synth.make_batch(cfg, 1, B=2)
+ok = gpu_scores(make_gpu(cfg, w, 2), batch)
+assert np.all(np.isfinite(ok))
+emb = w.emb_item.copy(); emb[int(batch.cand[5])] = 3e38
+cl = make_gpu(cfg, w.scaled(emb_item=emb), 2)
+try:
+    gpu_scores(cl, batch)
+    print("no error")
+except ClimberError as e:
+    print(e.name)
+""" % (root, os.path.join(root, "tests"))
+    env = dict(os.environ, CLIMBER_SYNC_CHECK="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and out.stdout.strip().endswith("E_NUMERIC"), (out.stdout, out.stderr[-2000:])
