@@ -19,7 +19,8 @@
  *     RMSNorm, FFN (d -> 4d SiLU -> d) + residual.  History attention is causal
  *     (hist_causal = 1) or bidirectional (0); every candidate attends to the
  *     whole history of its block plus itself only (L255: full-visible +
- *     diagonal masks).  Relative bias f_b is 0 on this path (G6).
+ *     diagonal masks).  Relative bias f_b is 0 (G6) unless the config sets
+ *     rel_bias = 1 (Eq. 3's f_b^{p,t}(a_k, r), see climber_config).
  *   - Bit-wise gating fusion (Eq. 4): one fusion ATL over the N_b block
  *     outputs (temperature tau_f[r][head], no mask), squeeze-and-excitation gate
  *     FC(N_b d -> N_b d / se_reduction) + b, ReLU, FC + b, sigmoid, product.

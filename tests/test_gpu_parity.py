@@ -336,3 +336,28 @@ except ClimberError as e:
     env = dict(os.environ, CLIMBER_SYNC_CHECK="1")
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and out.stdout.strip().endswith("E_NUMERIC"), (out.stdout, out.stderr[-2000:])
+
+
+def test_large_in_bench_launch_configuration_sampled():
+    # BASELINE configs[3] in the launch configuration bench.py times (waves of
+    # 64 users, up to 65536 pairs per wave, 1000 candidates per user): 128 users
+    # = two encode waves and two score waves; sampled users vs the oracle
+    cfg = synth.preset("large")
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 1, B=128)
+    from paper_2502_09888_b200 import Climber, ModelConfig
+    cl = Climber(ModelConfig.from_any(cfg), w, synth.strategies_for(cfg.N_b, cfg.R), max_users=128,
+                 max_wave_users=64, max_wave_pairs=65536, kv_users=128)
+    got = gpu_scores(cl, batch)
+    cl.stream_status()
+    assert np.all(np.isfinite(got))
+    ref = oracle_scores(cfg, w, batch, [0, 77, 127])
+    for b, r in ref.items():
+        ab, rel = parity_err(got[batch.cand_offsets[b]:batch.cand_offsets[b + 1]], r)
+        assert ab <= tolerance(cfg) and rel <= tolerance(cfg), (b, ab, rel)
+
+
+def test_sweep_deep_and_long_corners_bf16():
+    # BASELINE configs[4] axis ends: 16 layers, and n = 8192 (n_k = 1024)
+    for kw in (dict(L=16, n_k=128, M=64, n_s=3 * 128 * 8), dict(L=2, n_k=1024, M=64, n_s=3 * 1024 * 8)):
+        _check_cfg(synth.preset("sweep", **kw), B=1, users=[0])
