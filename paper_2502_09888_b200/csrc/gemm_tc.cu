@@ -566,7 +566,11 @@ void launch_gemm_tc_batched(const bf16* A, long long lda, long long a_bs, const 
       else tc::launch<128, 6, 4, 2, 1, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
       return;
     }
-    const bool heavy = (e.kind == EPI_STORE || e.kind == EPI_STORE_F32) && e.act != ACT_NONE;
+    // 8 epilogue warps for the plain epilogues too (QKV / K/V-page stores): the
+    // K = 512 launches are paced by the epilogue, 993-1002 vs 895 TFLOP/s for
+    // the QKV class in the large step (CLIMBER_GEMM_EPI8=0: 4 warps, 2 buffers)
+    static const bool epi8 = !(getenv("CLIMBER_GEMM_EPI8") && atoi(getenv("CLIMBER_GEMM_EPI8")) == 0);
+    const bool heavy = ((e.kind == EPI_STORE || e.kind == EPI_STORE_F32) && e.act != ACT_NONE) || epi8;
     if (N % 256 == 0) {
       if (heavy) tc::launch<256, 6, 8, 1, 0, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
       else tc::launch<256, 6, 4, 2, 0, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
