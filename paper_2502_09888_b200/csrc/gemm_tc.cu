@@ -571,8 +571,12 @@ void launch_gemm_tc_batched(const bf16* A, long long lda, long long a_bs, const 
     // the QKV class in the large step (CLIMBER_GEMM_EPI8=0: 4 warps, 2 buffers)
     static const bool epi8 = !(getenv("CLIMBER_GEMM_EPI8") && atoi(getenv("CLIMBER_GEMM_EPI8")) == 0);
     const bool heavy = ((e.kind == EPI_STORE || e.kind == EPI_STORE_F32) && e.act != ACT_NONE) || epi8;
+    // CLIMBER_GEMM_EPI16=1 (measurement knob): 16 epilogue warps for the activation epilogues
+    static const bool epi16 = getenv("CLIMBER_GEMM_EPI16") && atoi(getenv("CLIMBER_GEMM_EPI16")) == 1;
+    const bool act = (e.kind == EPI_STORE || e.kind == EPI_STORE_F32) && e.act != ACT_NONE;
     if (N % 256 == 0) {
-      if (heavy) tc::launch<256, 6, 8, 1, 0, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+      if (epi16 && act) tc::launch<256, 5, 16, 1, 0, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+      else if (heavy) tc::launch<256, 6, 8, 1, 0, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
       else tc::launch<256, 6, 4, 2, 0, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
     } else {
       tc::launch<128, 8, 4, 2, 0, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
