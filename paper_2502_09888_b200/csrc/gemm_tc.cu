@@ -296,11 +296,21 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
           tmem_ld32(taddr + c, v);  // lane = row row0 + lane
           if (!f32_out) tmem_ld32(taddr + c + 32, v + 32);
           const int n0 = n_blk * BN + c;
-          if (e.rs_part != nullptr) {
+          // FFN-up (the epilogue paces these K = 512 launches): SiLU(x rs) =
+          // h + h tanh(h) with h = x rs / 2 -- one multiply, one MUFU, one FMA
+          const bool silu_fused = !f32_out && e.kind == EPI_STORE && e.act == ACT_SILU && e.bias == nullptr;
+          if (silu_fused) {
+            const float hs = 0.5f * rsc;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+              const float h = v[i] * hs;
+              v[i] = fmaf(h, tanh_approx(h), h);
+            }
+          } else if (e.rs_part != nullptr) {
 #pragma unroll
             for (int i = 0; i < 64; ++i) v[i] *= rsc;
           }
-          if (e.kind != EPI_RESID && e.kind != EPI_QKV_PAGES) {
+          if (!silu_fused && e.kind != EPI_RESID && e.kind != EPI_QKV_PAGES) {
             // bias (vectorised) and activation, each hoisted out of the element loop
             if (e.bias != nullptr) {
               const float4* b4 = reinterpret_cast<const float4*>(e.bias + n0);
