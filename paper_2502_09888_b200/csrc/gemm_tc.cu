@@ -299,16 +299,24 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
           // FFN-up (the epilogue paces these K = 512 launches): SiLU(x rs) =
           // h + h tanh(h) with h = x rs / 2 -- one multiply, one MUFU, one FMA
           const bool silu_fused = !f32_out && e.kind == EPI_STORE && e.act == ACT_SILU && e.bias == nullptr;
-          if (silu_fused) {
-            const float hs = 0.5f * rsc;
+          if (silu_fused) {  // packed FP32x2 multiply / FMA: two elements per issue slot
+            const uint64_t hs2 = f2_pack(0.5f * rsc, 0.5f * rsc);
 #pragma unroll
-            for (int i = 0; i < 64; ++i) {
-              const float h = v[i] * hs;
-              v[i] = fmaf(h, tanh_approx(h), h);
+            for (int i = 0; i < 64; i += 2) {
+              const uint64_t h2 = f2_mul(f2_pack(v[i], v[i + 1]), hs2);
+              const float2 h = f2_unpack(h2);
+              const float2 y = f2_unpack(f2_fma(h2, f2_pack(tanh_approx(h.x), tanh_approx(h.y)), h2));
+              v[i] = y.x;
+              v[i + 1] = y.y;
             }
           } else if (e.rs_part != nullptr) {
+            const uint64_t r2 = f2_pack(rsc, rsc);
 #pragma unroll
-            for (int i = 0; i < 64; ++i) v[i] *= rsc;
+            for (int i = 0; i < 64; i += 2) {
+              const float2 y = f2_unpack(f2_mul(f2_pack(v[i], v[i + 1]), r2));
+              v[i] = y.x;
+              v[i + 1] = y.y;
+            }
           }
           if (!silu_fused && e.kind != EPI_RESID && e.kind != EPI_QKV_PAGES) {
             // bias (vectorised) and activation, each hoisted out of the element loop
