@@ -158,7 +158,8 @@ def run_reference(args, cfg):
             "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": int(cores), "kind": "oracle",
                              "sample": f"1 user (full encode) x {m_ref} candidates per step of workload "
                                        f"'{cfg.name}', fp64 NumPy"},
-            "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "ranks_launched": int(os.environ.get("WORLD_SIZE", "1"))}
     print(json.dumps(line), flush=True)
 
 
@@ -260,6 +261,25 @@ def roofline(prof, pk, pk_src, bf16=True):
             "share_of_step": p["ms"] / tot_ms if tot_ms else None, "peak_source": peak_note}
 
 
+def self_launch(args) -> bool:
+    """`--gpus N` with N > 1 outside torchrun: re-run this command as N ranks
+    (one process per GPU) through torch.distributed.run on 127.0.0.1 and
+    return True (the caller exits with the launcher's status)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.call(cmd)
+    if rc:
+        sys.exit(rc)
+    return True
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -275,11 +295,20 @@ def main():
                     help="warm K/V reuse: score R fresh candidate sets per cached user (SURVEY §8(d) medium)")
     ap.add_argument("--impl", default="climber", choices=["climber", "reference"])
     ap.add_argument("--users", type=int, default=0, help="override B (users per rank per step)")
-    ap.add_argument("--latency-requests", type=int, default=30)
+    ap.add_argument("--latency-requests", type=int, default=-1,
+                    help="closed-loop requests (SURVEY §8(d): 200 at large, 500 elsewhere; 0 = off)")
+    ap.add_argument("--latency-warmup", type=int, default=20)
+    ap.add_argument("--profile-steps", type=int, default=2,
+                    help="steps re-run with the per-launch profiler for the per-class breakdown and roofline")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
+    if self_launch(args):
+        return
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if world_env != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}")
     cfg = synth.preset(args.config)
     over = {}
     if args.L:
@@ -297,6 +326,8 @@ def main():
     if args.impl == "reference":
         run_reference(args, cfg)
         return
+    if args.latency_requests < 0:
+        args.latency_requests = 200 if cfg.name == "large" else 500
 
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -309,8 +340,17 @@ def main():
     w = synth.make_weights(cfg, 0)
     batch = rank_batch(cfg, rank)
     B, M = cfg.B, cfg.M
+    uid = None
+    if dist is not None:
+        # the library's own NCCL communicator (climber_kv_broadcast): rank 0's unique id to every rank
+        from paper_2502_09888_b200 import nccl_unique_id
+        t = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            t.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(t, src=0)
+        uid = bytes(t.cpu().tolist())
     cl = Climber(ModelConfig.from_any(cfg), w, synth.strategies_for(cfg.N_b, cfg.R), max_users=B,
-                 max_wave_users=64, max_wave_pairs=max(M, 65536), kv_users=B)
+                 max_wave_users=64, max_wave_pairs=max(M, 65536), kv_users=B, rank=rank, world=world, nccl_uid=uid)
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     item, action, scenario, ts, cand = (dev(batch.item), dev(batch.action), dev(batch.scenario), dev(batch.ts),
                                         dev(batch.cand))
@@ -336,7 +376,6 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     n0 = cl.launch_count
-    cl.profile(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
@@ -346,12 +385,54 @@ def main():
     if dist:
         dist.barrier()
     clk = clocks.stop()
-    cl.profile(False)
     launches = cl.launch_count - n0
-    prof = cl.profile_read()
     ms_max = max_over_ranks(dist, e0.elapsed_time(e1), "cuda")
     pairs_per_rank = int(batch.cand_offsets[-1]) * args.steps
     value = aggregate_rate(pairs_per_rank, world, ms_max)
+
+    # ---- per-class breakdown: the same steps again with the in-library
+    # profiler on (CUDA events around every launch on its stream); kept out of
+    # the headline's timed region ----
+    cl.profile(True)
+    q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    q0.record(stream)
+    for _ in range(max(1, args.profile_steps)):
+        step()
+    q1.record(stream)
+    torch.cuda.synchronize()
+    cl.profile(False)
+    prof = cl.profile_read()
+    prof_ms = q0.elapsed_time(q1) / max(1, args.profile_steps)
+
+    # ---- strong scaling: the config's B users split across the
+    # ranks (rank g takes users [g B / N, (g + 1) B / N) of the same batch) ----
+    strong = None
+    if world > 1:
+        lo, hi = rank * B // world, (rank + 1) * B // world
+        sb = batch.subset(range(lo, hi))
+        sdv = [dev(a) for a in (sb.item, sb.action, sb.scenario, sb.ts, sb.cand)]
+        sscores = torch.empty(int(sb.cand_offsets[-1]), dtype=torch.float32, device="cuda")
+
+        def sstep():
+            hs = cl.encode_users(sb.ev_offsets, *sdv[:4], sb.r)
+            cl.score_batched(hs, sb.cand_offsets, sdv[4], sscores)
+            cl.release(hs)
+        sstep()
+        dist.barrier()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            sstep()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        sms = max_over_ranks(dist, g0.elapsed_time(g1), "cuda")
+        tot = torch.tensor([float(sb.cand_offsets[-1])], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tot)
+        strong = {"value": tot.item() * args.steps / (sms / 1e3), "unit": "pairs/s", "users_total": B,
+                  "users_per_rank": hi - lo, "ms_per_step": sms / args.steps,
+                  "mode": "strong scaling: the config's B users split across the ranks, max over ranks"}
 
     # ---- end to end through the public C ABI with HOST buffers ----
     e2e = None
@@ -427,15 +508,16 @@ def main():
     # ---- per-request latency: one user, M candidates, host call to host scores ----
     lat = None
     if args.latency_requests > 0 and world == 1:
-        one = [batch.subset([b % B]) for b in range(args.latency_requests + 5)]
+        nw = args.latency_warmup
+        one = [batch.subset([b % B]) for b in range(args.latency_requests + nw)]
         tl = []
         for i, u in enumerate(one):
             t0 = time.perf_counter()
             cl.rank_host(u.ev_offsets, u.item, u.action, u.scenario, u.ts, u.r, u.cand_offsets, u.cand)
-            if i >= 5:
+            if i >= nw:
                 tl.append((time.perf_counter() - t0) * 1e3)
         lat = {"p50": float(np.percentile(tl, 50)), "p99": float(np.percentile(tl, 99)), "requests": len(tl),
-               "mode": "single GPU per request (B=1, M candidates), climber_rank_host: H2D + one CUDA graph (encode + score, captured once per shape) + D2H"}
+               "warmup": nw, "mode": "single GPU per request (B=1, M candidates), climber_rank_host: H2D + one CUDA graph (encode + score, captured once per shape) + D2H"}
         # where one request's device time goes: the same request eagerly with the
         # per-launch profiler on (CUDA events around every launch; graphs are off
         # while profiling), summed per kernel class, ms
@@ -451,32 +533,35 @@ def main():
         lat["device_ms_by_class"] = {k: round(v["ms"], 4) for k, v in br.items() if v["launches"]}
         lat["device_ms_total"] = round(sum(v["ms"] for v in br.values()), 4)
     elif args.latency_requests > 0:
-        # candidate sharding: owner encodes, K/V slab broadcast over
-        # the NCCL group, every rank scores floor(m G / M) == rank, scores gathered
-        from paper_2502_09888_b200.sharded import ClimberBackend, rank_request_sharded
+        # candidate sharding: owner encodes, the library's
+        # climber_kv_broadcast replicates the K/V (ncclBroadcast on the ctx's own
+        # communicator), every rank scores floor(m G / M) == rank, scores gathered
+        from paper_2502_09888_b200.sharded import ClimberBackend, rank_request_sharded_lib
         be = ClimberBackend(cl)
+        nw = args.latency_warmup
         tl = []
-        for i in range(args.latency_requests + 5):
+        for i in range(args.latency_requests + nw):
             u = batch.subset([i % B])
             items = dev(u.cand)
             dist.barrier()
             t0 = time.perf_counter()
             ev = (dev(u.item), dev(u.action), dev(u.scenario), dev(u.ts)) if rank == 0 else None
-            out = rank_request_sharded(be, dist, ev, int(u.r[0]), items)
+            out = rank_request_sharded_lib(cl, dist, ev, int(u.r[0]), items)
             if rank == 0:
                 out.cpu()
-                if i >= 5:
+                if i >= nw:
                     tl.append((time.perf_counter() - t0) * 1e3)
         if rank == 0:
             lat = {"p50": float(np.percentile(tl, 50)), "p99": float(np.percentile(tl, 99)), "requests": len(tl),
-                   "mode": f"candidate-sharded over {world} GPUs: owner encodes, K/V slab broadcast (NCCL), "
-                           f"scores all_gather; host call to host scores"}
+                   "warmup": nw,
+                   "mode": f"candidate-sharded over {world} GPUs: owner encodes, climber_kv_broadcast (library "
+                           f"ncclBroadcast of the K/V slab), scores all_gather; host call to host scores"}
         if cfg.N_b % world == 0:
             # block-parallel: each rank encodes + scores N_b / G blocks,
             # block outputs all-gathered, rank 0 fuses; no K/V moves
             from paper_2502_09888_b200.sharded import rank_request_block_parallel
             tb = []
-            for i in range(args.latency_requests + 5):
+            for i in range(args.latency_requests + nw):
                 u = batch.subset([i % B])
                 items = dev(u.cand)
                 dist.barrier()
@@ -485,7 +570,7 @@ def main():
                 out = rank_request_block_parallel(be, dist, ev, int(u.r[0]), items)
                 if rank == 0:
                     out.cpu()
-                    if i >= 5:
+                    if i >= nw:
                         tb.append((time.perf_counter() - t0) * 1e3)
             if rank == 0:
                 lat["block_parallel"] = {
@@ -496,12 +581,17 @@ def main():
     if rank == 0:
         pk, pk_src = peaks()
         roof = roofline(prof, pk, pk_src, cfg.dtype == "bf16")
-        tot_flops = sum(v["flops"] for v in prof.values())
+        flops_step = sum(v["flops"] for v in prof.values()) / max(1, args.profile_steps)
         line = {"metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if cfg.dtype == "bf16" else "f32",
                 "data": "synthetic", "config": workload_cfg(cfg), "roofline": roof,
-                "step_tflops": tot_flops / (ms_max * 1e-3) / 1e12,
+                "step_tflops": flops_step / (ms_max / args.steps * 1e-3) / 1e12,
+                "profiled_pass": {"steps": max(1, args.profile_steps), "ms_per_step": prof_ms,
+                                  "note": "kernel_ms / kernel_rate / roofline come from this second pass with "
+                                          "CUDA events around every launch; the headline value is timed "
+                                          "with the profiler off"},
+                **({"strong_scaling": strong} if strong else {}),
                 "e2e": e2e, "latency_ms": lat, "gpu_launches": int(launches), "clocks": clk,
                 **({"warm_reuse": warm} if warm else {}), **({"susi": susi} if susi else {}),
                 "kernel_ms": {k: round(v["ms"], 3) for k, v in prof.items() if v["launches"]},

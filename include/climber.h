@@ -323,16 +323,21 @@ climber_status climber_cache_stats(climber_ctx_t ctx, int64_t* stats);
  * contiguous DEVICE slab, the slab is replicated with a collective of the
  * caller's process group (e.g. an NCCL broadcast over NVLink), and every other
  * rank imports it into its own page pool; each rank then scores its shard of
- * the candidates.  Slab layout: 256-byte header (int32 magic, abi, n_blocks,
- * n_layers, pages per block, d, dtype, vlen[n_blocks]) followed by the
- * handle's pages in page-table order ([2][64][d] elements each).  The slab is
- * only meaningful to a ctx created with the same config. */
+ * the candidates.  Slab layout: 256-byte header (int32 magic, slab version 2,
+ * n_blocks, n_layers, pages per block, d, dtype, scenario r, vlen[n_blocks]
+ * at int 8.., rel_bias flag at int 16) followed by the handle's pages in
+ * page-table order ([2][64][d] elements each) and, for rel_bias contexts, the
+ * handle's relative-bias state (token ages int32 [n_blocks][n_k], candidate-
+ * row bias fp32 [n_layers][n_blocks][n_heads][n_k]).  The slab is only
+ * meaningful to a ctx created with the same config. */
 
 /* Bytes of one user's slab for this ctx's config. */
 size_t climber_kv_slab_bytes(climber_ctx_t ctx);
 
-/* Gather the handle's pages into `slab` (DEVICE, >= climber_kv_slab_bytes).
- * Asynchronous on `stream`. */
+/* Gather the handle's pages into `slab` (DEVICE, 16-byte aligned, >=
+ * climber_kv_slab_bytes).  Asynchronous on `stream`.  E_INVALID_ARG for a
+ * handle that holds only a block range (climber_encode_users_blocks), E_STALE
+ * for a released or foreign handle. */
 climber_status climber_kv_export(climber_ctx_t ctx, climber_kv_t kv, void* slab, climber_stream_t stream);
 
 /* Allocate a handle in this ctx's pool and scatter the slab's pages into it.
@@ -350,7 +355,14 @@ climber_status climber_kv_import(climber_ctx_t ctx, const void* slab, int32_t sc
  * returned in *kv.  Root exports the pages into one slab, one ncclBroadcast
  * (NVLink / NVSwitch) replicates it, the receivers import it; receivers
  * synchronise `stream` once (to read the handle's scenario from the slab
- * header).  A world-1 ctx without a communicator returns OK unchanged. */
+ * header).  A world-1 ctx without a communicator returns OK unchanged.
+ * Every rank joins the broadcast even when the root's export fails (stale
+ * handle, block-range handle): the root then sends an invalid header and
+ * returns the export's error, every receiver returns E_STALE and allocates
+ * nothing.  Receivers wait with a deadline (env CLIMBER_NCCL_TIMEOUT_MS,
+ * default 120000); on timeout or an asynchronous NCCL error the communicator
+ * is aborted (ncclCommAbort) and E_NCCL returned; later broadcasts on the
+ * ctx return E_UNSUPPORTED. */
 climber_status climber_kv_broadcast(climber_ctx_t ctx, climber_kv_t* kv, int32_t root,
                                     climber_stream_t stream);
 
@@ -371,10 +383,32 @@ const char* climber_last_error(void);
  * relative to the user's first event, left-padded with -1; vlen HOST int32[N_b]. */
 climber_status climber_debug_extract(climber_ctx_t ctx, climber_kv_t kv, int32_t* idx, int32_t* vlen);
 
-/* Canonical SUMI masks for M candidates, evaluated on the device from the same
- * visibility rule the attention kernels use: HOST uint8[N_b][(n_k+M)^2],
- * row-major, history slots left-padded, 1 = attend. */
+/* Canonical SUMI masks for M candidates, evaluated on the device from the
+ * written-out visibility rule (common.cuh sumi_visible): HOST
+ * uint8[N_b][(n_k+M)^2], row-major, history slots left-padded, 1 = attend
+ * (SURVEY §8(c), D8).  This is the rule, not the attention kernels: what the
+ * kernels actually attend is recovered by climber_debug_attn_probe. */
 climber_status climber_debug_mask(climber_ctx_t ctx, climber_kv_t kv, int32_t M, uint8_t* mask);
+
+/* Mask probe of the production attention kernels ("full-visible masks
+ * between each candidate item and the entire history ... diagonal masks for
+ * inter-item isolation"; G1 causal / bidirectional history; G14 self).
+ * Runs the same attention kernel the encode (mode 0: history rows of layer
+ * `layer`) or the score (mode 1: M candidate rows) launches for `block` of
+ * handle kv, on a probe input: q = k = 0 (so every visible key gets weight
+ * 1 / |visible set|) and V[j] one-hot: for head h, key j = key_off + h (d_h - 1)
+ * + c (0 <= c < d_h - 1) is channel c; SUMI rows get v_self = channel d_h - 1.
+ * out: HOST float [rows][d] (rows = n_k for mode 0, internal right-padded slot
+ * order: slot i = i-th kept event; M for mode 1), out[row][h d_h + c] != 0 iff
+ * that key (c < d_h - 1) or the self term (c = d_h - 1) is attended.  Pad rows
+ * (slot >= v_k) read 0.  Covers keys [key_off, key_off + h (d_h - 1)) per call.
+ * DEBUG ONLY, synchronous, not concurrent with other calls on the ctx: it
+ * OVERWRITES the handle's K/V pages of (layer, block) -- release the handle
+ * afterwards.  Errors: E_INVALID_ARG (mode, layer, block outside the handle's
+ * blocks, M outside [1, max_candidates]), E_UNSUPPORTED (rel_bias contexts),
+ * E_STALE, E_CUDA. */
+climber_status climber_debug_attn_probe(climber_ctx_t ctx, climber_kv_t kv, int32_t mode, int32_t layer,
+                                        int32_t block, int32_t M, int32_t key_off, float* out);
 
 /* One layer/block of the cache, gathered from its pages in canonical order:
  * K, V HOST arrays [vlen][d] of float (dtype FP32) or uint16 bf16 bits (BF16);

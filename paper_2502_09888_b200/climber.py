@@ -82,6 +82,7 @@ def lib() -> C.CDLL:
             "climber_debug_extract": (I32, [VP, VP, P, P]),
             "climber_debug_mask": (I32, [VP, VP, I32, P]),
             "climber_debug_kv": (I32, [VP, VP, I32, I32, P, P]),
+            "climber_debug_attn_probe": (I32, [VP, VP, I32, I32, I32, I32, I32, P]),
             "climber_launch_count": (I64, [VP]),
             "climber_debug_gemm": (I32, [VP, VP, VP, I64, I32, I32, I32, I32, VP]),
             "climber_profile": (I32, [VP, I32]),
@@ -111,6 +112,7 @@ EXPORTED_SYMBOLS = ("climber_arena_bytes", "climber_create", "climber_destroy", 
                     "climber_encode_users", "climber_score_items", "climber_score_items_batched",
                     "climber_rank_host", "climber_kv_release", "climber_kv_broadcast", "climber_stream_status",
                     "climber_last_error", "climber_debug_extract", "climber_debug_mask", "climber_debug_kv",
+                    "climber_debug_attn_probe",
                     "climber_launch_count", "climber_debug_gemm", "climber_profile", "climber_profile_read",
                     "climber_kv_slab_bytes", "climber_kv_export", "climber_kv_import",
                     "climber_encode_users_blocks", "climber_score_blocks", "climber_fuse_scores", "climber_forward",
@@ -434,6 +436,14 @@ class Climber:
         m = np.empty((self.cfg.N_b, T, T), np.uint8)
         _check(lib().climber_debug_mask(self.h, C.c_void_p(handle), int(M), _ptr(m)))
         return m
+
+    def debug_attn_probe(self, handle, mode: int, layer: int, block: int, M: int, key_off: int):
+        """climber_debug_attn_probe: float [rows][d] (rows = n_k for mode 0, M for mode 1)."""
+        rows = self.cfg.n_k if mode == 0 else M
+        out = np.zeros((rows, self.cfg.d), np.float32)
+        _check(lib().climber_debug_attn_probe(self.h, C.c_void_p(handle), int(mode), int(layer), int(block),
+                                              int(M), int(key_off), _ptr(out)))
+        return out
 
     def debug_kv(self, handle, layer: int, block: int, v: int):
         dt = np.uint16 if self.cfg.dtype == "bf16" else np.float32

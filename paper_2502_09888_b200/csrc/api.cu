@@ -6,7 +6,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <chrono>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -31,6 +33,8 @@ struct NcclApi {
   decltype(&ncclBroadcast) bcast = nullptr;
   decltype(&ncclCommDestroy) destroy = nullptr;
   decltype(&ncclGetErrorString) err = nullptr;
+  decltype(&ncclCommAbort) abort = nullptr;
+  decltype(&ncclCommGetAsyncError) async_err = nullptr;
   bool ok = false;
 };
 static NcclApi& nccl_api() {
@@ -44,7 +48,9 @@ static NcclApi& nccl_api() {
     x.bcast = (decltype(x.bcast))dlsym(h, "ncclBroadcast");
     x.destroy = (decltype(x.destroy))dlsym(h, "ncclCommDestroy");
     x.err = (decltype(x.err))dlsym(h, "ncclGetErrorString");
-    x.ok = x.get_uid && x.init && x.bcast && x.destroy && x.err;
+    x.abort = (decltype(x.abort))dlsym(h, "ncclCommAbort");
+    x.async_err = (decltype(x.async_err))dlsym(h, "ncclCommGetAsyncError");
+    x.ok = x.get_uid && x.init && x.bcast && x.destroy && x.err && x.abort && x.async_err;
     return x;
   }();
   return a;
@@ -204,6 +210,9 @@ static bool dims_from(const climber_config* cfg, Dims* D, std::string* why) {
   int dh = cfg->d / cfg->n_heads;
   if (dh != 16 && dh != 32 && dh != 64) { *why = "d_h must be 16, 32 or 64"; return false; }
   if (cfg->d % 32) { *why = "d must be a multiple of 32"; return false; }
+  // the row kernels (k_rmsnorm's per-lane buffer, the embedding kernels' norm
+  // partials) cover rows of at most 1024 columns
+  if (cfg->d > 1024) { *why = "d must be <= 1024"; return false; }
   if (cfg->n_layers < 1 || cfg->n_blocks < 1 || cfg->n_blocks > 8) { *why = "need L >= 1, 1 <= N_b <= 8"; return false; }
   if (cfg->n_k < 32 || cfg->n_k % 32 || cfg->n_k > 1024) { *why = "n_k must be a multiple of 32 in [32, 1024]"; return false; }
   if (cfg->ffn_mult < 1 || cfg->se_reduction < 1 || (cfg->n_blocks * cfg->d) % cfg->se_reduction ||
@@ -1199,6 +1208,8 @@ static climber_status stage_upload(climber_ctx_s* c, int B, bool with_ptab, cuda
 }
 
 static climber_status check_launch(climber_ctx_s* c, cudaStream_t s) {
+  char msg[256];
+  if (take_launch_error(msg, sizeof msg)) return fail(CLIMBER_E_CUDA, "launch setup: %s", msg);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(CLIMBER_E_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   if (c->sync_check) {
@@ -1456,33 +1467,78 @@ static size_t page_bytes(const climber_ctx_s* c);
 
 // replicate one user's K/V to every rank of the ctx's NCCL
 // group.  The root exports its handle into one slab (256 B header: config
-// fingerprint, v_k per block, scenario r; then the pages), one ncclBroadcast
-// over NVLink/NVSwitch replicates it, every other rank imports it into its own
-// page pool and receives a new handle in *kv.  Collective; synchronises
-// `stream` on the receivers (they read r from the header).
+// fingerprint, v_k per block, scenario r; then the pages and, with rel_bias,
+// the handle's bias state), one ncclBroadcast over NVLink/NVSwitch
+// replicates it, every other rank imports it into its own page pool and
+// receives a new handle in *kv.  Collective: every rank reaches the
+// broadcast, also when the root's export fails (it then sends an invalid
+// header and every receiver fails with E_STALE); the receivers wait for the
+// header with a deadline (CLIMBER_NCCL_TIMEOUT_MS, default 120 s) and abort
+// the communicator on timeout or on an asynchronous NCCL error.
+static climber_status nccl_abort(climber_ctx_s* c, const char* why) {
+  if (c->comm) nccl_api().abort(c->comm);
+  c->comm = nullptr;
+  return fail(CLIMBER_E_NCCL, "%s; communicator aborted", why);
+}
+
+// wait for `stream` with a deadline, watching the communicator's async error
+static climber_status nccl_wait(climber_ctx_s* c, cudaStream_t s) {
+  static const long long timeout_ms = [] {
+    const char* e = getenv("CLIMBER_NCCL_TIMEOUT_MS");
+    return e ? atoll(e) : 120000LL;
+  }();
+  cudaEvent_t ev;
+  CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CU(cudaEventRecord(ev, s));
+  const auto t0 = std::chrono::steady_clock::now();
+  climber_status st = CLIMBER_OK;
+  for (;;) {
+    cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) { st = fail(CLIMBER_E_CUDA, "broadcast wait: %s", cudaGetErrorString(q)); break; }
+    ncclResult_t ae = ncclSuccess;
+    nccl_api().async_err(c->comm, &ae);
+    if (ae != ncclSuccess && ae != ncclInProgress) { st = nccl_abort(c, nccl_api().err(ae)); break; }
+    if (std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count() >
+        timeout_ms) {
+      st = nccl_abort(c, "K/V broadcast timed out");
+      break;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+  cudaEventDestroy(ev);
+  return st;
+}
+
 extern "C" climber_status climber_kv_broadcast(climber_ctx_t c, climber_kv_t* kv, int32_t root,
                                                climber_stream_t stream) {
+  // checks that depend only on arguments every rank passes alike, so every
+  // rank returns before the collective or none does
   if (!c || !kv) return fail(CLIMBER_E_INVALID_ARG, "null argument");
   if (root < 0 || root >= c->world) return fail(CLIMBER_E_INVALID_ARG, "root out of range");
   if (c->world == 1 && !c->comm) return CLIMBER_OK;  // a single rank already holds it
-  if (!c->comm) return fail(CLIMBER_E_UNSUPPORTED, "ctx has no NCCL communicator");
+  if (!c->comm) return fail(CLIMBER_E_UNSUPPORTED, "ctx has no NCCL communicator (aborted or never created)");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const size_t bytes = climber_kv_slab_bytes(c);
   if (!c->bslab) CU(cudaMalloc(&c->bslab, bytes));
+  climber_status root_st = CLIMBER_OK;
   if (c->rank == root) {
-    climber_status st = climber_kv_export(c, *kv, c->bslab, stream);
-    if (st != CLIMBER_OK) return st;
+    root_st = climber_kv_export(c, *kv, c->bslab, stream);
+    // still join the collective: an invalid header tells the receivers
+    if (root_st != CLIMBER_OK) CU(cudaMemsetAsync(c->bslab, 0, 256, s));
   }
   ncclResult_t nr = nccl_api().bcast(c->bslab, c->bslab, bytes, ncclUint8, root, c->comm, s);
-  if (nr != ncclSuccess) return fail(CLIMBER_E_NCCL, "ncclBroadcast: %s", nccl_api().err(nr));
+  if (nr != ncclSuccess) return nccl_abort(c, nccl_api().err(nr));
   // CLIMBER_DEBUG_BCAST_SELF=1: the root also takes the receiver path (tests
   // the whole export -> broadcast -> import chain on one GPU)
   static const bool self_import = getenv("CLIMBER_DEBUG_BCAST_SELF") != nullptr;
-  if (c->rank == root && !self_import) return CLIMBER_OK;
-  int32_t r = 0;
-  CU(cudaMemcpyAsync(&r, (const char*)c->bslab + 28, 4, cudaMemcpyDeviceToHost, s));
-  CU(cudaStreamSynchronize(s));
-  return climber_kv_import(c, c->bslab, r, stream, kv);
+  if (c->rank == root && (!self_import || root_st != CLIMBER_OK)) return root_st;
+  climber_status ws = nccl_wait(c, s);
+  if (ws != CLIMBER_OK) return ws;
+  int32_t hdr[8];
+  CU(cudaMemcpy(hdr, c->bslab, sizeof hdr, cudaMemcpyDeviceToHost));
+  if (hdr[0] != 0x4B56534C) return fail(CLIMBER_E_STALE, "kv_broadcast: the root's export failed (no handle sent)");
+  return climber_kv_import(c, c->bslab, hdr[7], stream, kv);
 }
 
 extern "C" climber_status climber_nccl_unique_id(void* out) {
@@ -1497,13 +1553,37 @@ extern "C" climber_status climber_nccl_unique_id(void* out) {
 
 static size_t page_bytes(const climber_ctx_s* c) { return (size_t)2 * PAGE * c->D.d * c->esz; }
 
+// relative-bias state of one handle (rel_bias = 1): hage [N_b][n_k] int32 and
+// cbias [L][N_b][h][n_k] fp32, both contiguous per slot
+static size_t bias_state_bytes(const climber_ctx_s* c) {
+  if (!c->cfg.rel_bias) return 0;
+  const Dims& D = c->D;
+  return (size_t)D.Nb * D.nk * 4 + (size_t)D.L * D.Nb * D.h * D.nk * 4;
+}
+
 extern "C" size_t climber_kv_slab_bytes(climber_ctx_t c) {
-  return c ? 256 + (size_t)c->per_slot * page_bytes(c) : 0;
+  return c ? 256 + (size_t)c->per_slot * page_bytes(c) + bias_state_bytes(c) : 0;
+}
+
+static climber_status copy_bias_state(climber_ctx_s* c, int slot, char* slab, bool to_slab, cudaStream_t s) {
+  if (!c->cfg.rel_bias) return CLIMBER_OK;
+  const Dims& D = c->D;
+  const size_t hb = (size_t)D.Nb * D.nk * 4, cb = (size_t)D.L * D.Nb * D.h * D.nk * 4;
+  char* sec = slab + 256 + (size_t)c->per_slot * page_bytes(c);
+  char* h = reinterpret_cast<char*>(c->hage) + slot * hb;
+  char* cbs = reinterpret_cast<char*>(c->cbias) + slot * cb;
+  if (to_slab) {
+    CU(cudaMemcpyAsync(sec, h, hb, cudaMemcpyDeviceToDevice, s));
+    CU(cudaMemcpyAsync(sec + hb, cbs, cb, cudaMemcpyDeviceToDevice, s));
+  } else {
+    CU(cudaMemcpyAsync(h, sec, hb, cudaMemcpyDeviceToDevice, s));
+    CU(cudaMemcpyAsync(cbs, sec + hb, cb, cudaMemcpyDeviceToDevice, s));
+  }
+  return CLIMBER_OK;
 }
 
 extern "C" climber_status climber_kv_export(climber_ctx_t c, climber_kv_t kv, void* slab, climber_stream_t stream) {
   if (!c || !slab) return fail(CLIMBER_E_INVALID_ARG, "null argument");
-  if (c->cfg.rel_bias) return fail(CLIMBER_E_UNSUPPORTED, "K/V slabs do not carry the relative-bias state yet");
   if (reinterpret_cast<uintptr_t>(slab) % 16) return fail(CLIMBER_E_INVALID_ARG, "slab must be 16-byte aligned");
   int slot, r;
   {
@@ -1511,6 +1591,9 @@ extern "C" climber_status climber_kv_export(climber_ctx_t c, climber_kv_t kv, vo
     climber_status rs = resolve(c, kv, &slot);
     if (rs != CLIMBER_OK) return rs;
     r = c->slots[slot].r;
+    if (c->slots[slot].kb0 != 0 || c->slots[slot].kb1 != c->D.Nb)
+      return fail(CLIMBER_E_INVALID_ARG, "kv_export: the handle holds blocks [%d, %d) only (block-parallel encode)",
+                  c->slots[slot].kb0, c->slots[slot].kb1);
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   {
@@ -1518,13 +1601,14 @@ extern "C" climber_status climber_kv_export(climber_ctx_t c, climber_kv_t kv, vo
     launch_kv_export(c->pool, c->ptab, c->vlen_all, slot, c->per_slot, (long long)page_bytes(c), slab, c->D,
                      c->cfg.dtype, r, s);
   }
+  climber_status bs = copy_bias_state(c, slot, (char*)slab, true, s);
+  if (bs != CLIMBER_OK) return bs;
   return check_launch(c, s);
 }
 
 extern "C" climber_status climber_kv_import(climber_ctx_t c, const void* slab, int32_t scenario_r,
                                             climber_stream_t stream, climber_kv_t* out) {
   if (!c || !slab || !out) return fail(CLIMBER_E_INVALID_ARG, "null argument");
-  if (c->cfg.rel_bias) return fail(CLIMBER_E_UNSUPPORTED, "K/V slabs do not carry the relative-bias state yet");
   if (reinterpret_cast<uintptr_t>(slab) % 16) return fail(CLIMBER_E_INVALID_ARG, "slab must be 16-byte aligned");
   if (scenario_r < 0 || scenario_r >= c->D.R) return fail(CLIMBER_E_OUT_OF_RANGE, "scenario_r out of range");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -1560,6 +1644,8 @@ extern "C" climber_status climber_kv_import(climber_ctx_t c, const void* slab, i
     launch_kv_import(c->pool, c->ptab, c->vlen_all, slot, c->per_slot, (long long)page_bytes(c), slab, c->err, c->D,
                      c->cfg.dtype, s);
   }
+  climber_status bs = copy_bias_state(c, slot, (char*)const_cast<void*>(slab), false, s);
+  if (bs != CLIMBER_OK) return bs;
   return check_launch(c, s);
 }
 
@@ -2029,6 +2115,73 @@ extern "C" climber_status climber_debug_kv(climber_ctx_t c, climber_kv_t kv, int
   cudaFree(dk);
   cudaFree(dv);
   if (e1 != cudaSuccess || e2 != cudaSuccess) return fail(CLIMBER_E_CUDA, "debug_kv copy failed");
+  return CLIMBER_OK;
+}
+
+// Mask probe: the production attention kernel of `mode` run on the probe
+// pattern of launch_probe_pages (see include/climber.h).  Synchronous; the
+// handle's K/V of (layer, block) is overwritten.
+extern "C" climber_status climber_debug_attn_probe(climber_ctx_t c, climber_kv_t kv, int32_t mode, int32_t layer,
+                                                   int32_t block, int32_t M, int32_t key_off, float* out) {
+  if (!c || !out) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+  const Dims& D = c->D;
+  if ((mode != 0 && mode != 1) || layer < 0 || layer >= D.L || block < 0 || block >= D.Nb || key_off < 0)
+    return fail(CLIMBER_E_INVALID_ARG, "mode/layer/block/key_off");
+  if (mode == 1 && (M < 1 || M > D.Mmax)) return fail(CLIMBER_E_INVALID_ARG, "M out of [1, max_candidates]");
+  if (c->cfg.rel_bias) return fail(CLIMBER_E_UNSUPPORTED, "attn probe: rel_bias contexts add f_b to the scores");
+  int slot, r;
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    climber_status rs = resolve(c, kv, &slot);
+    if (rs != CLIMBER_OK) return rs;
+    r = c->slots[slot].r;
+    if (block < c->slots[slot].kb0 || block >= c->slots[slot].kb1)
+      return fail(CLIMBER_E_INVALID_ARG, "block not held by this handle");
+  }
+  CU(cudaDeviceSynchronize());
+  cudaStream_t s = 0;
+  const int64_t coff[2] = {0, (int64_t)M};
+  CU(cudaMemcpy(c->d_slots, &slot, 4, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(c->d_r, &r, 4, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(c->d_cand_off, coff, sizeof(coff), cudaMemcpyHostToDevice));
+  const long long rows = mode == 0 ? D.nk : M;
+  const bool b16 = c->cfg.dtype == CLIMBER_BF16;
+  if (b16) launch_probe_pages<bf16>((bf16*)c->pool, c->ptab, slot, block, layer, key_off, D, s);
+  else launch_probe_pages<float>((float*)c->pool, c->ptab, slot, block, layer, key_off, D, s);
+  if (mode == 0) {
+    CU(cudaMemsetAsync(c->QKV, 0, (size_t)rows * D.d * c->esz, s));
+  } else if (b16) {
+    launch_probe_qkv<bf16>((bf16*)c->QKV, rows, D, s);
+  } else {
+    launch_probe_qkv<float>((float*)c->QKV, rows, D, s);
+  }
+  CU(cudaMemsetAsync(c->O, 0, (size_t)rows * D.d * c->esz, s));
+  if (b16) {
+    if (mode == 0)
+      attn_hist_bf16(c, (const bf16*)c->QKV, c->d_slots, c->d_r, 1, (bf16*)c->O, block, layer, s);
+    else
+      attn_sumi_bf16(c, (const bf16*)c->QKV, M, c->d_cand_off, c->d_slots, c->d_r, 1, M, (bf16*)c->O, block, layer,
+                     s);
+  } else {
+    if (mode == 0)
+      launch_attn_hist<float>((const float*)c->QKV, c->d_slots, c->d_r, 1, (const float*)c->pool, c->ptab,
+                              c->vlen_all, c->tau, (float*)c->O, block, layer, D, s);
+    else
+      launch_attn_sumi<float>((const float*)c->QKV, c->d_cand_off, c->d_slots, c->d_r, 1, M, (const float*)c->pool,
+                              c->ptab, c->vlen_all, c->tau, (float*)c->O, block, layer, D, s);
+  }
+  c->launches += 4;
+  CU(cudaDeviceSynchronize());
+  std::vector<uint8_t> h((size_t)rows * D.d * c->esz);
+  CU(cudaMemcpy(h.data(), c->O, h.size(), cudaMemcpyDeviceToHost));
+  for (long long i = 0; i < rows * D.d; ++i) {
+    if (b16) {
+      uint32_t u = (uint32_t)reinterpret_cast<const uint16_t*>(h.data())[i] << 16;
+      memcpy(out + i, &u, 4);
+    } else {
+      out[i] = reinterpret_cast<const float*>(h.data())[i];
+    }
+  }
   return CLIMBER_OK;
 }
 

@@ -1096,14 +1096,10 @@ static void launch_pe(const CUtensorMap& mq, const CUtensorMap& mkv, const Args&
   // CLIMBER_ATTN_1CTA=1 (measurement knob): request enough smem for 1 CTA/SM
   static const int smem = getenv("CLIMBER_ATTN_1CTA") ? 150 * 1024 : Lay<DH>::TOTAL;
   constexpr int smem_b = Lay<DH>::TOTAL + 3072;  // + the staged relative-bias tables and 2-D lookup
-  static bool attr = false;
   static const bool es = [] { const char* e = getenv("CLIMBER_ATTN_EARLY_S"); return !(e && atoi(e) == 0); }();
-  if (!attr) {
-    cudaFuncSetAttribute(k_attn_tc<DH, MODE, PE8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_attn_tc<DH, MODE, PE8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_attn_tc<DH, MODE, PE8, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_b);
-    attr = true;
-  }
+  ensure_smem_attr((const void*)k_attn_tc<DH, MODE, PE8, 0>, smem);
+  ensure_smem_attr((const void*)k_attn_tc<DH, MODE, PE8, 1>, smem);
+  ensure_smem_attr((const void*)k_attn_tc<DH, MODE, PE8, 1, 1>, smem_b);
   if (a.D.bpos) k_attn_tc<DH, MODE, PE8, 1, 1><<<grid, THREADS, smem_b, s>>>(mq, mkv, a);
   else if (es) k_attn_tc<DH, MODE, PE8, 1><<<grid, THREADS, smem, s>>>(mq, mkv, a);
   else k_attn_tc<DH, MODE, PE8, 0><<<grid, THREADS, smem, s>>>(mq, mkv, a);
@@ -1161,8 +1157,11 @@ void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, 
                          const int* vlen_all, const float* tau, bf16* O, int k, int l, const Dims& D, cudaStream_t s,
                          int nbk) {
   CUtensorMap mq, mkv;
-  at::map2d(&mq, QKV, P * nbk, 3 * D.d, 3LL * D.d, D.dh, at::ROWS);
-  at::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, at::KEYS);
+  if (!at::map2d(&mq, QKV, P * nbk, 3 * D.d, 3LL * D.d, D.dh, at::ROWS) ||
+      !at::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, at::KEYS)) {
+    note_launch_error("SUMI attention: cuTensorMapEncodeTiled rejected a map (kernel not launched)");
+    return;
+  }
   at::Args a{QKV, cand_off, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, U, P, D, nullptr};
   dim3 grid((Mmax + at::ROWS - 1) / at::ROWS, D.h, U * nbk);
   if (at::use_pt() && !D.bpos) {
@@ -1214,8 +1213,11 @@ void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r,
                          long long pool_rows, const int* ptab, const int* vlen_all, const float* tau, bf16* O, int k,
                          int l, const Dims& D, cudaStream_t s, int nbk) {
   CUtensorMap mq, mkv;
-  at::map2d(&mq, Q, (long long)U * D.nk * nbk, D.d, D.d, D.dh, at::ROWS);
-  at::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, at::KEYS);
+  if (!at::map2d(&mq, Q, (long long)U * D.nk * nbk, D.d, D.d, D.dh, at::ROWS) ||
+      !at::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, at::KEYS)) {
+    note_launch_error("history attention: cuTensorMapEncodeTiled rejected a map (kernel not launched)");
+    return;
+  }
   at::Args a{Q, nullptr, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, U, (long long)U * D.nk, D, nullptr};
   dim3 grid(D.nk / at::ROWS, D.h, U * nbk);
   if (at::use_pt() && !D.bpos) {

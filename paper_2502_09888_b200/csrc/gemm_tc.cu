@@ -480,31 +480,31 @@ template <int BN, int STAGES, int EPIW, int SBUF, int NORM = 0, int CG = 1>
 static void launch(const bf16* A, long long lda, long long abs_, const bf16* B, long long ldb, long long bbs,
                    long long M, int N, int K, int batch, const Epilogue& e, cudaStream_t s) {
   CUtensorMap ma, mb, md, mp, mc;
-  make_map(&ma, A, M, K, lda, BM, BK, false, false, batch, abs_);
-  make_map(&mb, B, N, K, ldb, BN / CG, BK, false, false, batch, bbs);
+  bool ok = make_map(&ma, A, M, K, lda, BM, BK, false, false, batch, abs_);
+  ok = ok && make_map(&mb, B, N, K, ldb, BN / CG, BK, false, false, batch, bbs);
   mp = ma;  // unused unless QKV_PAGES
   mc = ma;  // unused unless RESID_NORM
-  if (e.kind == EPI_RESID_NORM) make_map(&mc, e.out_b16, M, N, e.ldo, 32, 32, false, true, batch, e.out_b16_bs);
+  if (e.kind == EPI_RESID_NORM) ok = ok && make_map(&mc, e.out_b16, M, N, e.ldo, 32, 32, false, true, batch, e.out_b16_bs);
   if (e.kind == EPI_QKV_PAGES) {
     if (e.d % 64 == 0) {
-      make_map(&md, e.out, M, e.d, e.ldo, 32, 64, false, false, batch, e.out_bs);  // Q buffer [b][M][d]
-      make_map(&mp, e.pool, e.pool_rows, e.d, e.d, 32, 64, false);                  // pages as [n_pages*2*64][d]
+      ok = ok && make_map(&md, e.out, M, e.d, e.ldo, 32, 64, false, false, batch, e.out_bs);  // Q buffer [b][M][d]
+      ok = ok && make_map(&mp, e.pool, e.pool_rows, e.d, e.d, 32, 64, false);  // pages as [n_pages*2*64][d]
     } else {
       md = ma;
     }
   } else if (e.kind == EPI_STORE) {
-    make_map(&md, e.out, M, N, e.ldo, 32, 64, false, false, batch, e.out_bs);
+    ok = ok && make_map(&md, e.out, M, N, e.ldo, 32, 64, false, false, batch, e.out_bs);
   } else {
-    make_map(&md, e.out, M, N, e.ldo, 32, 32, true, false, batch, e.out_bs);
+    ok = ok && make_map(&md, e.out, M, N, e.ldo, 32, 32, true, false, batch, e.out_bs);
+  }
+  if (!ok) {
+    note_launch_error("tcgen05 GEMM: cuTensorMapEncodeTiled rejected an operand map (kernel not launched)");
+    return;
   }
   constexpr int smem = Smem<BN, STAGES, EPIW, SBUF, NORM, CG>::TOTAL;
   static_assert(smem <= 232448, "smem");
   auto kern = k_gemm_tc<BN, STAGES, EPIW, SBUF, NORM, CG>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  ensure_smem_attr((const void*)kern, smem);
   const long long tiles = ((M + CG * BM - 1) / (CG * BM)) * (N / BN) * batch;  // per CTA (pair)
   const long long slots = num_sms() / CG;
   const int grid = (int)(tiles < slots ? tiles : slots) * CG;

@@ -1,3 +1,7 @@
+#include <mutex>
+#include <set>
+#include <string>
+#include <cstdio>
 // Non-GEMM kernels of the SUMI hot path (SURVEY §8(a) rows a1, a2, a4/a5
 // attention, a6 head) and the SIMT GEMM used by the fp32 verification build.
 //
@@ -7,6 +11,32 @@
 #include "kernels.cuh"
 
 namespace climber {
+
+static std::mutex g_launch_mu;
+static std::string g_launch_err;
+static std::set<std::pair<const void*, int>> g_attr_done;
+
+void note_launch_error(const char* what) {
+  std::lock_guard<std::mutex> g(g_launch_mu);
+  if (g_launch_err.empty()) g_launch_err = what;
+}
+
+bool take_launch_error(char* msg, int cap) {
+  std::lock_guard<std::mutex> g(g_launch_mu);
+  if (g_launch_err.empty()) return false;
+  snprintf(msg, cap, "%s", g_launch_err.c_str());
+  g_launch_err.clear();
+  return true;
+}
+
+void ensure_smem_attr(const void* kern, int bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(g_launch_mu);
+  if (g_attr_done.insert({kern, dev}).second)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
 
 // ===========================================================================
 // a1: validation + multi-scale sequence extraction (Eq. 2)
@@ -689,6 +719,53 @@ __global__ void k_debug_kv(const T* __restrict__ pool, const int* __restrict__ p
   }
 }
 
+// Mask probe (climber_debug_attn_probe): K = 0 and V[j] = one-hot on every
+// page slot of one (user, block, layer), so that the production attention
+// kernel, run on zero queries, gives every attended key weight 1/|set| and
+// its output channel reveals which keys it read.  Head h maps key
+// key_off + h (d_h - 1) + c to channel c < d_h - 1; channel d_h - 1 is left
+// for the SUMI self term.  Every slot of the pages is written, pads included,
+// so a kernel that reads past v_k shows it.
+template <typename T>
+__global__ void k_probe_pages(T* __restrict__ pool, const int* __restrict__ ptab, int slot, int k, int l,
+                              int key_off, Dims D) {
+  const int* pages = ptab + (((long long)slot * D.Nb + k) * D.L + l) * D.ppb;
+  const long long n = (long long)D.ppb * PAGE * D.d;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(g / D.d), col = (int)(g % D.d);
+    const int head = col / D.dh, c = col % D.dh;
+    const int page = pages[t / PAGE];
+    const bool hit = c < D.dh - 1 && t == key_off + head * (D.dh - 1) + c;
+    pool[page_elem_offset(page, 0, head, t % PAGE, c, D.d, D.dh)] = T(0.f);
+    pool[page_elem_offset(page, 1, head, t % PAGE, c, D.d, D.dh)] = T(hit ? 1.f : 0.f);
+  }
+}
+
+// SUMI probe rows: q = k_self = 0, v_self = e_{d_h - 1} per head
+template <typename T>
+__global__ void k_probe_qkv(T* __restrict__ QKV, long long rows, Dims D) {
+  const long long n = rows * 3 * D.d;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int col = (int)(g % (3 * D.d));
+    QKV[g] = T((col >= 2 * D.d && (col - 2 * D.d) % D.dh == D.dh - 1) ? 1.f : 0.f);
+  }
+}
+
+template <typename T>
+void launch_probe_pages(T* pool, const int* ptab, int slot, int k, int l, int key_off, const Dims& D, cudaStream_t s) {
+  k_probe_pages<T><<<296, 256, 0, s>>>(pool, ptab, slot, k, l, key_off, D);
+}
+template <typename T>
+void launch_probe_qkv(T* QKV, long long rows, const Dims& D, cudaStream_t s) {
+  k_probe_qkv<T><<<296, 256, 0, s>>>(QKV, rows, D);
+}
+template void launch_probe_pages<bf16>(bf16*, const int*, int, int, int, int, const Dims&, cudaStream_t);
+template void launch_probe_pages<float>(float*, const int*, int, int, int, int, const Dims&, cudaStream_t);
+template void launch_probe_qkv<bf16>(bf16*, long long, const Dims&, cudaStream_t);
+template void launch_probe_qkv<float>(float*, long long, const Dims&, cudaStream_t);
+
 // K/V slab export / import (multi-GPU candidate sharding): 16-byte copies of
 // the handle's pages in page-table order, behind a 256-byte header.
 constexpr int SLAB_MAGIC = 0x4B56534C;  // "KVSL"
@@ -697,9 +774,10 @@ __global__ void k_kv_export(const uint4* __restrict__ pool, const int* __restric
                             int slot, int per_slot, long long page_vec, int* __restrict__ hdr, uint4* __restrict__ body,
                             Dims D, int dtype, int r) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    hdr[0] = SLAB_MAGIC; hdr[1] = 1; hdr[2] = D.Nb; hdr[3] = D.L; hdr[4] = D.ppb; hdr[5] = D.d; hdr[6] = dtype;
+    hdr[0] = SLAB_MAGIC; hdr[1] = 2; hdr[2] = D.Nb; hdr[3] = D.L; hdr[4] = D.ppb; hdr[5] = D.d; hdr[6] = dtype;
     hdr[7] = r;  // the handle's request scenario (for climber_kv_broadcast's receivers)
     for (int k = 0; k < D.Nb; ++k) hdr[8 + k] = vlen_all[(long long)slot * D.Nb + k];
+    hdr[16] = D.hage != nullptr;  // version 2: relative-bias state (hage, cbias rows) follows the pages
   }
   const long long n = (long long)per_slot * page_vec;
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += (long long)gridDim.x * blockDim.x) {
@@ -711,8 +789,8 @@ __global__ void k_kv_export(const uint4* __restrict__ pool, const int* __restric
 __global__ void k_kv_import(uint4* __restrict__ pool, const int* __restrict__ ptab, int* __restrict__ vlen_all, int slot,
                             int per_slot, long long page_vec, const int* __restrict__ hdr, const uint4* __restrict__ body,
                             int* __restrict__ err, Dims D, int dtype) {
-  const bool ok = hdr[0] == SLAB_MAGIC && hdr[1] == 1 && hdr[2] == D.Nb && hdr[3] == D.L && hdr[4] == D.ppb &&
-                  hdr[5] == D.d && hdr[6] == dtype;
+  const bool ok = hdr[0] == SLAB_MAGIC && hdr[1] == 2 && hdr[2] == D.Nb && hdr[3] == D.L && hdr[4] == D.ppb &&
+                  hdr[5] == D.d && hdr[6] == dtype && hdr[16] == (D.hage != nullptr);
   if (!ok) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       atomicOr(err, ERR_CONFIG);

@@ -4,6 +4,15 @@
 
 namespace climber {
 
+// Host-side launch setup failures (a tensor map the driver rejects): the
+// kernel is NOT launched, the failure is recorded, and the next status check
+// of the C-ABI call (check_launch) returns CLIMBER_E_CUDA with the message.
+void note_launch_error(const char* what);
+bool take_launch_error(char* msg, int cap);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute is per device, so a process driving several GPUs sets it on each.
+void ensure_smem_attr(const void* kern, int bytes);
+
 struct EventsDev {
   const int32_t* item;
   const uint8_t* action;
@@ -54,6 +63,11 @@ void launch_debug_mask(const int* vlen_all, int slot, int M, uint8_t* mask, cons
 template <typename T>
 void launch_debug_kv(const T* pool, const int* ptab, const int* vlen_all, int slot, int k, int l, T* K, T* V,
                      const Dims& D, cudaStream_t s);
+// mask probe (climber_debug_attn_probe)
+template <typename T>
+void launch_probe_pages(T* pool, const int* ptab, int slot, int k, int l, int key_off, const Dims& D, cudaStream_t s);
+template <typename T>
+void launch_probe_qkv(T* QKV, long long rows, const Dims& D, cudaStream_t s);
 void launch_kv_export(const void* pool, const int* ptab, const int* vlen_all, int slot, int per_slot, long long page_bytes,
                       void* slab, const Dims& D, int dtype, int r, cudaStream_t s);
 void launch_kv_import(void* pool, const int* ptab, int* vlen_all, int slot, int per_slot, long long page_bytes,

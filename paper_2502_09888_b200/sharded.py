@@ -116,6 +116,34 @@ def rank_request_sharded(backend, dist, events, r: int, items, root: int = 0):
     return out
 
 
+def rank_request_sharded_lib(cl, dist, events, r: int, items, root: int = 0):
+    """Candidate sharding with the K/V replicated by the library itself
+    (climber_kv_broadcast: export, ncclBroadcast on the ctx's communicator,
+    import) instead of the process group.  `cl` is a Climber created with this
+    rank's (rank, world, nccl_uid).  Same return convention as
+    rank_request_sharded."""
+    torch = cl.torch
+    G, rank = dist.get_world_size(), dist.get_rank()
+    M = int(items.numel())
+    handle = cl.encode_user(*events, r) if rank == root else None
+    handle = cl.kv_broadcast(handle, root)
+    lo, hi = shard_bounds(M, G, rank)
+    width = -(-M // G)
+    part = torch.full((width,), float("nan"), dtype=torch.float32, device=items.device)
+    if hi > lo:
+        part[:hi - lo] = cl.score_items(handle, items[lo:hi])
+    parts = [torch.empty_like(part) for _ in range(G)]
+    dist.all_gather(parts, part)
+    cl.release(handle)
+    if rank != root:
+        return None
+    out = torch.empty(M, dtype=torch.float32, device=items.device)
+    for g in range(G):
+        a, b = shard_bounds(M, G, g)
+        out[a:b] = parts[g][:b - a]
+    return out
+
+
 # ---------------------------------------------------------------------------
 # block-parallel serving (SURVEY §8(f) NEXT-2; PAPER.md L155 "block-parallel
 # KV cache", L203: the N_b blocks are independent until the fusion step)

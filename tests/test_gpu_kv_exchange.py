@@ -302,3 +302,63 @@ print("ok")
     env = dict(os.environ, CLIMBER_DEBUG_BCAST_SELF="1")
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_export_import_carries_relative_bias_state():
+    # rel_bias = 1 slabs carry the handle's token ages and candidate-row bias
+    # (version-2 slab): the imported handle scores bit-identically
+    cfg = synth.preset("medium", rel_bias=1)
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 5, B=1)
+    a = make_gpu(cfg, w, 1, kv_users=2)
+    b = make_gpu(cfg, w, 1, kv_users=2)
+    item, action, scenario, ts, cand = to_dev(batch)
+    ha = a.encode_user(item, action, scenario, ts, int(batch.r[0]))
+    sa = a.score_items(ha, cand).cpu().numpy()
+    hb = b.kv_import(a.kv_export(ha), int(batch.r[0]))
+    sb = b.score_items(hb, cand).cpu().numpy()
+    a.stream_status()
+    b.stream_status()
+    assert np.array_equal(sa, sb)
+    # a ctx without the bias rejects the slab (header flag)
+    c0 = synth.preset("medium")
+    c = make_gpu(c0, synth.make_weights(c0, 0), 1, kv_users=2)
+    import torch
+    from paper_2502_09888_b200 import ClimberError
+    slab = a.kv_export(ha)
+    big = torch.zeros(c.slab_bytes, dtype=torch.uint8, device="cuda")
+    big[:] = slab[:big.numel()]
+    c.kv_import(big, int(batch.r[0]))
+    with pytest.raises(ClimberError) as ei:
+        c.stream_status()
+    assert ei.value.name == "E_CONFIG"
+
+
+def test_export_rejects_block_range_handle_and_broadcast_failure_is_symmetric():
+    # a block-range handle holds K/V only for its blocks -> export
+    # refuses; a failed root export still joins the broadcast (world-1
+    # communicator) and the communicator stays usable afterwards
+    import torch
+    from paper_2502_09888_b200 import ClimberError, nccl_unique_id
+    cfg = synth.preset("medium")
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 5, B=1)
+    cl = make_gpu(cfg, w, 1, kv_users=3, rank=0, world=1, nccl_uid=nccl_unique_id())
+    item, action, scenario, ts, cand = to_dev(batch)
+    hp = cl.encode_users_blocks(batch.ev_offsets, item, action, scenario, ts, batch.r, 0, 2)[0]
+    with pytest.raises(ClimberError) as ei:
+        cl.kv_export(hp)
+    assert ei.value.name == "E_INVALID_ARG"
+    with pytest.raises(ClimberError) as ei:
+        cl.kv_broadcast(hp, root=0)
+    assert ei.value.name == "E_INVALID_ARG"
+    cl.release([hp])
+    with pytest.raises(ClimberError) as ei:
+        cl.kv_broadcast(hp, root=0)               # released: stale
+    assert ei.value.name == "E_STALE"
+    h = cl.encode_user(item, action, scenario, ts, int(batch.r[0]))
+    ref = cl.score_items(h, cand)
+    assert cl.kv_broadcast(h, root=0) == h        # the communicator still works
+    assert torch.equal(cl.score_items(h, cand), ref)
+    cl.release(h)
+    cl.stream_status()
