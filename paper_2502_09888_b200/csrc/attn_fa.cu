@@ -1,0 +1,606 @@
+// tcgen05/TMEM flash attention for the bf16 path (Eq. 3 with f_b = 0;
+// SUMI masks P:L255): softmax(q.k / (sqrt(d_h) tau)) v.
+//
+//   MODE_SUMI: a tile of 128 candidates of one (user, block, head) attends to
+//              the v cached history keys of its (block, layer) plus itself.
+//   MODE_HIST: 128 history rows of one (user, block, head) attend keys j <= t
+//              (causal) or j < v (bidirectional).
+//
+// CTA = 8 warps, one 128-row query tile (TMEM lane = query row), keys in
+// chunks of 128 (two 64-token pages); two CTAs per SM, so one CTA's prologue
+// (q tiles) and epilogue overlap the other's chunks.
+//   warp 0      K producer (TMA): q (+ SUMI k_self, v_self, parked in the last
+//               K / V stages until the self term is read) once, then K of each
+//               chunk into a three-stage ring, freed as soon as its Q K^T
+//               completes
+//   warp 3      V producer: V of each chunk into a two-stage ring, freed when
+//               its P V completes (K runs ahead of V: Q K_{j+1}^T is needed
+//               before P(j) V_j)
+//   warp 1      MMA issuer (one thread): S(j+1) = Q K_{j+1}^T (M=128, N=128,
+//               K=d_h) as soon as the softmax has loaded S(j) into registers,
+//               so it runs under the exponentials of chunk j; O += P(j) V_j
+//               (M=128, N=d_h, K=128; P read from TMEM, V an MN-major smem
+//               operand) once P(j) is written
+//   warp 2      TMEM allocator (256 columns: S [0,128), P [128,192) (bf16
+//               pairs), O [192, 192+d_h))
+//   warps 4-7   softmax, one thread per query row, the whole 128-key S row in
+//               registers: row max, lazy online rescale (O is rescaled only
+//               when the row max grows by > 2^8), P = 2^(s sc - m) (PE of every
+//               8 on an FMA-pipe polynomial, the rest on the MUFU), packed to
+//               bf16 into TMEM, fp32 row sum with packed FADD2
+//   epilogue    O / l -> bf16, staged in the (then idle) q buffer, coalesced
+//               row stores
+// The SUMI self term initialises the row state (m = s_self, l = 1, O = v_self),
+// so no candidate ever reads another candidate's K/V.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+
+#include "kernels.cuh"
+#include "tc_util.cuh"
+
+namespace climber {
+namespace fa {
+using namespace tcu;
+
+constexpr int ROWS = 128;      // query rows per CTA (TMEM lanes)
+constexpr int KEYS = 128;      // keys per chunk (two pages)
+constexpr int KST = 3;         // K ring stages
+constexpr int VST = 2;         // V ring stages
+constexpr int THREADS = 256;
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float RESCALE_LOG2 = 8.0f;
+enum { MODE_SUMI = 0, MODE_HIST = 1 };
+
+template <int DH>
+struct Lay {
+  static constexpr int RB = DH * 2;                       // bytes per q/k/v row (one swizzle atom)
+  static constexpr uint32_t SWZ = (DH == 64) ? 2u : 4u;   // descriptor swizzle: 128B / 64B
+  static constexpr int TILE_B = ROWS * RB;                // the q tile (also k_self, v_self)
+  static constexpr int KV_B = KEYS * RB;                  // K (or V) of one chunk
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = Q_OFF + TILE_B;            // [KST] K chunks
+  static constexpr int V_OFF = K_OFF + KST * KV_B;        // [VST] V chunks
+  static constexpr int BAR_OFF = V_OFF + VST * KV_B;
+  static constexpr int PG_OFF = BAR_OFF + 256;            // page ids of the (user, block, layer), <= 32
+  static constexpr int TOTAL = PG_OFF + 128 + 1024;       // + 1024 B alignment slack
+  // SUMI: k_self / v_self are parked in the last K and V stages until the self term is read
+  static constexpr int KS_OFF = K_OFF + (KST - 1) * KV_B;
+  static constexpr int VS_OFF = V_OFF + (VST - 1) * KV_B;
+  static_assert(KV_B == TILE_B, "a self tile is one K (or V) stage");
+  __device__ static constexpr int k_off(int j) { return K_OFF + (j % KST) * KV_B; }
+  __device__ static constexpr int v_off(int j) { return V_OFF + (j % VST) * KV_B; }
+};
+
+struct Args {
+  const bf16* Q;  // SUMI: QKV [P][3d] (q | k_self | v_self); HIST: Q [U*nk][d]
+  const int64_t* cand_off;
+  const int* wave_slot;
+  const int* wave_r;
+  const int* ptab;
+  const int* vlen_all;
+  const float* tau;
+  bf16* O;        // [rows][d]
+  int k, l;       // first block, layer
+  int U;          // users in the wave
+  long long rows_pb;  // grouped over nbk blocks: block kk's rows start at kk * rows_pb in Q/QKV and O
+  Dims D;
+  unsigned long long* trace;  // clock64 timeline per CTA (CLIMBER_FA_TRACE), nullptr normally
+};
+// trace slots per CTA: [2j] softmax saw S(j), [40 + j] its S row loaded,
+// [52 + j] max / rescale done, [2j + 1] it released P(j) (j < 12); [30 / 31]
+// epilogue start / end; [64 + j] MMA thread saw P(j);
+// [96 + j] MMA thread saw K/V chunk j; [126] q tiles seen; [127] start
+constexpr int TRACE_N = 128;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// 2^x on the FMA pipe: x = j + f, j = rne(x), f in [-1/2, 1/2]; 2^f by a
+// degree-3 fit (max rel. error 7.5e-5, below the bf16 rounding of P), 2^j
+// added to the exponent field with one integer multiply-add
+__device__ __forceinline__ float ex2_poly(float x) {
+  constexpr float MAGIC = 12582912.f;  // 1.5 * 2^23
+  const float xc = fmaxf(x, -125.f);
+  const float t = xc + MAGIC;
+  const float f = xc - (t - MAGIC);
+  const float p = fmaf(fmaf(fmaf(0.055171628f, f, 0.24261117f), f, 0.69326103f), f, 0.99992806f);
+  const float y = __int_as_float(__float_as_int(t) * (1 << 23) + __float_as_int(p));
+  return x < -125.f ? 0.f : y;  // masked keys (-inf) give exactly 0, like the MUFU
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float max3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+// 16-byte chunk j of staged row `row` (the TMA box swizzle: 128B or 64B pattern)
+template <int DH>
+__device__ __forceinline__ int swz(int row, int j) {
+  return (DH == 64) ? (j ^ (row & 7)) : (j ^ ((row >> 1) & 3));
+}
+
+template <int DH, int MODE, int PE>
+__global__ void __launch_bounds__(THREADS, 2)
+    k_attn_fa(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, Args a) {
+  using Ly = Lay<DH>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Ly::BAR_OFF);
+  uint64_t* bar_q = bars;
+  uint64_t* k_full = bars + 1;                // [KST]
+  uint64_t* k_empty = k_full + KST;           // [KST]
+  uint64_t* v_full = k_empty + KST;           // [VST]
+  uint64_t* v_empty = v_full + VST;           // [VST]
+  uint64_t* s_full = v_empty + VST;           // S(j) written
+  uint64_t* s_read = s_full + 1;              // S(j) loaded by the softmax (S columns free)
+  uint64_t* p_full = s_read + 1;              // P(j) written
+  uint64_t* pv_done = p_full + 1;             // P(j) V_j complete (P columns free, O current)
+  uint64_t* self_done = pv_done + 1;          // SUMI: k_self / v_self read (their stages are free)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(self_done + 1);
+  int* spg = reinterpret_cast<int*>(smem + Ly::PG_OFF);
+
+  const Dims& D = a.D;
+  const int u = blockIdx.z % a.U, head = blockIdx.y, tile0 = blockIdx.x * ROWS;
+  const int kk = blockIdx.z / a.U;
+  const int kblk = a.k + kk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = a.wave_slot[u];
+  const int r = a.wave_r[u];
+  const int v = a.vlen_all[(long long)slot * D.Nb + kblk];
+  const int* pages = a.ptab + (((long long)slot * D.Nb + kblk) * D.L + a.l) * D.ppb;
+  const float sc = LOG2E / (sqrtf((float)DH) * a.tau[((a.l * D.Nb + kblk) * D.R + r) * D.h + head]);
+
+  // tile geometry (CTA-uniform)
+  int n_rows, n_out, kend;
+  long long rbase;
+  if (MODE == MODE_SUMI) {
+    const long long p0 = a.cand_off[u], p1 = a.cand_off[u + 1];
+    if (p0 + tile0 >= p1) return;
+    n_rows = (int)min((long long)ROWS, p1 - p0 - tile0);
+    n_out = n_rows;
+    kend = v;
+    rbase = kk * a.rows_pb + p0 + tile0;
+  } else {
+    if (tile0 >= D.nk) return;
+    n_rows = max(0, min(ROWS, v - tile0));
+    n_out = min(ROWS, D.nk - tile0);
+    kend = D.causal ? min(v, tile0 + ROWS) : v;
+    rbase = kk * a.rows_pb + (long long)u * D.nk + tile0;
+  }
+  const int nch = (MODE == MODE_SUMI || n_rows > 0) ? (kend + KEYS - 1) / KEYS : 0;
+  const bool need_q = MODE == MODE_SUMI || nch > 0;
+  const int n_pages = min(D.ppb, (nch * KEYS + PAGE - 1) / PAGE);
+
+  if (warp == 0) {
+    for (int i = lane; i < n_pages; i += 32) spg[i] = pages[i];
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmQ) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmKV) : "memory");
+      mbar_init(bar_q, 1);
+      for (int s = 0; s < KST; ++s) {
+        mbar_init(&k_full[s], 1);
+        mbar_init(&k_empty[s], 1);
+      }
+      for (int s = 0; s < VST; ++s) {
+        mbar_init(&v_full[s], 1);
+        mbar_init(&v_empty[s], 1);
+      }
+      mbar_init(s_full, 1);
+      mbar_init(s_read, 128);
+      mbar_init(p_full, 128);
+      mbar_init(pv_done, 1);
+      mbar_init(self_done, 128);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      // the query-side tiles go out first: their round trip heads every CTA's critical path
+      if (need_q) {
+        mbar_expect_tx(bar_q, (MODE == MODE_SUMI ? 3 : 1) * Ly::TILE_B);
+        tma_load_2d(smem + Ly::Q_OFF, &tmQ, bar_q, head * DH, (int)rbase);
+        if (MODE == MODE_SUMI) {
+          tma_load_2d(smem + Ly::KS_OFF, &tmQ, bar_q, D.d + head * DH, (int)rbase);
+          tma_load_2d(smem + Ly::VS_OFF, &tmQ, bar_q, 2 * D.d + head * DH, (int)rbase);
+        }
+      }
+    }
+  } else if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tS = tmem_base;                 // S(j)
+  const uint32_t tP = tmem_base + KEYS;          // P(j), bf16 pairs
+  const uint32_t tO = tmem_base + KEYS + KEYS / 2;  // O [DH]
+  unsigned long long* tr = a.trace ? a.trace + ((long long)(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x +
+                                                blockIdx.x) * TRACE_N
+                                   : nullptr;
+  if (tr && threadIdx.x == 0) tr[127] = clock64();
+
+  if (warp < 4) {
+    // the control warpgroup hands registers to the softmax warpgroup (whole S
+    // rows live in registers): 128 x 64 + 128 x 192 = 256 x 128
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
+    if ((warp == 0 || warp == 3) && lane == 0) {
+      // ---------------- TMA producers: K (warp 0) and V (warp 3) of chunk j, two pages each ----------------
+      const bool is_k = warp == 0;
+      const int nst = is_k ? KST : VST;
+      uint64_t* full = is_k ? k_full : v_full;
+      uint64_t* empty = is_k ? k_empty : v_empty;
+      const int kv = is_k ? 0 : 1;
+      for (int j = 0; j < nch; ++j) {
+        const int st = j % nst;
+        mbar_wait(&empty[st], ((j / nst) & 1) ^ 1);
+        if (MODE == MODE_SUMI && j == nst - 1) mbar_wait(self_done, 0);  // the last stage held a self tile
+        const int pa = spg[2 * j];
+        const int pb = (2 * j + 1 < n_pages) ? spg[2 * j + 1] : pa;  // past the pages: finite, masked keys
+        mbar_expect_tx(&full[st], Ly::KV_B);
+        uint8_t* dst = smem + (is_k ? Ly::k_off(j) : Ly::v_off(j));
+        tma_load_2d(dst, &tmKV, &full[st], head * DH, (int)page_row(pa, kv, 0));
+        tma_load_2d(dst + PAGE * Ly::RB, &tmKV, &full[st], head * DH, (int)page_row(pb, kv, 0));
+      }
+    } else if (warp == 1 && lane == 0 && nch > 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t idesc_qk = idesc_bf16_major(ROWS, KEYS, 0, 0);
+      constexpr uint32_t idesc_pv = idesc_bf16_major(ROWS, DH, 0, 1);
+      const uint64_t qd = make_sdesc(smem_u32(smem + Ly::Q_OFF), 16, 8 * Ly::RB, Ly::SWZ);
+      auto qk = [&](int j) {
+        mbar_wait(&k_full[j % KST], (j / KST) & 1);
+        fence_after();
+        if (tr && j < 16) tr[96 + j] = clock64();
+        const uint64_t kd = make_sdesc(smem_u32(smem + Ly::k_off(j)), 16, 8 * Ly::RB, Ly::SWZ);
+#pragma unroll
+        for (int s = 0; s < DH / 16; ++s) mma_bf16(tS, qd + 2 * s, kd + 2 * s, idesc_qk, s > 0 ? 1u : 0u);
+        mma_commit(&k_empty[j % KST]);
+        mma_commit(s_full);
+      };
+      mbar_wait(bar_q, 0);
+      qk(0);
+      for (int j = 0; j < nch; ++j) {
+        if (j + 1 < nch) {  // S(j+1) as soon as S(j) is in the softmax's registers
+          mbar_wait(s_read, j & 1);
+          fence_after();
+          qk(j + 1);
+        }
+        mbar_wait(p_full, j & 1);
+        fence_after();
+        if (tr && j < 12) tr[64 + j] = clock64();
+        mbar_wait(&v_full[j % VST], (j / VST) & 1);
+        fence_after();
+        const uint64_t vd = make_sdesc(smem_u32(smem + Ly::v_off(j)), 16, 8 * Ly::RB, Ly::SWZ);
+#pragma unroll 1
+        for (int s = 0; s < KEYS / 16; ++s) {
+          const uint64_t vds = vd + (uint64_t)((16 * Ly::RB) >> 4) * s;  // 16 keys = 2 groups of 8 rows
+          const uint32_t acc = (MODE == MODE_SUMI || j > 0 || s > 0) ? 1u : 0u;
+          mma_bf16_ts(tO, tP + 8 * s, vds, idesc_pv, acc);  // 16 keys of P = 8 packed columns
+        }
+        mma_commit(&v_empty[j % VST]);
+        mma_commit(pv_done);
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 192;");
+    // ---------------- softmax + epilogue ----------------
+    const int ew = warp & 3;            // TMEM lane quadrant of this warp
+    const int row = ew * 32 + lane;     // query row = TMEM lane
+    const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
+    const bool valid = row < n_rows;
+    const int t_row = tile0 + row;      // HIST: this row's position in the subsequence
+    float m_used = -INFINITY, l = 0.f;
+    unsigned long long* trs = (tr && threadIdx.x == 128) ? tr : nullptr;
+    if (MODE == MODE_SUMI) {
+      // self term from the TMA-loaded q / k_self / v_self tiles (16-byte chunks
+      // XOR-swizzled like the TMA box)
+      mbar_wait(bar_q, 0);
+      if (trs) trs[126] = clock64();
+      const uint8_t* qrow = smem + Ly::Q_OFF + row * Ly::RB;
+      const uint8_t* krow = smem + Ly::KS_OFF + row * Ly::RB;
+      const uint8_t* vrow = smem + Ly::VS_OFF + row * Ly::RB;
+      float ss = 0.f;
+#pragma unroll
+      for (int j = 0; j < DH / 8; ++j) {
+        float q[8], k8[8];
+        load8(reinterpret_cast<const bf16*>(qrow + (swz<DH>(row, j) << 4)), q);
+        load8(reinterpret_cast<const bf16*>(krow + (swz<DH>(row, j) << 4)), k8);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ss = fmaf(q[i], k8[i], ss);
+      }
+      m_used = valid ? ss * sc : 0.f;
+#pragma unroll
+      for (int c = 0; c < DH; c += 32) {  // O = v_self
+        float vs[32];
+#pragma unroll
+        for (int cc = 0; cc < 32; cc += 8) {
+          if (valid) {
+            load8(reinterpret_cast<const bf16*>(vrow + (swz<DH>(row, (c + cc) / 8) << 4)), vs + cc);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) vs[cc + i] = 0.f;
+          }
+        }
+        tmem_st32(tO + lane_off + c, vs);
+      }
+      l = 1.f;  // the self term's weight
+      // the self tiles' stages become K / V stages
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(self_done);
+    }
+    const bool causal_hist = (MODE == MODE_HIST) && D.causal;
+    for (int j = 0; j < nch; ++j) {
+      mbar_wait(s_full, j & 1);
+      fence_after();
+      if (trs && j < 12) trs[2 * j] = clock64();
+      const int key0 = j * KEYS;
+      int lim = kend - key0;  // keys [0, lim) of the chunk are visible to this row
+      if (causal_hist) lim = min(lim, t_row - key0 + 1);
+      uint32_t sr[KEYS];
+#pragma unroll
+      for (int c = 0; c < KEYS; c += 32) tmem_ld32_nw(tS + lane_off + c, sr + c);
+      tmem_ld_wait();
+      fence_before();
+      mbar_arrive(s_read);  // the S columns may take S(j+1)
+      if (trs && j < 12) trs[40 + j] = clock64();
+      if (lim < KEYS) {  // masked keys -> -inf (2^-inf = +0)
+#pragma unroll
+        for (int i = 0; i < KEYS; ++i)
+          if (i >= lim) sr[i] = __float_as_uint(-INFINITY);
+      }
+      float mx8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < KEYS; i += 2)
+        mx8[(i >> 1) & 7] = max3(mx8[(i >> 1) & 7], __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
+      const float mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      const float mx = mraw * sc;  // sc > 0
+      // lazy rescale: per row, only when its max grew by > 2^8; tcgen05.ld/st
+      // are warp-collective, so the warp decides together.  s_full(j) implies
+      // P(j-1) V_{j-1} is complete (the MMAs of one thread complete in order).
+      const bool mine = mx > m_used + RESCALE_LOG2;
+      const float alpha = mine ? exp2f(m_used - mx) : 1.f;  // m_used = -inf -> 0
+      if (mine) {
+        l *= alpha;
+        m_used = mx;
+      }
+      // P(j-1) V_{j-1} must be complete before O is rescaled or P(j) written
+      const bool need_pv = j > 0;
+      bool pv_seen = false;
+      if ((MODE == MODE_SUMI || j > 0) && __any_sync(0xffffffffu, mine)) {
+        if (need_pv) {
+          mbar_wait(pv_done, (j - 1) & 1);
+          fence_after();
+          pv_seen = true;
+        }
+#pragma unroll
+        for (int c = 0; c < DH; c += 16) {  // 16 columns at a time
+          uint32_t o[16];
+          tmem_ld16_nw(tO + lane_off + c, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st16u(tO + lane_off + c, o);
+        }
+      }
+      if (trs && j < 12) trs[52 + j] = clock64();
+      // P = 2^(s sc - m) (fp32), packed to bf16 into S's first 64 columns
+      const float nb = (m_used == -INFINITY) ? 0.f : -m_used;
+      const uint64_t sc2 = f2_pack(sc, sc), nb2 = f2_pack(nb, nb);
+      uint64_t ls2[4] = {0ull, 0ull, 0ull, 0ull};  // packed (0.f, 0.f)
+#pragma unroll
+      for (int c = 0; c < KEYS; c += 32) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float2 x = f2_unpack(f2_fma(f2_pack(__uint_as_float(sr[c + i]), __uint_as_float(sr[c + i + 1])),
+                                            sc2, nb2));
+          const float e0 = ((i & 7) < PE) ? ex2_poly(x.x) : ex2_approx(x.x);
+          const float e1 = (((i + 1) & 7) < PE) ? ex2_poly(x.y) : ex2_approx(x.y);
+          ls2[(i >> 1) & 3] = f2_add(ls2[(i >> 1) & 3], f2_pack(e0, e1));
+          __nv_bfloat162 pp = __floats2bfloat162_rn(e0, e1);
+          pk[i >> 1] = *reinterpret_cast<uint32_t*>(&pp);
+        }
+        if (c == 0 && need_pv && !pv_seen) {
+          mbar_wait(pv_done, (j - 1) & 1);
+          fence_after();
+        }
+        tmem_st16u(tP + lane_off + c / 2, pk);
+      }
+      {
+        const float2 a0 = f2_unpack(f2_add(ls2[0], ls2[1])), a1 = f2_unpack(f2_add(ls2[2], ls2[3]));
+        l += (a0.x + a0.y) + (a1.x + a1.y);
+      }
+      tmem_st_wait();
+      fence_before();
+      mbar_arrive(p_full);
+      if (trs && j < 12) trs[2 * j + 1] = clock64();
+    }
+    if (trs) trs[30] = clock64();
+    // ---- epilogue: O / l -> bf16, staged in the q buffer (every MMA has
+    // completed once the last pv_done fires), coalesced row stores
+    if (nch > 0) {
+      mbar_wait(pv_done, (nch - 1) & 1);
+      fence_after();
+    }
+    const bool have_o = MODE == MODE_SUMI || nch > 0;
+    const float inv = (valid && l > 0.f) ? 1.f / l : 0.f;
+    uint8_t* qtile = smem + Ly::Q_OFF;
+#pragma unroll
+    for (int c = 0; c < DH; c += 32) {
+      float o[32];
+      if (have_o) {
+        tmem_ld32(tO + lane_off + c, o);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] = 0.f;
+      }
+#pragma unroll
+      for (int cc = 0; cc < 32; cc += 8) {
+        float y[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[i] = o[cc + i] * inv;
+        store8(reinterpret_cast<bf16*>(qtile + row * Ly::RB + (swz<DH>(row, (c + cc) / 8) << 4)), y);
+      }
+    }
+    named_sync(1, 128);
+    constexpr int LPR = DH / 8;      // lanes per row, 16 B (8 bf16) each
+    constexpr int RPI = 32 / LPR;    // rows per warp instruction
+#pragma unroll
+    for (int i = 0; i < 32; i += RPI) {
+      const int rr = ew * 32 + i + lane / LPR;
+      const int cj = lane % LPR;
+      if (rr < n_out) {
+        const uint4 val = *reinterpret_cast<const uint4*>(qtile + rr * Ly::RB + (swz<DH>(rr, cj) << 4));
+        *reinterpret_cast<uint4*>(a.O + (rbase + rr) * D.d + head * DH + cj * 8) = val;
+      }
+    }
+    if (trs) trs[31] = clock64();
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 map: [rows][cols] with row stride ld, box {box_cols, box_rows}, swizzle = box row bytes
+static bool map2d(CUtensorMap* m, const void* base, long long rows, int cols, long long ld, int box_cols,
+                  int box_rows) {
+  auto enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMapSwizzle sw = box_cols * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int DH, int MODE, int PE>
+static void launch_pe(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s) {
+  constexpr int smem = Lay<DH>::TOTAL;
+  static_assert(2 * (smem + 1024) <= 233472, "two CTAs per SM");
+  ensure_smem_attr((const void*)k_attn_fa<DH, MODE, PE>, smem);
+  k_attn_fa<DH, MODE, PE><<<grid, THREADS, smem, s>>>(mq, mkv, a);
+}
+
+// PE: how many of every 8 exponentials run on the FMA pipe (CLIMBER_FA_PE)
+template <int DH, int MODE>
+static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s) {
+  static const int pe = [] { const char* e = getenv("CLIMBER_FA_PE"); return e ? atoi(e) : 0; }();
+  switch (pe) {
+    case 1: launch_pe<DH, MODE, 1>(mq, mkv, a, grid, s); break;
+    case 2: launch_pe<DH, MODE, 2>(mq, mkv, a, grid, s); break;
+    case 3: launch_pe<DH, MODE, 3>(mq, mkv, a, grid, s); break;
+    default: launch_pe<DH, MODE, 0>(mq, mkv, a, grid, s); break;
+  }
+}
+
+// CLIMBER_FA_TRACE=n: record the n-th launch of this process (clock64 per CTA)
+// and print the mean timeline relative to each CTA's start
+static unsigned long long* trace_begin(long long n_cta) {
+  static const int at = [] { const char* e = getenv("CLIMBER_FA_TRACE"); return e ? atoi(e) : -1; }();
+  static int n_launch = 0;
+  if (at < 0 || n_launch++ != at) return nullptr;
+  unsigned long long* buf = nullptr;
+  cudaMallocManaged(&buf, n_cta * TRACE_N * 8);
+  cudaMemset(buf, 0, n_cta * TRACE_N * 8);
+  return buf;
+}
+static void trace_end(unsigned long long* buf, long long n_cta, cudaStream_t s) {
+  if (!buf) return;
+  cudaStreamSynchronize(s);
+  double acc[TRACE_N] = {0};
+  long long cnt[TRACE_N] = {0};
+  for (long long c = 0; c < n_cta; ++c) {
+    const unsigned long long* t = buf + c * TRACE_N;
+    if (!t[127]) continue;
+    for (int i = 0; i < 127; ++i)
+      if (t[i]) acc[i] += (double)(long long)(t[i] - t[127]), cnt[i]++;
+  }
+  auto m = [&](int i) { return cnt[i] ? acc[i] / cnt[i] : -1.0; };
+  fprintf(stderr, "[fa trace] %lld CTAs (cycles since start)\n", n_cta);
+  fprintf(stderr, "[fa trace] q tiles seen %7.0f\n", m(126));
+  for (int j = 0; j < 12; ++j)
+    fprintf(stderr, "[fa trace] chunk %2d: kv %7.0f | S %7.0f ld %7.0f max %7.0f P %7.0f | mma saw P %7.0f\n", j,
+            m(96 + j), m(2 * j), m(40 + j), m(52 + j), m(2 * j + 1), m(64 + j));
+  fprintf(stderr, "[fa trace] epilogue %7.0f -> %7.0f\n", m(30), m(31));
+  cudaFree(buf);
+}
+
+}  // namespace fa
+
+bool attn_fa_supported(int dh, int nk) { return (dh == 32 || dh == 64) && nk % PAGE == 0 && fa::encoder(); }
+
+void launch_attn_sumi_fa(const bf16* QKV, long long P, const int64_t* cand_off, const int* wave_slot,
+                         const int* wave_r, int U, int Mmax, const bf16* pool, long long pool_rows, const int* ptab,
+                         const int* vlen_all, const float* tau, bf16* O, int k, int l, const Dims& D, cudaStream_t s,
+                         int nbk) {
+  CUtensorMap mq, mkv;
+  if (!fa::map2d(&mq, QKV, P * nbk, 3 * D.d, 3LL * D.d, D.dh, fa::ROWS) ||
+      !fa::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, PAGE)) {
+    note_launch_error("SUMI attention: cuTensorMapEncodeTiled rejected a map (kernel not launched)");
+    return;
+  }
+  fa::Args a{QKV, cand_off, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, U, P, D, nullptr};
+  dim3 grid((Mmax + fa::ROWS - 1) / fa::ROWS, D.h, U * nbk);
+  const long long n_cta = (long long)grid.x * grid.y * grid.z;
+  a.trace = fa::trace_begin(n_cta);
+  if (D.dh == 64) fa::launch<64, fa::MODE_SUMI>(mq, mkv, a, grid, s);
+  else fa::launch<32, fa::MODE_SUMI>(mq, mkv, a, grid, s);
+  fa::trace_end(a.trace, n_cta, s);
+}
+
+void launch_attn_hist_fa(const bf16* Q, const int* wave_slot, const int* wave_r, int U, const bf16* pool,
+                         long long pool_rows, const int* ptab, const int* vlen_all, const float* tau, bf16* O, int k,
+                         int l, const Dims& D, cudaStream_t s, int nbk) {
+  CUtensorMap mq, mkv;
+  if (!fa::map2d(&mq, Q, (long long)U * D.nk * nbk, D.d, D.d, D.dh, fa::ROWS) ||
+      !fa::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, PAGE)) {
+    note_launch_error("history attention: cuTensorMapEncodeTiled rejected a map (kernel not launched)");
+    return;
+  }
+  fa::Args a{Q, nullptr, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, U, (long long)U * D.nk, D, nullptr};
+  dim3 grid((D.nk + fa::ROWS - 1) / fa::ROWS, D.h, U * nbk);
+  if (D.dh == 64) fa::launch<64, fa::MODE_HIST>(mq, mkv, a, grid, s);
+  else fa::launch<32, fa::MODE_HIST>(mq, mkv, a, grid, s);
+}
+
+}  // namespace climber

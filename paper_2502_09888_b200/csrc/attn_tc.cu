@@ -1146,6 +1146,12 @@ static bool use_pt() {
 
 }  // namespace at
 
+// CLIMBER_ATTN_FA=0 keeps the one-tile kernel below for A/B measurements
+static bool use_fa() {
+  static const bool v = [] { const char* e = getenv("CLIMBER_ATTN_FA"); return !(e && atoi(e) == 0); }();
+  return v;
+}
+
 bool attn_tc_supported(int dh, int nk, bool hist) {
   if (dh != 32 && dh != 64) return false;
   if (hist && nk % at::ROWS) return false;
@@ -1156,6 +1162,11 @@ void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, 
                          const int* wave_r, int U, int Mmax, const bf16* pool, long long pool_rows, const int* ptab,
                          const int* vlen_all, const float* tau, bf16* O, int k, int l, const Dims& D, cudaStream_t s,
                          int nbk) {
+  if (!D.bpos && use_fa() && attn_fa_supported(D.dh, D.nk)) {
+    launch_attn_sumi_fa(QKV, P, cand_off, wave_slot, wave_r, U, Mmax, pool, pool_rows, ptab, vlen_all, tau, O, k, l,
+                        D, s, nbk);
+    return;
+  }
   CUtensorMap mq, mkv;
   if (!at::map2d(&mq, QKV, P * nbk, 3 * D.d, 3LL * D.d, D.dh, at::ROWS) ||
       !at::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, at::KEYS)) {
@@ -1212,6 +1223,10 @@ void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, 
 void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r, int U, const bf16* pool,
                          long long pool_rows, const int* ptab, const int* vlen_all, const float* tau, bf16* O, int k,
                          int l, const Dims& D, cudaStream_t s, int nbk) {
+  if (!D.bpos && use_fa() && attn_fa_supported(D.dh, D.nk)) {
+    launch_attn_hist_fa(Q, wave_slot, wave_r, U, pool, pool_rows, ptab, vlen_all, tau, O, k, l, D, s, nbk);
+    return;
+  }
   CUtensorMap mq, mkv;
   if (!at::map2d(&mq, Q, (long long)U * D.nk * nbk, D.d, D.d, D.dh, at::ROWS) ||
       !at::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, at::KEYS)) {

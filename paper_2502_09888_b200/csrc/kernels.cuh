@@ -96,6 +96,17 @@ void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r,
                          long long pool_rows, const int* ptab, const int* vlen_all, const float* tau, bf16* O, int k,
                          int l, const Dims& D, cudaStream_t s, int nbk = 1);
 
+// Two-tile tcgen05/TMEM attention (128-key chunks, one CTA per SM), attn_fa.cu;
+// the *_tc launchers route here unless the relative bias is on.
+bool attn_fa_supported(int dh, int nk);
+void launch_attn_sumi_fa(const bf16* QKV, long long P, const int64_t* cand_off, const int* wave_slot,
+                         const int* wave_r, int U, int Mmax, const bf16* pool, long long pool_rows, const int* ptab,
+                         const int* vlen_all, const float* tau, bf16* O, int k, int l, const Dims& D, cudaStream_t s,
+                         int nbk);
+void launch_attn_hist_fa(const bf16* Q, const int* wave_slot, const int* wave_r, int U, const bf16* pool,
+                         long long pool_rows, const int* ptab, const int* vlen_all, const float* tau, bf16* O, int k,
+                         int l, const Dims& D, cudaStream_t s, int nbk);
+
 // tcgen05 GEMM (bf16 in, fp32 accumulate in TMEM), gemm_tc.cu.  Returns false
 // if the shape is not supported by the tensor-core kernel.
 bool gemm_tc_supported(long long M, int N, int K, long long lda, long long ldb);
