@@ -4,7 +4,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) $(EXTRA) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
 SRC := paper_2502_09888_b200/csrc
 OUT := paper_2502_09888_b200/lib
-OBJS := $(OUT)/api.o $(OUT)/kernels.o $(OUT)/gemm_tc.o $(OUT)/attn_mma.o $(OUT)/attn_tc.o $(OUT)/attn_fa.o
+OBJS := $(OUT)/api.o $(OUT)/kernels.o $(OUT)/gemm_tc.o $(OUT)/attn_mma.o $(OUT)/attn_fa.o
 HDRS := $(wildcard $(SRC)/*.cuh) include/climber.h
 
 all: $(OUT)/libclimber.so

@@ -231,8 +231,8 @@ static bool dims_from(const climber_config* cfg, Dims* D, std::string* why) {
   D->causal = cfg->hist_causal ? 1 : 0; D->ppb = (cfg->n_k + PAGE - 1) / PAGE; D->eps = cfg->rms_eps;
   D->bpos = D->btime = nullptr; D->hage = nullptr; D->cbias = nullptr;
   if (cfg->rel_bias != 0 && cfg->rel_bias != 1) { *why = "rel_bias must be 0 or 1"; return false; }
-  if (cfg->rel_bias && cfg->dtype == CLIMBER_BF16 && !((dh == 32 || dh == 64) && cfg->n_k % 128 == 0)) {
-    *why = "rel_bias on the bf16 path needs d_h in {32, 64} and n_k % 128 == 0 (tcgen05 attention)";
+  if (cfg->rel_bias && cfg->dtype == CLIMBER_BF16 && !((dh == 32 || dh == 64) && cfg->n_k % PAGE == 0)) {
+    *why = "rel_bias on the bf16 path needs d_h in {32, 64} and n_k % 64 == 0 (tcgen05 attention)";
     return false;
   }
   return true;

@@ -25,13 +25,20 @@
 //               pairs), O [192, 192+d_h))
 //   warps 4-7   softmax, one thread per query row, the whole 128-key S row in
 //               registers: row max, lazy online rescale (O is rescaled only
-//               when the row max grows by > 2^8), P = 2^(s sc - m) (PE of every
-//               8 on an FMA-pipe polynomial, the rest on the MUFU), packed to
-//               bf16 into TMEM, fp32 row sum with packed FADD2
+//               when the row max grows by > 2^8), P = 2^(s sc - m) on the MUFU,
+//               packed to bf16 into TMEM, fp32 row sum with packed FADD2 (the
+//               MUFU bounds it: 16 exponentials / clk / SM; an FMA-pipe
+//               polynomial for part of them measured slower)
 //   epilogue    O / l -> bf16, staged in the (then idle) q buffer, coalesced
 //               row stores
 // The SUMI self term initialises the row state (m = s_self, l = 1, O = v_self),
 // so no candidate ever reads another candidate's K/V.
+// BIAS = 1 adds Eq. 3's relative bias f_b^{p,t}(a_k, r) to the raw scores before
+// the 1/(sqrt(d_h) tau) scaling (G6b-G6e): SUMI rows add the request's
+// candidate-row bias cbias[slot][l][k][head][j] (the same for every candidate);
+// history rows look up b_pos[bucket_pos(t - j)] + b_time[bucket_time(age_j -
+// age_t)] from tables staged in shared memory (causal: one 64 x 7 (offset
+// bucket, time bucket) table, one lookup per score).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -66,7 +73,12 @@ struct Lay {
   static constexpr int V_OFF = K_OFF + KST * KV_B;        // [VST] V chunks
   static constexpr int BAR_OFF = V_OFF + VST * KV_B;
   static constexpr int PG_OFF = BAR_OFF + 256;            // page ids of the (user, block, layer), <= 32
-  static constexpr int TOTAL = PG_OFF + 128 + 1024;       // + 1024 B alignment slack
+  // relative bias (BIAS = 1): b_pos [128], b_time [16], causal 2-D lookup [64 x 7],
+  // then the (user, block)'s row of n_k <= 1024 values: SUMI the candidate-row
+  // bias of this (layer, head), HIST the token ages
+  static constexpr int BIAS_OFF = PG_OFF + 128;
+  static constexpr int BROW_OFF = BIAS_OFF + (NB_POS + 16 + 64 * 7) * 4;
+  static constexpr int TOTAL = BROW_OFF + 1024 * 4 + 1024;  // + 1024 B alignment slack
   // SUMI: k_self / v_self are parked in the last K and V stages until the self term is read
   static constexpr int KS_OFF = K_OFF + (KST - 1) * KV_B;
   static constexpr int VS_OFF = V_OFF + (VST - 1) * KV_B;
@@ -101,18 +113,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x on the FMA pipe: x = j + f, j = rne(x), f in [-1/2, 1/2]; 2^f by a
-// degree-3 fit (max rel. error 7.5e-5, below the bf16 rounding of P), 2^j
-// added to the exponent field with one integer multiply-add
-__device__ __forceinline__ float ex2_poly(float x) {
-  constexpr float MAGIC = 12582912.f;  // 1.5 * 2^23
-  const float xc = fmaxf(x, -125.f);
-  const float t = xc + MAGIC;
-  const float f = xc - (t - MAGIC);
-  const float p = fmaf(fmaf(fmaf(0.055171628f, f, 0.24261117f), f, 0.69326103f), f, 0.99992806f);
-  const float y = __int_as_float(__float_as_int(t) * (1 << 23) + __float_as_int(p));
-  return x < -125.f ? 0.f : y;  // masked keys (-inf) give exactly 0, like the MUFU
-}
 __device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
   uint64_t r;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -139,7 +139,7 @@ __device__ __forceinline__ int swz(int row, int j) {
   return (DH == 64) ? (j ^ (row & 7)) : (j ^ ((row >> 1) & 3));
 }
 
-template <int DH, int MODE, int PE>
+template <int DH, int MODE, int BIAS>
 __global__ void __launch_bounds__(THREADS, 2)
     k_attn_fa(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, Args a) {
   using Ly = Lay<DH>;
@@ -308,6 +308,31 @@ __global__ void __launch_bounds__(THREADS, 2)
     const bool valid = row < n_rows;
     const int t_row = tile0 + row;      // HIST: this row's position in the subsequence
     float m_used = -INFINITY, l = 0.f;
+    // relative bias (BIAS = 1): this (layer, block, scenario, head)'s tables in smem
+    float* sbp = reinterpret_cast<float*>(smem + Ly::BIAS_OFF);
+    float* sbt = sbp + NB_POS;
+    float* lut = sbt + 16;  // causal history: lut[bp * 7 + bt] = b_pos[bp] + b_time[bt], bp < 64, bt < 7
+    const int* hag = nullptr;
+    const float* cbr = nullptr;
+    int t_age = 0;
+    if constexpr (BIAS) {
+      const long long br = bias_row(D, a.l, kblk, r, head);
+      sbp[row] = D.bpos[br * NB_POS + row];
+      if (row < NB_TIME) sbt[row] = D.btime[br * NB_TIME + row];
+      if (MODE == MODE_HIST && D.causal)
+        for (int e = row; e < 64 * 7; e += 128) lut[e] = D.bpos[br * NB_POS + e / 7] + D.btime[br * NB_TIME + e % 7];
+      // the (user, block)'s row (ages or candidate-row bias) in smem: the
+      // per-chunk reads are broadcast shared loads off the critical path
+      const int* gag = D.hage + ((long long)slot * D.Nb + kblk) * D.nk;
+      const float* gcb = D.cbias + ((((long long)slot * D.L + a.l) * D.Nb + kblk) * D.h + head) * D.nk;
+      int* srow = reinterpret_cast<int*>(smem + Ly::BROW_OFF);
+      for (int i = row; i < D.nk; i += 128)
+        srow[i] = MODE == MODE_SUMI ? __float_as_int(gcb[i]) : gag[i];
+      named_sync(1, 128);
+      hag = srow;
+      cbr = reinterpret_cast<const float*>(srow);
+      if (MODE == MODE_HIST && t_row < v) t_age = hag[t_row];
+    }
     unsigned long long* trs = (tr && threadIdx.x == 128) ? tr : nullptr;
     if (MODE == MODE_SUMI) {
       // self term from the TMA-loaded q / k_self / v_self tiles (16-byte chunks
@@ -326,6 +351,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 #pragma unroll
         for (int i = 0; i < 8; ++i) ss = fmaf(q[i], k8[i], ss);
       }
+      if constexpr (BIAS) ss += sbp[bucket_pos(0)] + sbt[bucket_time32(0)];  // self: offset 0, delta 0
       m_used = valid ? ss * sc : 0.f;
 #pragma unroll
       for (int c = 0; c < DH; c += 32) {  // O = v_self
@@ -361,6 +387,43 @@ __global__ void __launch_bounds__(THREADS, 2)
       fence_before();
       mbar_arrive(s_read);  // the S columns may take S(j+1)
       if (trs && j < 12) trs[40 + j] = clock64();
+      if constexpr (BIAS) {  // R = QK^T + f_b (before the 1/(sqrt(d_h) tau) scaling, Eq. 3)
+        if (MODE == MODE_SUMI) {
+          const float4* c4 = reinterpret_cast<const float4*>(cbr + key0);
+#pragma unroll
+          for (int i = 0; i < KEYS; i += 4) {
+            const float4 b = (key0 + i < D.nk) ? c4[i >> 2] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float2 s01 = f2_unpack(f2_add(f2_pack(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])),
+                                                f2_pack(b.x, b.y)));
+            const float2 s23 = f2_unpack(f2_add(f2_pack(__uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3])),
+                                                f2_pack(b.z, b.w)));
+            sr[i] = __float_as_uint(s01.x);
+            sr[i + 1] = __float_as_uint(s01.y);
+            sr[i + 2] = __float_as_uint(s23.x);
+            sr[i + 3] = __float_as_uint(s23.y);
+          }
+        } else {
+          // t_row - t_key = age_key - age_row; key ages 4 per 16-byte load
+          const int4* a4 = reinterpret_cast<const int4*>(hag + key0);
+#pragma unroll
+          for (int i = 0; i < KEYS; i += 4) {
+            const int4 ka = (key0 + i < D.nk) ? a4[i >> 2] : make_int4(0, 0, 0, 0);
+            const int kv4[4] = {ka.x, ka.y, ka.z, ka.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float b;
+              if (D.causal) {  // offsets >= 0 and time deltas >= 0 on every visible key: one 2-D lookup
+                const int bp = bucket_pos(t_row - (key0 + i + q)) & 63;  // masked keys (offset < 0) stay in range
+                const int bt = bucket_time32(kv4[q] - t_age) % 7;
+                b = lut[bp * 7 + bt];
+              } else {
+                b = sbp[bucket_pos(t_row - (key0 + i + q))] + sbt[bucket_time32(kv4[q] - t_age)];
+              }
+              sr[i + q] = __float_as_uint(__uint_as_float(sr[i + q]) + b);
+            }
+          }
+        }
+      }
       if (lim < KEYS) {  // masked keys -> -inf (2^-inf = +0)
 #pragma unroll
         for (int i = 0; i < KEYS; ++i)
@@ -415,8 +478,8 @@ __global__ void __launch_bounds__(THREADS, 2)
         for (int i = 0; i < 32; i += 2) {
           const float2 x = f2_unpack(f2_fma(f2_pack(__uint_as_float(sr[c + i]), __uint_as_float(sr[c + i + 1])),
                                             sc2, nb2));
-          const float e0 = ((i & 7) < PE) ? ex2_poly(x.x) : ex2_approx(x.x);
-          const float e1 = (((i + 1) & 7) < PE) ? ex2_poly(x.y) : ex2_approx(x.y);
+          const float e0 = ex2_approx(x.x);
+          const float e1 = ex2_approx(x.y);
           ls2[(i >> 1) & 3] = f2_add(ls2[(i >> 1) & 3], f2_pack(e0, e1));
           __nv_bfloat162 pp = __floats2bfloat162_rn(e0, e1);
           pk[i >> 1] = *reinterpret_cast<uint32_t*>(&pp);
@@ -513,23 +576,16 @@ static bool map2d(CUtensorMap* m, const void* base, long long rows, int cols, lo
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int DH, int MODE, int PE>
-static void launch_pe(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s) {
-  constexpr int smem = Lay<DH>::TOTAL;
-  static_assert(2 * (smem + 1024) <= 233472, "two CTAs per SM");
-  ensure_smem_attr((const void*)k_attn_fa<DH, MODE, PE>, smem);
-  k_attn_fa<DH, MODE, PE><<<grid, THREADS, smem, s>>>(mq, mkv, a);
-}
-
-// PE: how many of every 8 exponentials run on the FMA pipe (CLIMBER_FA_PE)
 template <int DH, int MODE>
 static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s) {
-  static const int pe = [] { const char* e = getenv("CLIMBER_FA_PE"); return e ? atoi(e) : 0; }();
-  switch (pe) {
-    case 1: launch_pe<DH, MODE, 1>(mq, mkv, a, grid, s); break;
-    case 2: launch_pe<DH, MODE, 2>(mq, mkv, a, grid, s); break;
-    case 3: launch_pe<DH, MODE, 3>(mq, mkv, a, grid, s); break;
-    default: launch_pe<DH, MODE, 0>(mq, mkv, a, grid, s); break;
+  constexpr int smem = Lay<DH>::TOTAL;
+  static_assert(2 * (smem + 1024) <= 233472, "two CTAs per SM");
+  if (a.D.bpos) {
+    ensure_smem_attr((const void*)k_attn_fa<DH, MODE, 1>, smem);
+    k_attn_fa<DH, MODE, 1><<<grid, THREADS, smem, s>>>(mq, mkv, a);
+  } else {
+    ensure_smem_attr((const void*)k_attn_fa<DH, MODE, 0>, smem);
+    k_attn_fa<DH, MODE, 0><<<grid, THREADS, smem, s>>>(mq, mkv, a);
   }
 }
 
@@ -567,9 +623,13 @@ static void trace_end(unsigned long long* buf, long long n_cta, cudaStream_t s) 
 
 }  // namespace fa
 
-bool attn_fa_supported(int dh, int nk) { return (dh == 32 || dh == 64) && nk % PAGE == 0 && fa::encoder(); }
+// d_h 32 / 64 and whole pages (the history kernel covers n_k % 128 == 64 with a
+// half-empty last tile)
+bool attn_tc_supported(int dh, int nk, bool /*hist*/) {
+  return (dh == 32 || dh == 64) && nk % PAGE == 0 && fa::encoder() != nullptr;
+}
 
-void launch_attn_sumi_fa(const bf16* QKV, long long P, const int64_t* cand_off, const int* wave_slot,
+void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, const int* wave_slot,
                          const int* wave_r, int U, int Mmax, const bf16* pool, long long pool_rows, const int* ptab,
                          const int* vlen_all, const float* tau, bf16* O, int k, int l, const Dims& D, cudaStream_t s,
                          int nbk) {
@@ -588,7 +648,7 @@ void launch_attn_sumi_fa(const bf16* QKV, long long P, const int64_t* cand_off, 
   fa::trace_end(a.trace, n_cta, s);
 }
 
-void launch_attn_hist_fa(const bf16* Q, const int* wave_slot, const int* wave_r, int U, const bf16* pool,
+void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r, int U, const bf16* pool,
                          long long pool_rows, const int* ptab, const int* vlen_all, const float* tau, bf16* O, int k,
                          int l, const Dims& D, cudaStream_t s, int nbk) {
   CUtensorMap mq, mkv;

@@ -98,6 +98,34 @@ __device__ __forceinline__ void store8(float* p, const float* v) {
   *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
   *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
 }
+// N consecutive bf16 (N = 4: 8-byte access, N % 8 == 0: 16-byte accesses)
+template <int N>
+__device__ __forceinline__ void load_n(const bf16* p, float* v) {
+  if constexpr (N % 8 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 8) load8(p + i, v + i);
+  } else {
+    static_assert(N == 4, "load_n: N = 4 or a multiple of 8");
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    const bf16* b = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = __bfloat162float(b[i]);
+  }
+}
+template <int N>
+__device__ __forceinline__ void store_n(bf16* p, const float* v) {
+  if constexpr (N % 8 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 8) store8(p + i, v + i);
+  } else {
+    static_assert(N == 4, "store_n: N = 4 or a multiple of 8");
+    uint2 u;
+    bf16* b = reinterpret_cast<bf16*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) b[i] = __float2bfloat16_rn(v[i]);
+    *reinterpret_cast<uint2*>(p) = u;
+  }
+}
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

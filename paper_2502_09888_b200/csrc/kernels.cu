@@ -1,3 +1,4 @@
+#include <type_traits>
 #include <mutex>
 #include <set>
 #include <string>
@@ -944,9 +945,117 @@ void launch_attn_hist(const T* Q, const int* wave_slot, const int* wave_r, int U
 #undef CL_HIST
 }
 
+// Fusion ATL attention, bf16 (G16): one CTA per candidate pair, all heads.
+// The pair's N_b token rows of QKV (contiguous: rows p N_b .. p N_b + N_b - 1,
+// 3 d bf16 each) are copied to shared memory with coalesced 16-byte loads,
+// every warp computes heads w, w + 8, ... from there (4 lanes per token,
+// scores reduced over them with two shuffles), and O is staged in shared
+// memory and written back with coalesced 16-byte stores: one streaming read
+// of 3 N_b d and one write of N_b d elements per pair.
+template <int DH>
+__global__ void __launch_bounds__(256) k_attn_fusion_pair(const bf16* __restrict__ QKV,
+                                                          const int64_t* __restrict__ cand_off,
+                                                          const int* __restrict__ wave_r, int U, long long P,
+                                                          const float* __restrict__ tau_f, bf16* __restrict__ O,
+                                                          Dims D) {
+  constexpr int PD = DH / 4;  // dims per lane
+  extern __shared__ __align__(16) uint8_t fsm[];
+  const int rs = 3 * D.d + 8;                       // token row stride (elements): +16 B spreads the banks
+  bf16* sq = reinterpret_cast<bf16*>(fsm);           // [N_b][rs]
+  bf16* so = sq + D.Nb * rs;                         // [N_b][d + 8] staged O
+  const int ros = D.d + 8;
+  const long long p = blockIdx.x;
+  const int u = pair_user(cand_off, U, p);
+  const int r = wave_r[u];
+  // coalesced copy of the pair's rows
+  {
+    const int cpr = 3 * D.d / 8;  // 16-byte chunks per row
+    const uint4* g = reinterpret_cast<const uint4*>(QKV + p * D.Nb * 3LL * D.d);
+    for (int i = threadIdx.x; i < D.Nb * cpr; i += blockDim.x) {
+      const int t = i / cpr, c = i % cpr;
+      *reinterpret_cast<uint4*>(sq + t * rs + c * 8) = g[i];
+    }
+  }
+  __syncthreads();
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tok = lane >> 2, part = lane & 3;
+  const bool act = tok < D.Nb;
+  const int tk = act ? tok : 0;
+  for (int head = wib; head < D.h; head += 8) {
+    const float sc = LOG2E / (sqrtf((float)DH) * tau_f[r * D.h + head]);
+    float q[PD];
+    load_n<PD>(sq + tk * rs + head * DH + part * PD, q);
+    float s[8];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float acc = 0.f;
+      if (j < D.Nb) {
+        float k[PD];
+        load_n<PD>(sq + j * rs + D.d + head * DH + part * PD, k);
+#pragma unroll
+        for (int c = 0; c < PD; ++c) acc = fmaf(q[c], k[c], acc);
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      s[j] = (j < D.Nb) ? acc * sc : -INFINITY;
+      mx = fmaxf(mx, s[j]);
+    }
+    float l = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      s[j] = (j < D.Nb) ? exp2f(s[j] - mx) : 0.f;
+      l += s[j];
+    }
+    const float inv = 1.f / l;
+    float o[PD];
+#pragma unroll
+    for (int c = 0; c < PD; ++c) o[c] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j < D.Nb) {
+        float v[PD];
+        load_n<PD>(sq + j * rs + 2 * D.d + head * DH + part * PD, v);
+#pragma unroll
+        for (int c = 0; c < PD; ++c) o[c] = fmaf(s[j], v[c], o[c]);
+      }
+    }
+    if (act) {
+#pragma unroll
+      for (int c = 0; c < PD; ++c) o[c] *= inv;
+      store_n<PD>(so + tok * ros + head * DH + part * PD, o);
+    }
+  }
+  __syncthreads();
+  {
+    const int cpr = D.d / 8;
+    uint4* g = reinterpret_cast<uint4*>(O + p * D.Nb * (long long)D.d);
+    for (int i = threadIdx.x; i < D.Nb * cpr; i += blockDim.x) {
+      const int t = i / cpr, c = i % cpr;
+      g[i] = *reinterpret_cast<const uint4*>(so + t * ros + c * 8);
+    }
+  }
+}
+
 template <typename T>
 void launch_attn_fusion(const T* QKV, const int64_t* cand_off, const int* wave_r, int U, long long P,
                         const float* tau_f, T* O, const Dims& D, cudaStream_t s) {
+  if constexpr (std::is_same<T, bf16>::value) {
+    // bf16 path: one CTA per pair, coalesced row copies (k_attn_fusion_pair)
+    if (D.dh >= 16 && P > 0) {
+      const int smem = (D.Nb * (3 * D.d + 8) + D.Nb * (D.d + 8)) * 2;
+#define CL_FP(DH)                                                                                          \
+  do {                                                                                                     \
+    ensure_smem_attr((const void*)k_attn_fusion_pair<DH>, smem);                                           \
+    k_attn_fusion_pair<DH><<<(unsigned)P, 256, smem, s>>>(QKV, cand_off, wave_r, U, P, tau_f, O, D);       \
+  } while (0)
+      if (D.dh == 16) CL_FP(16);
+      else if (D.dh == 32) CL_FP(32);
+      else CL_FP(64);
+#undef CL_FP
+      return;
+    }
+  }
   long long n = P * D.h;  // warps
   unsigned g = blocks_for(n, 8);
 #define CL_FUS(DH) k_attn_fusion<T, DH><<<g, 256, 0, s>>>(QKV, cand_off, wave_r, U, P, tau_f, O, D)

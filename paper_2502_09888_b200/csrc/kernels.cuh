@@ -86,7 +86,8 @@ void launch_attn_hist_mma(const bf16* Q, const int* wave_slot, const int* wave_r
                           const int* ptab, const int* vlen_all, const float* tau, bf16* O, int k, int l, const Dims& D,
                           cudaStream_t s);
 
-// tcgen05/TMEM attention for the bf16 path, attn_tc.cu.
+// tcgen05/TMEM flash attention for the bf16 path, attn_fa.cu (d_h 32 / 64,
+// n_k % 64 == 0; relative bias included).
 bool attn_tc_supported(int dh, int nk, bool hist);
 void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, const int* wave_slot,
                          const int* wave_r, int U, int Mmax, const bf16* pool, long long pool_rows, const int* ptab,
@@ -95,17 +96,6 @@ void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, 
 void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r, int U, const bf16* pool,
                          long long pool_rows, const int* ptab, const int* vlen_all, const float* tau, bf16* O, int k,
                          int l, const Dims& D, cudaStream_t s, int nbk = 1);
-
-// Two-tile tcgen05/TMEM attention (128-key chunks, one CTA per SM), attn_fa.cu;
-// the *_tc launchers route here unless the relative bias is on.
-bool attn_fa_supported(int dh, int nk);
-void launch_attn_sumi_fa(const bf16* QKV, long long P, const int64_t* cand_off, const int* wave_slot,
-                         const int* wave_r, int U, int Mmax, const bf16* pool, long long pool_rows, const int* ptab,
-                         const int* vlen_all, const float* tau, bf16* O, int k, int l, const Dims& D, cudaStream_t s,
-                         int nbk);
-void launch_attn_hist_fa(const bf16* Q, const int* wave_slot, const int* wave_r, int U, const bf16* pool,
-                         long long pool_rows, const int* ptab, const int* vlen_all, const float* tau, bf16* O, int k,
-                         int l, const Dims& D, cudaStream_t s, int nbk);
 
 // tcgen05 GEMM (bf16 in, fp32 accumulate in TMEM), gemm_tc.cu.  Returns false
 // if the shape is not supported by the tensor-core kernel.

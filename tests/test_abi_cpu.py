@@ -81,7 +81,7 @@ def test_arena_bytes_and_config_validation_on_host():
     assert n2 - n >= 64 * 2 * 64 * 128 * 2
     for bad in (dict(d=100), dict(n_heads=3), dict(n_k=48), dict(n_blocks=9), dict(page_tokens=32),
                 dict(abi_version=1), dict(dtype=7), dict(max_wave_pairs=10), dict(rel_bias=2),
-                dict(rel_bias=1)):   # rel_bias on bf16 needs n_k % 128 == 0 (here 64)
+                dict(rel_bias=1, n_heads=8)):   # rel_bias on bf16 needs d_h in {32, 64} (here 16)
         assert L.climber_arena_bytes(C.byref(_cfg(**bad))) == 0, bad
     # create rejects a bad config synchronously, before touching the device
     h = C.c_void_p()

@@ -30,7 +30,7 @@ def _user_scores_vs_oracle(cfg, w, u, cl, strats=None):
 
 
 def test_medium_tcgen05_bidirectional_history():
-    """hist_causal = 0 on the tcgen05 history kernel (k_attn_tc HIST, D.causal = 0)."""
+    """hist_causal = 0 on the tcgen05 history kernel (k_attn_fa HIST, D.causal = 0)."""
     cfg = synth.preset("medium", hist_causal=0)
     w = synth.make_weights(cfg, 0)
     batch = synth.make_batch(cfg, 1, B=3)

@@ -13,5 +13,5 @@ FULL="ncu --set full --clock-control none --import-source on --kernel-name-base 
 $FULL -k 'regex:k_gemm_tc<.int.256, .int.5, .int.4, .int.2, .int.1, .int.2>' -s 40 -c 1 -o gpurun_out/prof_gemm_norm $CMD > gpurun_out/ncu_gemm_norm.log 2>&1
 $FULL -k 'regex:k_gemm_tc<.int.256, .int.6, .int.8, .int.1, .int.0, .int.2>' -s 20 -c 1 -o gpurun_out/prof_gemm_silu $CMD > gpurun_out/ncu_gemm_silu.log 2>&1
 # SUMI attention (tcgen05, d_h = 64)
-$FULL -k 'regex:k_attn_tc<.int.64, .int.0' -s 8 -c 1 -o gpurun_out/prof_attn_sumi $CMD > gpurun_out/ncu_attn_sumi.log 2>&1
+$FULL -k 'regex:k_attn_fa<.int.64, .int.0' -s 8 -c 1 -o gpurun_out/prof_attn_sumi $CMD > gpurun_out/ncu_attn_sumi.log 2>&1
 ls -la gpurun_out

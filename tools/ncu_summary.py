@@ -14,9 +14,9 @@ def launches(path):
         name = r[ki].split("(")[0].split("<")[0].replace("void ", "").strip()
         if "k_attn<" in r[ki]:
             name = "k_attn<" + r[ki].split("k_attn<")[1].split(">")[0] + ">"
-        if "k_attn_tc<" in r[ki]:
-            args = r[ki].split("k_attn_tc<")[1].split(">")[0].replace("(int)", "").split(",")
-            name = "k_attn_tc<d_h=%s, %s>" % (args[0].strip(), "SUMI" if args[1].strip() == "0" else "HIST")
+        if "k_attn_fa<" in r[ki]:
+            args = r[ki].split("k_attn_fa<")[1].split(">")[0].replace("(int)", "").split(",")
+            name = "k_attn_fa<d_h=%s, %s>" % (args[0].strip(), "SUMI" if args[1].strip() == "0" else "HIST")
         if "k_gemm_tc<" in r[ki]:
             name = "k_gemm_tc<" + r[ki].split("k_gemm_tc<")[1].split(">")[0] + ">"
         v = float(r[vi].replace(",", ""))
