@@ -1,5 +1,7 @@
+#include <algorithm>
 #include <type_traits>
 #include <mutex>
+#include <map>
 #include <set>
 #include <string>
 #include <cstdio>
@@ -10,12 +12,13 @@
 // (bf16 production path, fp32 verification build); statistics,
 // softmax and residuals are fp32 in both.
 #include "kernels.cuh"
+#include "tc_util.cuh"
 
 namespace climber {
 
 static std::mutex g_launch_mu;
 static std::string g_launch_err;
-static std::set<std::pair<const void*, int>> g_attr_done;
+static std::map<std::pair<const void*, int>, int> g_attr_done;  // (kernel, device) -> bytes set
 
 void note_launch_error(const char* what) {
   std::lock_guard<std::mutex> g(g_launch_mu);
@@ -34,8 +37,11 @@ void ensure_smem_attr(const void* kern, int bytes) {
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> g(g_launch_mu);
-  if (g_attr_done.insert({kern, dev}).second)
+  int& have = g_attr_done[{kern, dev}];  // 0 when new; raised when a launch needs more
+  if (bytes > have) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    have = bytes;
+  }
 }
 
 
@@ -945,13 +951,15 @@ void launch_attn_hist(const T* Q, const int* wave_slot, const int* wave_r, int U
 #undef CL_HIST
 }
 
-// Fusion ATL attention, bf16 (G16): one CTA per candidate pair, all heads.
-// The pair's N_b token rows of QKV (contiguous: rows p N_b .. p N_b + N_b - 1,
-// 3 d bf16 each) are copied to shared memory with coalesced 16-byte loads,
-// every warp computes heads w, w + 8, ... from there (4 lanes per token,
-// scores reduced over them with two shuffles), and O is staged in shared
-// memory and written back with coalesced 16-byte stores: one streaming read
-// of 3 N_b d and one write of N_b d elements per pair.
+// Fusion ATL attention, bf16 (G16): persistent CTAs, one candidate pair at a
+// time, all heads.  The pair's N_b token rows of QKV (contiguous: rows
+// p N_b .. p N_b + N_b - 1, 3 d bf16 each) arrive in shared memory by bulk
+// async copies (one per row, into rows padded by 16 B so the 4-lane token
+// groups hit distinct banks), double-buffered: the next pair streams in while
+// this one is computed.  Every warp computes heads w, w + 8, ... (4 lanes per
+// token, scores reduced over them with two shuffles); O is staged in shared
+// memory and written back with coalesced 16-byte stores.  Traffic per pair:
+// one read of 3 N_b d and one write of N_b d elements.
 template <int DH>
 __global__ void __launch_bounds__(256) k_attn_fusion_pair(const bf16* __restrict__ QKV,
                                                           const int64_t* __restrict__ cand_off,
@@ -960,80 +968,104 @@ __global__ void __launch_bounds__(256) k_attn_fusion_pair(const bf16* __restrict
                                                           Dims D) {
   constexpr int PD = DH / 4;  // dims per lane
   extern __shared__ __align__(16) uint8_t fsm[];
-  const int rs = 3 * D.d + 8;                       // token row stride (elements): +16 B spreads the banks
-  bf16* sq = reinterpret_cast<bf16*>(fsm);           // [N_b][rs]
-  bf16* so = sq + D.Nb * rs;                         // [N_b][d + 8] staged O
+  const int rs = 3 * D.d + 8;                       // token row stride (elements)
   const int ros = D.d + 8;
-  const long long p = blockIdx.x;
-  const int u = pair_user(cand_off, U, p);
-  const int r = wave_r[u];
-  // coalesced copy of the pair's rows
-  {
-    const int cpr = 3 * D.d / 8;  // 16-byte chunks per row
-    const uint4* g = reinterpret_cast<const uint4*>(QKV + p * D.Nb * 3LL * D.d);
-    for (int i = threadIdx.x; i < D.Nb * cpr; i += blockDim.x) {
-      const int t = i / cpr, c = i % cpr;
-      *reinterpret_cast<uint4*>(sq + t * rs + c * 8) = g[i];
-    }
+  bf16* sq0 = reinterpret_cast<bf16*>(fsm);          // [2][N_b][rs] double buffer
+  bf16* so = sq0 + 2 * D.Nb * rs;                    // [N_b][ros] staged O
+  uint64_t* bar = reinterpret_cast<uint64_t*>(so + D.Nb * ros);  // [2]
+  const unsigned row_bytes = 3u * D.d * 2u;
+  auto issue = [&](long long p, int b) {  // one thread: the pair's rows into buffer b
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the generic reads of the buffer
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tcu::smem_u32(&bar[b])),
+                 "r"(row_bytes * D.Nb) : "memory");
+    for (int t = 0; t < D.Nb; ++t)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              tcu::smem_u32(sq0 + (b * D.Nb + t) * rs)),
+          "l"(QKV + (p * D.Nb + t) * 3LL * D.d), "r"(row_bytes), "r"(tcu::smem_u32(&bar[b]))
+          : "memory");
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tcu::smem_u32(&bar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tcu::smem_u32(&bar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (threadIdx.x == 0 && (long long)blockIdx.x < P) issue(blockIdx.x, 0);
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tok = lane >> 2, part = lane & 3;
   const bool act = tok < D.Nb;
   const int tk = act ? tok : 0;
-  for (int head = wib; head < D.h; head += 8) {
-    const float sc = LOG2E / (sqrtf((float)DH) * tau_f[r * D.h + head]);
-    float q[PD];
-    load_n<PD>(sq + tk * rs + head * DH + part * PD, q);
-    float s[8];
-    float mx = -INFINITY;
+  int it = 0;
+  for (long long p = blockIdx.x; p < P; p += gridDim.x, ++it) {
+    const int b = it & 1;
+    // the other buffer was released by the __syncthreads that ended the previous pair
+    if (threadIdx.x == 0 && p + gridDim.x < P) issue(p + gridDim.x, b ^ 1);
+    {
+      const uint32_t ba = tcu::smem_u32(&bar[b]), ph = (it >> 1) & 1;
+      asm volatile(
+          "{\n.reg .pred q;\nWF_%=:\nmbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n@!q bra WF_%=;\n}\n" ::"r"(ba),
+          "r"(ph)
+          : "memory");
+    }
+    const bf16* sq = sq0 + b * D.Nb * rs;
+    const int u = pair_user(cand_off, U, p);
+    const int r = wave_r[u];
+    for (int head = wib; head < D.h; head += 8) {
+      const float sc = LOG2E / (sqrtf((float)DH) * tau_f[r * D.h + head]);
+      float q[PD];
+      load_n<PD>(sq + tk * rs + head * DH + part * PD, q);
+      float s[8];
+      float mx = -INFINITY;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float acc = 0.f;
-      if (j < D.Nb) {
-        float k[PD];
-        load_n<PD>(sq + j * rs + D.d + head * DH + part * PD, k);
+      for (int j = 0; j < 8; ++j) {
+        float acc = 0.f;
+        if (j < D.Nb) {
+          float k[PD];
+          load_n<PD>(sq + j * rs + D.d + head * DH + part * PD, k);
 #pragma unroll
-        for (int c = 0; c < PD; ++c) acc = fmaf(q[c], k[c], acc);
+          for (int c = 0; c < PD; ++c) acc = fmaf(q[c], k[c], acc);
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        s[j] = (j < D.Nb) ? acc * sc : -INFINITY;
+        mx = fmaxf(mx, s[j]);
       }
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      s[j] = (j < D.Nb) ? acc * sc : -INFINITY;
-      mx = fmaxf(mx, s[j]);
-    }
-    float l = 0.f;
+      float l = 0.f;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      s[j] = (j < D.Nb) ? exp2f(s[j] - mx) : 0.f;
-      l += s[j];
-    }
-    const float inv = 1.f / l;
-    float o[PD];
+      for (int j = 0; j < 8; ++j) {
+        s[j] = (j < D.Nb) ? exp2f(s[j] - mx) : 0.f;
+        l += s[j];
+      }
+      const float inv = 1.f / l;
+      float o[PD];
 #pragma unroll
-    for (int c = 0; c < PD; ++c) o[c] = 0.f;
+      for (int c = 0; c < PD; ++c) o[c] = 0.f;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (j < D.Nb) {
-        float v[PD];
-        load_n<PD>(sq + j * rs + 2 * D.d + head * DH + part * PD, v);
+      for (int j = 0; j < 8; ++j) {
+        if (j < D.Nb) {
+          float v[PD];
+          load_n<PD>(sq + j * rs + 2 * D.d + head * DH + part * PD, v);
 #pragma unroll
-        for (int c = 0; c < PD; ++c) o[c] = fmaf(s[j], v[c], o[c]);
+          for (int c = 0; c < PD; ++c) o[c] = fmaf(s[j], v[c], o[c]);
+        }
+      }
+      if (act) {
+#pragma unroll
+        for (int c = 0; c < PD; ++c) o[c] *= inv;
+        store_n<PD>(so + tok * ros + head * DH + part * PD, o);
       }
     }
-    if (act) {
-#pragma unroll
-      for (int c = 0; c < PD; ++c) o[c] *= inv;
-      store_n<PD>(so + tok * ros + head * DH + part * PD, o);
+    __syncthreads();
+    {
+      const int cpr = D.d / 8;
+      uint4* g = reinterpret_cast<uint4*>(O + p * D.Nb * (long long)D.d);
+      for (int i = threadIdx.x; i < D.Nb * cpr; i += blockDim.x) {
+        const int t = i / cpr, c = i % cpr;
+        g[i] = *reinterpret_cast<const uint4*>(so + t * ros + c * 8);
+      }
     }
-  }
-  __syncthreads();
-  {
-    const int cpr = D.d / 8;
-    uint4* g = reinterpret_cast<uint4*>(O + p * D.Nb * (long long)D.d);
-    for (int i = threadIdx.x; i < D.Nb * cpr; i += blockDim.x) {
-      const int t = i / cpr, c = i % cpr;
-      g[i] = *reinterpret_cast<const uint4*>(so + t * ros + c * 8);
-    }
+    __syncthreads();  // staging and this buffer free again
   }
 }
 
@@ -1043,11 +1075,19 @@ void launch_attn_fusion(const T* QKV, const int64_t* cand_off, const int* wave_r
   if constexpr (std::is_same<T, bf16>::value) {
     // bf16 path: one CTA per pair, coalesced row copies (k_attn_fusion_pair)
     if (D.dh >= 16 && P > 0) {
-      const int smem = (D.Nb * (3 * D.d + 8) + D.Nb * (D.d + 8)) * 2;
+      const int smem = (2 * D.Nb * (3 * D.d + 8) + D.Nb * (D.d + 8)) * 2 + 16;
+      static int n_sm = 0;
+      if (!n_sm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+      }
+      const int per_sm = std::max(1, std::min(8, (int)(227 * 1024 / (smem + 1024))));
+      const unsigned grid = (unsigned)std::min<long long>(P, (long long)n_sm * per_sm);
 #define CL_FP(DH)                                                                                          \
   do {                                                                                                     \
     ensure_smem_attr((const void*)k_attn_fusion_pair<DH>, smem);                                           \
-    k_attn_fusion_pair<DH><<<(unsigned)P, 256, smem, s>>>(QKV, cand_off, wave_r, U, P, tau_f, O, D);       \
+    k_attn_fusion_pair<DH><<<grid, 256, smem, s>>>(QKV, cand_off, wave_r, U, P, tau_f, O, D);              \
   } while (0)
       if (D.dh == 16) CL_FP(16);
       else if (D.dh == 32) CL_FP(32);

@@ -9,8 +9,9 @@ namespace climber {
 // of the C-ABI call (check_launch) returns CLIMBER_E_CUDA with the message.
 void note_launch_error(const char* what);
 bool take_launch_error(char* msg, int cap);
-// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
-// the attribute is per device, so a process driving several GPUs sets it on each.
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) per (kernel, device), raised
+// whenever a launch needs more than was set before (the attribute is per
+// device, so a process driving several GPUs sets it on each).
 void ensure_smem_attr(const void* kern, int bytes);
 
 struct EventsDev {
