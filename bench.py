@@ -556,6 +556,26 @@ def main():
                    "warmup": nw,
                    "mode": f"candidate-sharded over {world} GPUs: owner encodes, climber_kv_broadcast (library "
                            f"ncclBroadcast of the K/V slab), scores all_gather; host call to host scores"}
+        # the same with the K/V replicated layer by layer while it is encoded
+        # (climber_encode_user_bcast: per-layer ncclBroadcast behind each QKV GEMM)
+        from paper_2502_09888_b200.sharded import rank_request_sharded_pipelined
+        tp = []
+        for i in range(args.latency_requests + nw):
+            u = batch.subset([i % B])
+            items = dev(u.cand)
+            dist.barrier()
+            t0 = time.perf_counter()
+            ev = (dev(u.item), dev(u.action), dev(u.scenario), dev(u.ts)) if rank == 0 else None
+            out = rank_request_sharded_pipelined(cl, dist, ev, int(u.r[0]), items)
+            if rank == 0:
+                out.cpu()
+                if i >= nw:
+                    tp.append((time.perf_counter() - t0) * 1e3)
+        if rank == 0:
+            lat["pipelined"] = {
+                "p50": float(np.percentile(tp, 50)), "p99": float(np.percentile(tp, 99)), "requests": len(tp),
+                "mode": f"candidate-sharded over {world} GPUs, K/V replicated per layer while it is encoded "
+                        f"(climber_encode_user_bcast), scores all_gather; host call to host scores"}
         if cfg.N_b % world == 0:
             # block-parallel: each rank encodes + scores N_b / G blocks,
             # block outputs all-gathered, rank 0 fuses; no K/V moves

@@ -366,6 +366,28 @@ climber_status climber_kv_import(climber_ctx_t ctx, const void* slab, int32_t sc
 climber_status climber_kv_broadcast(climber_ctx_t ctx, climber_kv_t* kv, int32_t root,
                                     climber_stream_t stream);
 
+/* Encode one user on `root` and replicate its K/V to every rank WHILE it is
+ * being encoded ("pipelined per layer, overlapping encode of
+ * layer l+1 with the broadcast of layer l").  Collective over the
+ * ctx's communicator: every rank passes the same scenario_r and root; events /
+ * n_s are read on root only (others may pass NULL / 0).  The root encodes as
+ * climber_encode_user and, on a side stream, posts L + 1 ncclBroadcasts of
+ * one slab: the header section (v_k, r, relative-bias state) as soon as
+ * extraction is done, then layer l's pages of every block as soon as layer
+ * l's QKV GEMM has written them; the receivers post the same broadcasts on
+ * `stream` and unpack each section into their own pages right behind it.
+ * Nothing synchronises the host.  On return every rank holds a handle in *out
+ * (root: the encoded one); all work is ordered on `stream`.
+ * Errors: E_INVALID_ARG / E_OUT_OF_RANGE (arguments, checked alike on every
+ * rank), E_UNSUPPORTED (no communicator, or not the grouped bf16 tcgen05
+ * path), E_CAPACITY (this rank's pool is full: it still posts its broadcasts,
+ * so the others do not hang, and returns the error), root-side encode errors
+ * (the root then sends a zeroed header: receivers get E_CONFIG from
+ * climber_stream_status), E_NCCL (the communicator is aborted). */
+climber_status climber_encode_user_bcast(climber_ctx_t ctx, const climber_events* events, int64_t n_s,
+                                         int32_t scenario_r, int32_t root, climber_stream_t stream,
+                                         climber_kv_t* out);
+
 /* An NCCL unique id (128 bytes into `out`) for climber_create's nccl_uid:
  * rank 0 calls it and shares the bytes with the other ranks. */
 climber_status climber_nccl_unique_id(void* out);

@@ -98,6 +98,7 @@ def lib() -> C.CDLL:
             "climber_cache_release": (I32, [VP, VP]),
             "climber_cache_append": (I32, [VP, C.c_uint64, I32, C.c_uint64, C.c_uint64, P, I64, VP, P, P, P]),
             "climber_nccl_unique_id": (I32, [P]),
+            "climber_encode_user_bcast": (I32, [VP, P, I64, I32, I32, VP, P]),
             "climber_cache_stats": (I32, [VP, P]),
         }
         for name, (res, args) in sig.items():
@@ -117,7 +118,7 @@ EXPORTED_SYMBOLS = ("climber_arena_bytes", "climber_create", "climber_destroy", 
                     "climber_kv_slab_bytes", "climber_kv_export", "climber_kv_import",
                     "climber_encode_users_blocks", "climber_score_blocks", "climber_fuse_scores", "climber_forward",
                     "climber_cache_acquire", "climber_cache_release", "climber_cache_stats",
-                    "climber_cache_append", "climber_nccl_unique_id")
+                    "climber_cache_append", "climber_nccl_unique_id", "climber_encode_user_bcast")
 
 KERNEL_CLASSES = ("extract", "embed", "rmsnorm", "gemm_qkv", "gemm_o", "gemm_ffn_up", "gemm_ffn_down", "gemm_se",
                   "attn_hist", "attn_sumi", "attn_fusion", "head", "other")
@@ -415,6 +416,20 @@ class Climber:
         kv = C.c_void_p(handle or 0)
         _check(lib().climber_kv_broadcast(self.h, C.byref(kv), int(root), self._stream(stream)))
         return kv.value
+
+    def encode_user_bcast(self, events, r: int, root: int = 0, stream=None) -> int:
+        """Collective: encode on root and replicate the K/V layer by layer while
+        it is encoded (climber_encode_user_bcast).  events = (item, action,
+        scenario, ts) CUDA tensors on root, None elsewhere."""
+        ev, n_s = None, 0
+        if events is not None:
+            item, action, scenario, ts = events
+            n_s = int(item.numel())
+            ev = _Events(item.data_ptr(), action.data_ptr(), scenario.data_ptr(), ts.data_ptr())
+        out = C.c_void_p()
+        _check(lib().climber_encode_user_bcast(self.h, C.byref(ev) if ev is not None else None, n_s, int(r),
+                                               int(root), self._stream(stream), C.byref(out)))
+        return out.value
 
     def kv_import(self, slab, r: int, stream=None) -> int:
         out = C.c_void_p()

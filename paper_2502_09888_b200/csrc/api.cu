@@ -180,6 +180,11 @@ struct climber_ctx_s {
   void* bslab = nullptr;  // broadcast slab (device, slab_bytes)
   std::vector<cudaEvent_t> ov_evt;          // [L + 2]: per-layer K/V ready, fork, join
   bool ov_record = false, ov_wait = false;
+  // pipelined replication (climber_encode_user_bcast): [0] extraction done,
+  // [1 + l] layer l's pages written, [L + 1] broadcasts done; the root's side stream
+  std::vector<cudaEvent_t> bc_evt;
+  bool bc_record = false;
+  cudaStream_t bc_stream = nullptr;
   bool graphs = true;
 };
 
@@ -532,6 +537,8 @@ extern "C" climber_status climber_destroy(climber_ctx_t c) {
   if (c->g_stream) cudaStreamDestroy(c->g_stream);
   if (c->g_stream2) cudaStreamDestroy(c->g_stream2);
   for (cudaEvent_t ev : c->ov_evt) cudaEventDestroy(ev);
+  if (c->bc_stream) cudaStreamDestroy(c->bc_stream);
+  for (cudaEvent_t ev : c->bc_evt) cudaEventDestroy(ev);
   if (c->d_flags) cudaFree(c->d_flags);
   cudaEventDestroy(c->stage_evt);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -1014,6 +1021,7 @@ static void encode_wave_grouped(climber_ctx_s* c, const EventsDev& ev, int u0, i
     Prof p(c, CLIMBER_K_OTHER, s, 0, (double)U * D.L * D.Nb * D.h * D.nk * 12);
     launch_cand_bias(wslot, c->d_r + u0, U, c->vlen_all, D, s);
   }
+  if (c->bc_record) cudaEventRecord(c->bc_evt[0], s);  // v_k (and the bias state) final
   if (nbk == 0) return;  // extraction (and the candidate bias rows) only: incremental append
   bf16* Xb = (bf16*)c->Xb;   // [Nb][rows][d]
   bf16* Qb = (bf16*)c->QKV;  // [Nb][rows][d]
@@ -1044,6 +1052,7 @@ static void encode_wave_grouped(climber_ctx_s* c, const EventsDev& ev, int u0, i
       e.col_off = 0;
       gemm_g(c, CLIMBER_K_GEMM_QKV, gXb, d, rows * d, Wqkv, d, Lk * 3 * d * d, rows, 3 * D.d, D.d, nbk, e, s);
       if (c->ov_record) cudaEventRecord(c->ov_evt[l], s);  // layer l's K/V pages written
+      if (c->bc_record) cudaEventRecord(c->bc_evt[1 + l], s);
       {
         Prof p(c, CLIMBER_K_ATTN_HIST, s, 4.0 * U * causal_pairs * d * nbk, (double)rows * d * 2 * 4 * nbk);
         launch_attn_hist_tc(gQb, wslot, wr, U, (const bf16*)c->pool, c->n_pages * 2 * PAGE, c->ptab, c->vlen_all,
@@ -1064,6 +1073,7 @@ static void encode_wave_grouped(climber_ctx_s* c, const EventsDev& ev, int u0, i
       gemm_g(c, CLIMBER_K_GEMM_QKV, gXb, d, rows * d, Wqkv + d * d, d, Lk * 3 * d * d, rows, 2 * D.d, D.d, nbk, e,
              s);
       if (c->ov_record) cudaEventRecord(c->ov_evt[l], s);
+      if (c->bc_record) cudaEventRecord(c->bc_evt[1 + l], s);
     }
   }
 }
@@ -1464,6 +1474,8 @@ extern "C" climber_status climber_kv_release(climber_ctx_t c, climber_kv_t kv) {
 }
 
 static size_t page_bytes(const climber_ctx_s* c);
+static size_t bias_state_bytes(const climber_ctx_s* c);
+static climber_status copy_bias_state_at(climber_ctx_s* c, int slot, char* sec, bool to_slab, cudaStream_t s);
 
 // replicate one user's K/V to every rank of the ctx's NCCL
 // group.  The root exports its handle into one slab (256 B header: config
@@ -1520,7 +1532,7 @@ extern "C" climber_status climber_kv_broadcast(climber_ctx_t c, climber_kv_t* kv
   if (!c->comm) return fail(CLIMBER_E_UNSUPPORTED, "ctx has no NCCL communicator (aborted or never created)");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const size_t bytes = climber_kv_slab_bytes(c);
-  if (!c->bslab) CU(cudaMalloc(&c->bslab, bytes));
+  if (!c->bslab) CU(cudaMalloc(&c->bslab, bytes + 16));  // + 16: the pipelined layout's padded header
   climber_status root_st = CLIMBER_OK;
   if (c->rank == root) {
     root_st = climber_kv_export(c, *kv, c->bslab, stream);
@@ -1539,6 +1551,147 @@ extern "C" climber_status climber_kv_broadcast(climber_ctx_t c, climber_kv_t* kv
   CU(cudaMemcpy(hdr, c->bslab, sizeof hdr, cudaMemcpyDeviceToHost));
   if (hdr[0] != 0x4B56534C) return fail(CLIMBER_E_STALE, "kv_broadcast: the root's export failed (no handle sent)");
   return climber_kv_import(c, c->bslab, hdr[7], stream, kv);
+}
+
+// Pipelined replication of one user's K/V while it is encoded (SURVEY §8(e):
+// "pipelined per layer, overlapping encode of layer l+1 with the broadcast of
+// layer l").  Slab sections: [header 256 B + bias state][layer 0 pages]...
+// [layer L-1 pages]; L + 1 ncclBroadcasts on every rank in that order.  The
+// root posts its broadcasts on a side stream, each behind the event its
+// encode records when that section is final; receivers post theirs on
+// `stream` and unpack each section right behind it -- no host sync anywhere.
+// A rank whose own preparation fails still posts all L + 1 broadcasts (the
+// root with a zeroed header, so the receivers' imports fail on the device
+// with E_CONFIG) and returns its error.
+extern "C" climber_status climber_encode_user_bcast(climber_ctx_t c, const climber_events* events, int64_t n_s,
+                                                    int32_t scenario_r, int32_t root, climber_stream_t stream,
+                                                    climber_kv_t* out) {
+  if (!c || !out) return fail(CLIMBER_E_INVALID_ARG, "null argument");
+  if (root < 0 || root >= c->world) return fail(CLIMBER_E_INVALID_ARG, "root out of range");
+  if (scenario_r < 0 || scenario_r >= c->D.R) return fail(CLIMBER_E_OUT_OF_RANGE, "scenario_r out of range");
+  if (!c->comm) return fail(CLIMBER_E_UNSUPPORTED, "ctx has no NCCL communicator (aborted or never created)");
+  if (!(c->fused && grouped_ok(c) && attn_tc_supported(c->D.dh, c->D.nk, true)))
+    return fail(CLIMBER_E_UNSUPPORTED, "encode_user_bcast needs the grouped bf16 tcgen05 path");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const Dims& D = c->D;
+  const size_t hdr_bytes = (256 + bias_state_bytes(c) + 15) / 16 * 16;
+  const size_t layer_bytes = (size_t)D.Nb * D.ppb * page_bytes(c);
+  const size_t bytes = hdr_bytes + (size_t)D.L * layer_bytes;
+  if (!c->bslab) CU(cudaMalloc(&c->bslab, climber_kv_slab_bytes(c) + 16));
+  char* slab = reinterpret_cast<char*>(c->bslab);
+  static_assert(sizeof(int) == 4, "");
+  if ((size_t)bytes > climber_kv_slab_bytes(c) + 16) return fail(CLIMBER_E_CUDA, "slab layout");
+  if ((int)c->bc_evt.size() < D.L + 2) {
+    while ((int)c->bc_evt.size() < D.L + 2) {
+      cudaEvent_t ev;
+      CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      c->bc_evt.push_back(ev);
+    }
+  }
+  static const bool self_import = getenv("CLIMBER_DEBUG_BCAST_SELF") != nullptr;
+  climber_status local = CLIMBER_OK;
+  ncclResult_t nr = ncclSuccess;
+  auto bcast = [&](size_t off, size_t n, cudaStream_t st) {
+    if (nr == ncclSuccess) nr = nccl_api().bcast(slab + off, slab + off, n, ncclUint8, root, c->comm, st);
+  };
+  // receiver side: allocate the handle, then (broadcast +) unpack section by section
+  auto receive = [&](bool do_bcast) -> climber_status {
+    int slot = -1;
+    climber_status mine = CLIMBER_OK;
+    {
+      std::lock_guard<std::mutex> g(c->mu);
+      if (c->free_slots.empty() || (long long)c->free_pages.size() < c->per_slot) {
+        mine = fail(CLIMBER_E_CAPACITY, "K/V page pool exhausted");
+      } else {
+        cudaError_t e = cudaEventSynchronize(c->stage_evt);
+        if (e != cudaSuccess) return fail(CLIMBER_E_CUDA, "stage: %s", cudaGetErrorString(e));
+        Stage h = stage_layout(c, c->h_stage);
+        slot = c->free_slots.back();
+        c->free_slots.pop_back();
+        SlotState& st = c->slots[slot];
+        st.live = true;
+        st.r = scenario_r;
+        st.kb0 = 0;
+        st.kb1 = D.Nb;
+        st.pages.resize(c->per_slot);
+        for (int i = 0; i < c->per_slot; ++i) {
+          st.pages[i] = c->free_pages.back();
+          c->free_pages.pop_back();
+          h.ptab[i] = st.pages[i];
+        }
+        h.slots[0] = slot;
+        h.r[0] = scenario_r;
+        h.ev_off[0] = h.ev_off[1] = 0;
+        climber_status rs = stage_upload(c, 1, true, s);
+        if (rs != CLIMBER_OK) return rs;
+        *out = make_handle(c, slot, st.gen);
+      }
+    }
+    if (do_bcast) bcast(0, hdr_bytes, s);
+    if (mine == CLIMBER_OK) {
+      launch_kv_import(c->pool, c->ptab, c->vlen_all, slot, 0, (long long)page_bytes(c), slab, c->err, D,
+                       c->cfg.dtype, s);
+      climber_status st = copy_bias_state_at(c, slot, slab + 256, false, s);
+      if (st != CLIMBER_OK) return st;
+    }
+    for (int l = 0; l < D.L; ++l) {
+      if (do_bcast) bcast(hdr_bytes + l * layer_bytes, layer_bytes, s);
+      if (mine == CLIMBER_OK)
+        launch_kv_layer_copy(c->pool, c->ptab, slot, l, (long long)page_bytes(c),
+                             slab + hdr_bytes + l * layer_bytes, true, D, s);
+    }
+    if (nr != ncclSuccess) return nccl_abort(c, nccl_api().err(nr));
+    if (mine != CLIMBER_OK) return mine;
+    return check_launch(c, s);
+  };
+  if (c->rank == root) {
+    if (!c->bc_stream) CU(cudaStreamCreateWithFlags(&c->bc_stream, cudaStreamNonBlocking));
+    cudaStream_t bs = c->bc_stream;
+    int slot = -1;
+    if (!events) {
+      local = fail(CLIMBER_E_INVALID_ARG, "root needs the events");
+    } else {
+      const int64_t off[2] = {0, n_s};
+      c->bc_record = true;
+      local = encode_users_range(c, 1, off, events, &scenario_r, stream, out, 0, D.Nb);
+      c->bc_record = false;
+      if (local == CLIMBER_OK) {
+        std::lock_guard<std::mutex> g(c->mu);
+        if (resolve(c, *out, &slot) != CLIMBER_OK) local = fail(CLIMBER_E_STALE, "fresh handle");
+      }
+    }
+    CU(cudaStreamWaitEvent(bs, c->bc_evt[0], 0));  // also orders behind earlier work on the ctx
+    if (local == CLIMBER_OK) {
+      launch_kv_export(c->pool, c->ptab, c->vlen_all, slot, 0, (long long)page_bytes(c), slab, D, c->cfg.dtype,
+                       scenario_r, bs);
+      climber_status st = copy_bias_state_at(c, slot, slab + 256, true, bs);
+      if (st != CLIMBER_OK) return st;
+    } else {
+      CU(cudaMemsetAsync(slab, 0, 256, bs));
+    }
+    bcast(0, hdr_bytes, bs);
+    for (int l = 0; l < D.L; ++l) {
+      if (local == CLIMBER_OK) {
+        CU(cudaStreamWaitEvent(bs, c->bc_evt[1 + l], 0));
+        launch_kv_layer_copy(c->pool, c->ptab, slot, l, (long long)page_bytes(c), slab + hdr_bytes + l * layer_bytes,
+                             false, D, bs);
+      }
+      bcast(hdr_bytes + l * layer_bytes, layer_bytes, bs);
+    }
+    CU(cudaEventRecord(c->bc_evt[D.L + 1], bs));
+    CU(cudaStreamWaitEvent(s, c->bc_evt[D.L + 1], 0));  // the slab and the pages are reused in stream order
+    if (nr != ncclSuccess) return nccl_abort(c, nccl_api().err(nr));
+    if (local != CLIMBER_OK || !self_import) return local;
+    // CLIMBER_DEBUG_BCAST_SELF (world-1 tests): the root also takes the receiver
+    // path (allocation, header and per-layer unpack) from its own slab into a
+    // second handle, which it returns
+    const climber_kv_t sent = *out;
+    climber_status st = receive(false);
+    CU(cudaStreamSynchronize(s));
+    climber_kv_release(c, sent);
+    return st;
+  }
+  return receive(true);
 }
 
 extern "C" climber_status climber_nccl_unique_id(void* out) {
@@ -1566,10 +1719,13 @@ extern "C" size_t climber_kv_slab_bytes(climber_ctx_t c) {
 }
 
 static climber_status copy_bias_state(climber_ctx_s* c, int slot, char* slab, bool to_slab, cudaStream_t s) {
+  return copy_bias_state_at(c, slot, slab + 256 + (size_t)c->per_slot * page_bytes(c), to_slab, s);
+}
+// the bias state of `slot` to / from `sec` (hage rows, then cbias rows)
+static climber_status copy_bias_state_at(climber_ctx_s* c, int slot, char* sec, bool to_slab, cudaStream_t s) {
   if (!c->cfg.rel_bias) return CLIMBER_OK;
   const Dims& D = c->D;
   const size_t hb = (size_t)D.Nb * D.nk * 4, cb = (size_t)D.L * D.Nb * D.h * D.nk * 4;
-  char* sec = slab + 256 + (size_t)c->per_slot * page_bytes(c);
   char* h = reinterpret_cast<char*>(c->hage) + slot * hb;
   char* cbs = reinterpret_cast<char*>(c->cbias) + slot * cb;
   if (to_slab) {

@@ -47,59 +47,152 @@ void ensure_smem_attr(const void* kern, int bytes) {
 
 // ===========================================================================
 // a1: validation + multi-scale sequence extraction (Eq. 2)
-// One CTA per user.  All threads validate the events (coalesced sweep), then
-// warp k extracts strategy k by a reverse ballot scan: lanes test 32 events
-// newest-first, the rank of a match among newer matches in the chunk is a
-// popcount, so the most recent n_k matches land in canonical left-padded
-// slots n_k-1, n_k-2, ... (G11, G12).
+// One CTA of 256 threads per user.  All threads validate the events
+// (coalesced sweep); then the events are taken from the newest in
+// super-chunks of 256 x EXT_EPT: thread t owns EXT_EPT consecutive events
+// (thread 0 the newest) and counts its matches for every strategy; a
+// block-wide exclusive scan (newest first) of the packed counts gives each
+// match its rank from the newest, and matches of rank < n_k go to slot
+// n_k - 1 - rank, so the most recent n_k matches land in canonical left-padded
+// slots n_k-1, n_k-2, ... (G11, G12).  The sweep stops once every strategy
+// has n_k matches: a user costs (events needed / 4096) steps of one coalesced
+// load and one scan each.
 // ===========================================================================
-__global__ void k_extract(const int32_t* __restrict__ item, const uint8_t* __restrict__ action,
+constexpr int EXT_EPT = 16;
+constexpr int EXT_THREADS = 256;
+
+__device__ __forceinline__ void ext_scan(uint64_t& a, uint64_t& b, uint64_t* sh, uint64_t& ta, uint64_t& tb) {
+  // exclusive scan over the block of two packed vectors (4 x 16-bit counters each)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t ia = a, ib = b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t xa = __shfl_up_sync(0xffffffffu, ia, o), xb = __shfl_up_sync(0xffffffffu, ib, o);
+    if (lane >= o) { ia += xa; ib += xb; }
+  }
+  if (lane == 31) { sh[2 * warp] = ia; sh[2 * warp + 1] = ib; }
+  __syncthreads();
+  uint64_t wa = 0, wb = 0;
+  ta = 0; tb = 0;
+#pragma unroll
+  for (int w = 0; w < EXT_THREADS / 32; ++w) {
+    if (w < warp) { wa += sh[2 * w]; wb += sh[2 * w + 1]; }
+    ta += sh[2 * w]; tb += sh[2 * w + 1];
+  }
+  __syncthreads();
+  a = wa + ia - a;
+  b = wb + ib - b;
+}
+__device__ __forceinline__ int ext_get(uint64_t a, uint64_t b, int k) {
+  return (int)(((k < 4 ? a : b) >> (16 * (k & 3))) & 0xFFFF);
+}
+
+__global__ void __launch_bounds__(EXT_THREADS) k_extract(const int32_t* __restrict__ item, const uint8_t* __restrict__ action,
                           const uint8_t* __restrict__ scenario, const int64_t* __restrict__ ts,
                           const int64_t* __restrict__ ev_off, const int* __restrict__ wave_slot,
                           const unsigned long long* __restrict__ amask,
                           const unsigned long long* __restrict__ smask, int* __restrict__ idx_all,
                           int* __restrict__ vlen_all, int* __restrict__ bad_all, int* __restrict__ err,
                           Dims D) {
+  __shared__ uint64_t sh[2 * EXT_THREADS / 32];
+  __shared__ unsigned long long sam[8], ssm[8];
   const int u = blockIdx.x;
   const long long s = ev_off[u], e = ev_off[u + 1];
   const int slot = wave_slot[u];
   int flags = 0;
-  for (long long i = s + threadIdx.x; i < e; i += blockDim.x) {
-    int it = item[i];
-    if (it < 0 || it >= D.V || action[i] >= D.A || scenario[i] >= D.R) flags |= ERR_RANGE;
-    if (i > s && ts[i] < ts[i - 1]) flags |= ERR_UNSORTED;
+  // validation sweep, 8 independent events per thread per step (the loads of a
+  // step are all in flight together: the sweep is latency-, not issue-bound)
+  constexpr int VU = 8;
+  for (long long i0 = s + threadIdx.x; i0 < e; i0 += (long long)VU * EXT_THREADS) {
+    int it[VU];
+    unsigned ac[VU], sc[VU];
+    long long t1[VU], t0[VU];
+#pragma unroll
+    for (int q = 0; q < VU; ++q) {
+      const long long i = i0 + (long long)q * EXT_THREADS;
+      const bool in = i < e;
+      it[q] = in ? item[i] : 0;
+      ac[q] = in ? action[i] : 0u;
+      sc[q] = in ? scenario[i] : 0u;
+      t1[q] = in ? ts[i] : 0;
+      t0[q] = (in && i > s) ? ts[i - 1] : t1[q];
+    }
+#pragma unroll
+    for (int q = 0; q < VU; ++q) {
+      if (it[q] < 0 || it[q] >= D.V || ac[q] >= (unsigned)D.A || sc[q] >= (unsigned)D.R) flags |= ERR_RANGE;
+      if (t1[q] < t0[q]) flags |= ERR_UNSORTED;
+    }
+  }
+  if (threadIdx.x < D.Nb) {
+    sam[threadIdx.x] = amask[threadIdx.x];
+    ssm[threadIdx.x] = smask[threadIdx.x];
   }
   int any = __syncthreads_or(flags);
   if (flags) atomicOr(err, flags);
   if (threadIdx.x == 0) bad_all[slot] = any ? 1 : 0;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int k = warp; k < D.Nb; k += blockDim.x >> 5) {
-    const unsigned long long am = amask[k], sm = smask[k];
-    int* idx = idx_all + ((long long)slot * D.Nb + k) * D.nk;
-    int cnt = 0;
-    for (long long base = e - 1; base >= s && cnt < D.nk; base -= 32) {
-      long long i = base - lane;
-      bool ok = false;
-      if (i >= s) {
-        unsigned a = action[i], sc = scenario[i];
-        ok = a < 64 && sc < 64 && ((am >> a) & 1ull) && ((sm >> sc) & 1ull);
-      }
-      unsigned bal = __ballot_sync(0xffffffffu, ok);
-      if (ok) {
-        int pos = D.nk - 1 - (cnt + __popc(bal & ((1u << lane) - 1u)));
-        if (pos >= 0) idx[pos] = (int)(i - s);
-      }
-      cnt += __popc(bal);
+  int* idx_u = idx_all + (long long)slot * D.Nb * D.nk;
+  int found[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // matches so far per strategy (block-uniform)
+  for (long long seg_end = e; seg_end > s; seg_end -= (long long)EXT_THREADS * EXT_EPT) {
+    bool done = true;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k < D.Nb && found[k] < D.nk) done = false;
+    if (done) break;
+    const long long hi = seg_end - (long long)threadIdx.x * EXT_EPT;  // this thread: events [lo, hi)
+    const long long lo = hi - EXT_EPT;
+    uint8_t ac[EXT_EPT], sc[EXT_EPT];
+#pragma unroll
+    for (int q = 0; q < EXT_EPT; ++q) {  // q = 0 is the newest of the thread's events
+      const long long i = hi - 1 - q;
+      const bool in = i >= s && i >= lo;
+      ac[q] = in ? action[i] : 0xFF;
+      sc[q] = in ? scenario[i] : 0xFF;
     }
-    int v = min(cnt, D.nk);
-    for (int p = lane; p < D.nk - v; p += 32) idx[p] = -1;
-    if (lane == 0) vlen_all[(long long)slot * D.Nb + k] = v;
+    uint64_t ca = 0, cb = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k >= D.Nb) break;
+      const unsigned long long am = sam[k], sm = ssm[k];
+      int c = 0;
+#pragma unroll
+      for (int q = 0; q < EXT_EPT; ++q)
+        c += (ac[q] < 64 && sc[q] < 64 && ((am >> ac[q]) & 1ull) && ((sm >> sc[q]) & 1ull)) ? 1 : 0;
+      if (k < 4) ca |= (uint64_t)c << (16 * k);
+      else cb |= (uint64_t)c << (16 * (k - 4));
+    }
+    uint64_t pa = ca, pb = cb, ta, tb;
+    ext_scan(pa, pb, sh, ta, tb);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k >= D.Nb) break;
+      int rank = found[k] + ext_get(pa, pb, k);
+      if (rank < D.nk) {
+        const unsigned long long am = sam[k], sm = ssm[k];
+        int* idx = idx_u + (long long)k * D.nk;
+#pragma unroll
+        for (int q = 0; q < EXT_EPT; ++q) {
+          const bool ok = ac[q] < 64 && sc[q] < 64 && ((am >> ac[q]) & 1ull) && ((sm >> sc[q]) & 1ull);
+          if (ok) {
+            if (rank < D.nk) idx[D.nk - 1 - rank] = (int)(hi - 1 - q - s);
+            ++rank;
+          }
+        }
+      }
+      found[k] += ext_get(ta, tb, k);
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < D.Nb; ++k) {
+    const int v = min(found[k], D.nk);
+    int* idx = idx_u + (long long)k * D.nk;
+    for (int p = threadIdx.x; p < D.nk - v; p += blockDim.x) idx[p] = -1;
+    if (threadIdx.x == 0) vlen_all[(long long)slot * D.Nb + k] = v;
     if (D.hage && v > 0) {  // relative bias: age of history token p at the request time (G6e:
-      __syncwarp();  // the request time is the last event's timestamp)
+      __syncthreads();      // the request time is the last event's timestamp)
       int* hage = D.hage + ((long long)slot * D.Nb + k) * D.nk;
       const long long t_req = ts[e - 1];  // v > 0 implies e > s
-      for (int p = lane; p < v; p += 32) {
+      for (int p = threadIdx.x; p < v; p += blockDim.x) {
         const long long age = t_req - ts[s + idx[D.nk - v + p]];
         hage[p] = age < 0 ? 0 : (age > 2147483647LL ? 2147483647 : (int)age);
       }
@@ -813,6 +906,25 @@ __global__ void k_kv_import(uint4* __restrict__ pool, const int* __restrict__ pt
   }
 }
 
+// Pipelined replication (climber_encode_user_bcast): the pages of one layer
+// l of every block, [N_b][ppb] pages in that order, packed into / unpacked
+// from one contiguous slab section with 16-byte copies.
+__global__ void k_kv_layer_copy(uint4* __restrict__ pool, const int* __restrict__ ptab, int slot, int l,
+                                long long page_vec, uint4* __restrict__ sec, int unpack, Dims D) {
+  const long long n = (long long)D.Nb * D.ppb * page_vec;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += (long long)gridDim.x * blockDim.x) {
+    const long long i = g / page_vec, w = g % page_vec;
+    const int k = (int)(i / D.ppb), pg = (int)(i % D.ppb);
+    const long long at = (long long)ptab[(((long long)slot * D.Nb + k) * D.L + l) * D.ppb + pg] * page_vec + w;
+    if (unpack) pool[at] = sec[g];
+    else sec[g] = pool[at];
+  }
+}
+void launch_kv_layer_copy(void* pool, const int* ptab, int slot, int l, long long page_bytes, void* sec, bool unpack,
+                          const Dims& D, cudaStream_t s) {
+  k_kv_layer_copy<<<296, 256, 0, s>>>((uint4*)pool, ptab, slot, l, page_bytes / 16, (uint4*)sec, unpack ? 1 : 0, D);
+}
+
 void launch_kv_export(const void* pool, const int* ptab, const int* vlen_all, int slot, int per_slot, long long page_bytes,
                       void* slab, const Dims& D, int dtype, int r, cudaStream_t s) {
   k_kv_export<<<592, 256, 0, s>>>((const uint4*)pool, ptab, vlen_all, slot, per_slot, page_bytes / 16, (int*)slab,
@@ -890,7 +1002,7 @@ static inline unsigned blocks_for(long long threads, int bs) { return (unsigned)
 void launch_extract(const EventsDev& ev, const int64_t* ev_off, const int* wave_slot, int U,
                     const unsigned long long* amask, const unsigned long long* smask, int* idx_all,
                     int* vlen_all, int* bad_all, int* err, const Dims& D, cudaStream_t s) {
-  k_extract<<<U, 256, 0, s>>>(ev.item, ev.action, ev.scenario, ev.ts, ev_off, wave_slot, amask, smask, idx_all,
+  k_extract<<<U, EXT_THREADS, 0, s>>>(ev.item, ev.action, ev.scenario, ev.ts, ev_off, wave_slot, amask, smask, idx_all,
                               vlen_all, bad_all, err, D);
 }
 

@@ -69,6 +69,8 @@ template <typename T>
 void launch_probe_pages(T* pool, const int* ptab, int slot, int k, int l, int key_off, const Dims& D, cudaStream_t s);
 template <typename T>
 void launch_probe_qkv(T* QKV, long long rows, const Dims& D, cudaStream_t s);
+void launch_kv_layer_copy(void* pool, const int* ptab, int slot, int l, long long page_bytes, void* sec, bool unpack,
+                          const Dims& D, cudaStream_t s);
 void launch_kv_export(const void* pool, const int* ptab, const int* vlen_all, int slot, int per_slot, long long page_bytes,
                       void* slab, const Dims& D, int dtype, int r, cudaStream_t s);
 void launch_kv_import(void* pool, const int* ptab, int* vlen_all, int slot, int per_slot, long long page_bytes,

@@ -144,6 +144,67 @@ def rank_request_sharded_lib(cl, dist, events, r: int, items, root: int = 0):
     return out
 
 
+def rank_request_sharded_pipelined(cl, dist, events, r: int, items, root: int = 0):
+    """Candidate sharding with the K/V replicated WHILE it is encoded
+    (climber_encode_user_bcast: the root broadcasts each layer's pages as soon
+    as its QKV GEMM wrote them, receivers unpack section by section, no host
+    sync).  Same return convention as rank_request_sharded."""
+    torch = cl.torch
+    G, rank = dist.get_world_size(), dist.get_rank()
+    M = int(items.numel())
+    handle = cl.encode_user_bcast(events if rank == root else None, r, root)
+    lo, hi = shard_bounds(M, G, rank)
+    width = -(-M // G)
+    part = torch.full((width,), float("nan"), dtype=torch.float32, device=items.device)
+    if hi > lo:
+        part[:hi - lo] = cl.score_items(handle, items[lo:hi])
+    parts = [torch.empty_like(part) for _ in range(G)]
+    dist.all_gather(parts, part)
+    cl.release(handle)
+    if rank != root:
+        return None
+    out = torch.empty(M, dtype=torch.float32, device=items.device)
+    for g in range(G):
+        a, b = shard_bounds(M, G, g)
+        out[a:b] = parts[g][:b - a]
+    return out
+
+
+def rank_request_layered_protocol(backend, dist, events, r: int, items, root: int = 0):
+    """The section protocol of climber_encode_user_bcast written against a
+    backend (for the gloo tests): the root produces a header section and one
+    section per layer, every rank takes part in 1 + L broadcasts in that order,
+    receivers rebuild the cache from the sections, then candidates are
+    sharded and gathered as in rank_request_sharded."""
+    torch = backend.torch
+    G, rank = dist.get_world_size(), dist.get_rank()
+    M = int(items.numel())
+    n_layers, sec_bytes = backend.layered_shape()
+    if rank == root:
+        handle, sections = backend.encode_layered(events, r)    # [header] + [layer 0 .. L-1]
+    else:
+        handle, sections = None, [torch.empty(n, dtype=torch.uint8, device=backend.device) for n in sec_bytes]
+    for sec in sections:                                         # header first, then layer by layer
+        dist.broadcast(sec, src=root)
+    if rank != root:
+        handle = backend.import_layered(sections, r)
+    lo, hi = shard_bounds(M, G, rank)
+    width = -(-M // G)
+    part = torch.full((width,), float("nan"), dtype=torch.float32, device=backend.device)
+    if hi > lo:
+        part[:hi - lo] = backend.score(handle, items[lo:hi])
+    parts = [torch.empty_like(part) for _ in range(G)]
+    dist.all_gather(parts, part)
+    backend.release(handle)
+    if rank != root:
+        return None
+    out = torch.empty(M, dtype=torch.float32, device=backend.device)
+    for g in range(G):
+        a, b = shard_bounds(M, G, g)
+        out[a:b] = parts[g][:b - a]
+    return out
+
+
 # ---------------------------------------------------------------------------
 # block-parallel serving (SURVEY §8(f) NEXT-2; PAPER.md L155 "block-parallel
 # KV cache", L203: the N_b blocks are independent until the fusion step)

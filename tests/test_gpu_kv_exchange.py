@@ -362,3 +362,50 @@ def test_export_rejects_block_range_handle_and_broadcast_failure_is_symmetric():
     assert torch.equal(cl.score_items(h, cand), ref)
     cl.release(h)
     cl.stream_status()
+
+
+@pytest.mark.parametrize("name,rel_bias", [("small", 0), ("medium", 1)])
+def test_encode_user_bcast_pipelined(name, rel_bias):
+    # climber_encode_user_bcast over a world-1 NCCL communicator: the root's
+    # handle scores exactly like a plain encode; with CLIMBER_DEBUG_BCAST_SELF
+    # (subprocess: the knob is read once) the root also runs the receiver path
+    # (header + per-layer unpack from the slab sections) into a second handle,
+    # which must score bit-identically
+    import subprocess
+    import sys
+    import torch
+    from paper_2502_09888_b200 import nccl_unique_id
+    cfg = synth.preset(name, rel_bias=rel_bias)
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 5, B=1)
+    cl = make_gpu(cfg, w, 1, kv_users=3, rank=0, world=1, nccl_uid=nccl_unique_id())
+    item, action, scenario, ts, cand = to_dev(batch)
+    r = int(batch.r[0])
+    h = cl.encode_user(item, action, scenario, ts, r)
+    ref = cl.score_items(h, cand)
+    cl.release(h)
+    h2 = cl.encode_user_bcast((item, action, scenario, ts), r, root=0)
+    assert torch.equal(cl.score_items(h2, cand), ref)
+    cl.release(h2)
+    cl.stream_status()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import sys, torch; sys.path[:0] = [%r, %r]
+import synth
+from helpers import make_gpu, to_dev
+from paper_2502_09888_b200 import nccl_unique_id
+cfg = synth.preset(%r, rel_bias=%d); w = synth.make_weights(cfg, 0); batch = synth.make_batch(cfg, 5, B=1)
+cl = make_gpu(cfg, w, 1, kv_users=3, rank=0, world=1, nccl_uid=nccl_unique_id())
+item, action, scenario, ts, cand = to_dev(batch)
+r = int(batch.r[0])
+h = cl.encode_user(item, action, scenario, ts, r)
+ref = cl.score_items(h, cand)
+cl.release(h)
+h2 = cl.encode_user_bcast((item, action, scenario, ts), r, root=0)   # the received copy
+assert torch.equal(cl.score_items(h2, cand), ref)
+cl.stream_status()
+print("ok")
+""" % (root, os.path.join(root, "tests"), name, rel_bias)
+    env = dict(os.environ, CLIMBER_DEBUG_BCAST_SELF="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]

@@ -198,3 +198,89 @@ def test_two_rank_block_parallel_matches_single_process():
     u = synth.make_user(cfg, np.random.default_rng(4), n_s=150, M=5)
     ref = O.sumi_scores(cfg, w, synth.strategies_for(cfg.N_b, cfg.R), u, 0)
     np.testing.assert_allclose(res[0], ref, rtol=0, atol=1e-12)     # fp64 transport: exact
+
+
+# ---------------------------------------------------------------------------
+# the section protocol of climber_encode_user_bcast (header, then one section
+# per layer, 1 + L broadcasts in that order) with the oracle behind it
+# ---------------------------------------------------------------------------
+class OracleLayeredBackend(OracleBackend):
+    """Sections as length-prefixed pickles: the header carries the extraction
+    result, request scenario and times; layer section l the K/V of layer l of
+    every block (the library's layout: [N_b][pages] of layer l)."""
+    SEC = 1 << 20
+
+    def layered_shape(self):
+        return self.cfg.L, [self.SEC] * (1 + self.cfg.L)
+
+    def _pack(self, obj):
+        blob = pickle.dumps(obj)
+        t = self.torch.zeros(self.SEC, dtype=self.torch.uint8)
+        t[:8] = self.torch.tensor(list(len(blob).to_bytes(8, "little")), dtype=self.torch.uint8)
+        t[8:8 + len(blob)] = self.torch.tensor(list(blob), dtype=self.torch.uint8)
+        return t
+
+    def _unpack(self, t):
+        n = int.from_bytes(bytes(t[:8].tolist()), "little")
+        return pickle.loads(bytes(t[8:8 + n].tolist()))
+
+    def encode_layered(self, events, r):
+        cache = self.encode(events, r)
+        head = self._pack((cache.idx, cache.vlen, cache.r, cache.t_hist, cache.t_req))
+        layers = [self._pack([(cache.K[k][l], cache.V[k][l]) for k in range(self.cfg.N_b)])
+                  for l in range(self.cfg.L)]
+        return cache, [head] + layers
+
+    def import_layered(self, sections, r):
+        import oracle as O
+        idx, vlen, rr, t_hist, t_req = self._unpack(sections[0])
+        assert rr == r
+        per_layer = [self._unpack(s) for s in sections[1:]]
+        K = [[per_layer[l][k][0] for l in range(self.cfg.L)] for k in range(self.cfg.N_b)]
+        V = [[per_layer[l][k][1] for l in range(self.cfg.L)] for k in range(self.cfg.N_b)]
+        return O.Cache(idx, vlen, K, V, rr, t_hist, t_req)
+
+
+def _layered_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    import synth
+    from paper_2502_09888_b200.sharded import rank_request_layered_protocol
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = synth.preset("tiny", L=3, M=9)
+    w = synth.make_weights(cfg, 2)
+    u = synth.make_user(cfg, np.random.default_rng(5), n_s=130, M=9)
+    item, action, scenario, _ = u.user_events(0)
+    be = OracleLayeredBackend(cfg, w, synth.strategies_for(cfg.N_b, cfg.R))
+    events = (item, action, scenario) if rank == 0 else None
+    out = rank_request_layered_protocol(be, dist, events, int(u.r[0]), torch.from_numpy(u.user_cands(0)))
+    q.put((rank, None if out is None else out.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_layered_replication_protocol():
+    sys.path.insert(0, ROOT)
+    import oracle as O
+    import synth
+    port = socket.socket()
+    port.bind(("127.0.0.1", 0))
+    p = port.getsockname()[1]
+    port.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_layered_worker, args=(r, 2, p, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=180) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert res[1] is None
+    cfg = synth.preset("tiny", L=3, M=9)
+    w = synth.make_weights(cfg, 2)
+    u = synth.make_user(cfg, np.random.default_rng(5), n_s=130, M=9)
+    ref = O.sumi_scores(cfg, w, synth.strategies_for(cfg.N_b, cfg.R), u, 0)
+    np.testing.assert_allclose(res[0], ref, rtol=0, atol=1e-6)   # fp32 transport of fp64 scores
