@@ -659,8 +659,11 @@ void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r,
   }
   fa::Args a{Q, nullptr, wave_slot, wave_r, ptab, vlen_all, tau, O, k, l, U, (long long)U * D.nk, D, nullptr};
   dim3 grid((D.nk + fa::ROWS - 1) / fa::ROWS, D.h, U * nbk);
+  const long long n_cta = (long long)grid.x * grid.y * grid.z;
+  a.trace = fa::trace_begin(n_cta);
   if (D.dh == 64) fa::launch<64, fa::MODE_HIST>(mq, mkv, a, grid, s);
   else fa::launch<32, fa::MODE_HIST>(mq, mkv, a, grid, s);
+  fa::trace_end(a.trace, n_cta, s);
 }
 
 }  // namespace climber
