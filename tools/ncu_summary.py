@@ -14,7 +14,9 @@ def launches(path):
         name = r[ki].split("(")[0].split("<")[0].replace("void ", "").strip()
         if "k_attn<" in r[ki]:
             name = "k_attn<" + r[ki].split("k_attn<")[1].split(">")[0] + ">"
-        if "k_attn_fa<" in r[ki]:
+        if "k_attn_fusion_pair" in r[ki]:
+            name = "k_attn_fusion_pair"
+        elif "k_attn_fa<" in r[ki]:
             args = r[ki].split("k_attn_fa<")[1].split(">")[0].replace("(int)", "").split(",")
             name = "k_attn_fa<d_h=%s, %s>" % (args[0].strip(), "SUMI" if args[1].strip() == "0" else "HIST")
         if "k_gemm_tc<" in r[ki]:
@@ -32,7 +34,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "launch__grid_size", "smsp__inst_executed_pipe_xu", "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
-        "sm__inst_executed_pipe_uniform", "sm__pipe_shared_cycles_active"]
+        "sm__inst_executed_pipe_uniform", "sm__pipe_shared_cycles_active",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"]
 
 def full(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
