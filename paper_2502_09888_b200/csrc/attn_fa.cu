@@ -36,9 +36,10 @@
 // BIAS = 1 adds Eq. 3's relative bias f_b^{p,t}(a_k, r) to the raw scores before
 // the 1/(sqrt(d_h) tau) scaling (G6b-G6e): SUMI rows add the request's
 // candidate-row bias cbias[slot][l][k][head][j] (the same for every candidate);
-// history rows look up b_pos[bucket_pos(t - j)] + b_time[bucket_time(age_j -
-// age_t)] from tables staged in shared memory (causal: one 64 x 7 (offset
-// bucket, time bucket) table, one lookup per score).
+// history rows add b_pos[bucket_pos(t - j)] + b_time[bucket_time(age_j -
+// age_t)] from tables staged in shared memory (causal: a per-offset table of
+// b_pos[bucket_pos(d)] -- consecutive offsets across the lanes, no bank
+// conflicts -- and the time bucket by a comparison tree).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -73,12 +74,14 @@ struct Lay {
   static constexpr int V_OFF = K_OFF + KST * KV_B;        // [VST] V chunks
   static constexpr int BAR_OFF = V_OFF + VST * KV_B;
   static constexpr int PG_OFF = BAR_OFF + 256;            // page ids of the (user, block, layer), <= 32
-  // relative bias (BIAS = 1): b_pos [128], b_time [16], causal 2-D lookup [64 x 7],
+  // relative bias (BIAS = 1): b_pos [128], b_time [16], (spare [64 x 7]),
   // then the (user, block)'s row of n_k <= 1024 values: SUMI the candidate-row
   // bias of this (layer, head), HIST the token ages
   static constexpr int BIAS_OFF = PG_OFF + 128;
   static constexpr int BROW_OFF = BIAS_OFF + (NB_POS + 16 + 64 * 7) * 4;
-  static constexpr int TOTAL = BROW_OFF + 1024 * 4 + 1024;  // + 1024 B alignment slack
+  // causal history: b_pos[bucket_pos(d)] for offsets d in [-127, n_k) (float)
+  static constexpr int PBT_OFF = BROW_OFF + 1024 * 4;
+  static constexpr int TOTAL = PBT_OFF + (1024 + 128) * 4 + 1024;  // + 1024 B alignment slack
   // SUMI: k_self / v_self are parked in the last K and V stages until the self term is read
   static constexpr int KS_OFF = K_OFF + (KST - 1) * KV_B;
   static constexpr int VS_OFF = V_OFF + (VST - 1) * KV_B;
@@ -117,6 +120,18 @@ __device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
   uint64_t r;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
+}
+// explicit shared-space loads (the aligned smem base is a generic pointer:
+// without these the compiler emits generic LD with 64-bit addresses)
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int4 lds_v4(uint32_t a) {
+  int4 v;
+  asm("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
 }
 __device__ __forceinline__ float max3(float a, float b, float c) {
   float r;
@@ -311,7 +326,6 @@ __global__ void __launch_bounds__(THREADS, 2)
     // relative bias (BIAS = 1): this (layer, block, scenario, head)'s tables in smem
     float* sbp = reinterpret_cast<float*>(smem + Ly::BIAS_OFF);
     float* sbt = sbp + NB_POS;
-    float* lut = sbt + 16;  // causal history: lut[bp * 7 + bt] = b_pos[bp] + b_time[bt], bp < 64, bt < 7
     const int* hag = nullptr;
     const float* cbr = nullptr;
     int t_age = 0;
@@ -319,8 +333,6 @@ __global__ void __launch_bounds__(THREADS, 2)
       const long long br = bias_row(D, a.l, kblk, r, head);
       sbp[row] = D.bpos[br * NB_POS + row];
       if (row < NB_TIME) sbt[row] = D.btime[br * NB_TIME + row];
-      if (MODE == MODE_HIST && D.causal)
-        for (int e = row; e < 64 * 7; e += 128) lut[e] = D.bpos[br * NB_POS + e / 7] + D.btime[br * NB_TIME + e % 7];
       // the (user, block)'s row (ages or candidate-row bias) in smem: the
       // per-chunk reads are broadcast shared loads off the critical path
       const int* gag = D.hage + ((long long)slot * D.Nb + kblk) * D.nk;
@@ -328,6 +340,11 @@ __global__ void __launch_bounds__(THREADS, 2)
       int* srow = reinterpret_cast<int*>(smem + Ly::BROW_OFF);
       for (int i = row; i < D.nk; i += 128)
         srow[i] = MODE == MODE_SUMI ? __float_as_int(gcb[i]) : gag[i];
+      if (MODE == MODE_HIST && D.causal) {  // offset -> its position bias, offsets -127 .. n_k - 1
+        float* pbt = reinterpret_cast<float*>(smem + Ly::PBT_OFF);
+        const long long br = bias_row(D, a.l, kblk, r, head);
+        for (int i = row; i < D.nk + 127; i += 128) pbt[i] = i >= 127 ? D.bpos[br * NB_POS + bucket_pos(i - 127)] : 0.f;
+      }
       named_sync(1, 128);
       hag = srow;
       cbr = reinterpret_cast<const float*>(srow);
@@ -389,10 +406,13 @@ __global__ void __launch_bounds__(THREADS, 2)
       if (trs && j < 12) trs[40 + j] = clock64();
       if constexpr (BIAS) {  // R = QK^T + f_b (before the 1/(sqrt(d_h) tau) scaling, Eq. 3)
         if (MODE == MODE_SUMI) {
-          const float4* c4 = reinterpret_cast<const float4*>(cbr + key0);
+          const uint32_t c4 = smem_u32(cbr + key0);
 #pragma unroll
           for (int i = 0; i < KEYS; i += 4) {
-            const float4 b = (key0 + i < D.nk) ? c4[i >> 2] : make_float4(0.f, 0.f, 0.f, 0.f);
+            int4 bi = make_int4(0, 0, 0, 0);
+            if (key0 + i < D.nk) bi = lds_v4(c4 + 4u * i);
+            const float4 b = make_float4(__int_as_float(bi.x), __int_as_float(bi.y), __int_as_float(bi.z),
+                                         __int_as_float(bi.w));
             const float2 s01 = f2_unpack(f2_add(f2_pack(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])),
                                                 f2_pack(b.x, b.y)));
             const float2 s23 = f2_unpack(f2_add(f2_pack(__uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3])),
@@ -403,23 +423,41 @@ __global__ void __launch_bounds__(THREADS, 2)
             sr[i + 3] = __float_as_uint(s23.y);
           }
         } else {
-          // t_row - t_key = age_key - age_row; key ages 4 per 16-byte load
+          // t_row - t_key = age_key - age_row; key ages 4 per 16-byte load.
+          // The mask mode is hoisted out of the element loops: a branch per
+          // score serialises the shared loads (measured 35k cycles / chunk)
           const int4* a4 = reinterpret_cast<const int4*>(hag + key0);
+          if (D.causal) {
+            // offsets >= 0 and time deltas >= 0 on every visible key: the
+            // position bias from the per-offset table (the offset t - j >=
+            // -127 inside a causal tile's chunks; consecutive offsets across
+            // the lanes: no bank conflicts), the time bucket by a 3-level
+            // comparison tree (the edges of S:L285), <= 7 time entries
+            const uint32_t pbt = smem_u32(smem + Ly::PBT_OFF) + 4u * (127 + t_row - key0);
+            const uint32_t sag = smem_u32(hag + key0), sbt_a = smem_u32(sbt);
 #pragma unroll
-          for (int i = 0; i < KEYS; i += 4) {
-            const int4 ka = (key0 + i < D.nk) ? a4[i >> 2] : make_int4(0, 0, 0, 0);
-            const int kv4[4] = {ka.x, ka.y, ka.z, ka.w};
+            for (int i = 0; i < KEYS; i += 4) {
+              const int4 ka = (key0 + i < D.nk) ? lds_v4(sag + 4u * i) : make_int4(0, 0, 0, 0);
+              const int kv4[4] = {ka.x, ka.y, ka.z, ka.w};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              float b;
-              if (D.causal) {  // offsets >= 0 and time deltas >= 0 on every visible key: one 2-D lookup
-                const int bp = bucket_pos(t_row - (key0 + i + q)) & 63;  // masked keys (offset < 0) stay in range
-                const int bt = bucket_time32(kv4[q] - t_age) % 7;
-                b = lut[bp * 7 + bt];
-              } else {
-                b = sbp[bucket_pos(t_row - (key0 + i + q))] + sbt[bucket_time32(kv4[q] - t_age)];
+              for (int q = 0; q < 4; ++q) {
+                const int dt = kv4[q] - t_age;  // >= 0 on visible keys: branch-free bucket count
+                const int bt = (dt > 0) + (dt >= 60) + (dt >= 3600) + (dt >= 86400) + (dt >= 604800) +
+                               (dt >= 2592000);
+                const float b = lds_f32(pbt - 4u * (i + q)) + lds_f32(sbt_a + 4u * bt);
+                sr[i + q] = __float_as_uint(__uint_as_float(sr[i + q]) + b);
               }
-              sr[i + q] = __float_as_uint(__uint_as_float(sr[i + q]) + b);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < KEYS; i += 4) {
+              const int4 ka = (key0 + i < D.nk) ? a4[i >> 2] : make_int4(0, 0, 0, 0);
+              const int kv4[4] = {ka.x, ka.y, ka.z, ka.w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float b = sbp[bucket_pos(t_row - (key0 + i + q))] + sbt[bucket_time32(kv4[q] - t_age)];
+                sr[i + q] = __float_as_uint(__uint_as_float(sr[i + q]) + b);
+              }
             }
           }
         }

@@ -10,7 +10,7 @@ import synth  # noqa: E402
 from paper_2502_09888_b200 import Climber, ModelConfig  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "large"
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 64
-cfg = synth.preset(name, L=2)
+cfg = synth.preset(name, L=2, rel_bias=int(sys.argv[3]) if len(sys.argv) > 3 else 0)
 w = synth.make_weights(cfg, 0)
 b = synth.make_batch(cfg, 1, B=B)
 cl = Climber(ModelConfig.from_any(cfg), w, synth.strategies_for(cfg.N_b, cfg.R), max_users=B, kv_users=B)
