@@ -412,23 +412,21 @@ extern "C" climber_status climber_create(const climber_config* cfg, const climbe
     }
     Carver cv{reinterpret_cast<char*>(arena)};
     carve(c, cv);
-    const char* env = getenv("CLIMBER_GEMM");
-    c->use_tc = !(env && strcmp(env, "simt") == 0);
-    const char* ea = getenv("CLIMBER_ATTN");
-    c->attn_mode = (ea && strcmp(ea, "simt") == 0) ? 0 : (ea && strcmp(ea, "mma") == 0) ? 1 : 2;
+    // bf16: tcgen05 GEMMs and attention wherever supported (d_h 32 / 64),
+    // mma.sync attention for d_h = 16; fp32: the SIMT verification kernels
+    c->use_tc = true;
+    c->attn_mode = 2;
     const char* sc = getenv("CLIMBER_SYNC_CHECK");
     c->sync_check = sc && atoi(sc) != 0;
-    const char* gr = getenv("CLIMBER_GRAPHS");
-    c->graphs = !(gr && atoi(gr) == 0);
+    c->graphs = true;
 
     const size_t d = D.d, L = D.L, Nb = D.Nb, F = D.F;
     // Fused-norm bf16 path: every RMSNorm gain is folded into the rows (input
     // dimension) of the weight matrix that consumes the normalised activations,
     // W' = diag(g) W (rounded to bf16 once), and 1/rms is applied per row in
     // that GEMM's epilogue from the producer's partial sums of squares.
-    const char* en = getenv("CLIMBER_FUSED_NORM");
     c->fused = cfg->dtype == CLIMBER_BF16 && c->use_tc && gemm_tc_available() && D.d % 128 == 0 &&
-               (D.dh == 32 || D.dh == 64) && D.Hse % 128 == 0 && !(en && atoi(en) == 0);
+               (D.dh == 32 || D.dh == 64) && D.Hse % 128 == 0;
     std::vector<float> wqkv_f, w1_f, fwqkv_f, fw1_f;
     const float *w_qkv = w->w_qkv, *w1 = w->w1, *f_w_qkv = w->f_w_qkv, *f_w1 = w->f_w1;
     if (c->fused) {
@@ -972,33 +970,14 @@ static void gemm_g(climber_ctx_s* c, int cls, const bf16* A, long long lda, long
   launch_gemm_tc_batched(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
 }
 
-// debug bisection: CLIMBER_GROUPED_MASK bit i = 0 runs stage i per block
-// (bit 0 QKV, 1 SUMI attention, 2 O-proj, 3 FFN-up, 4 FFN-down)
-static int grouped_mask() {
-  const char* m = getenv("CLIMBER_GROUPED_MASK");
-  return m ? atoi(m) : 31;
-}
-static Epilogue shift_epi(Epilogue e, long long k) {
-  if (e.out) e.out = (char*)e.out + k * e.out_bs * ((e.kind == EPI_STORE || e.kind == EPI_QKV_PAGES) ? 2 : 4);
-  if (e.out_b16) e.out_b16 = (char*)e.out_b16 + k * e.out_b16_bs * 2;
-  if (e.part) e.part += k * e.part_bs;
-  if (e.rs_part) e.rs_part += k * e.rs_bs;
-  return e;
-}
-static void gemm_stage(climber_ctx_s* c, int bit, int cls, const bf16* A, long long lda, long long a_bs, const bf16* B,
-                       long long ldb, long long b_bs, long long M, int N, int K, int batch, const Epilogue& e,
-                       cudaStream_t s) {
-  if (grouped_mask() & bit) {
-    gemm_g(c, cls, A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
-  } else {
-    for (int k = 0; k < batch; ++k)
-      gemm_g(c, cls, A + k * a_bs, lda, 0, B + k * b_bs, ldb, 0, M, N, K, 1, shift_epi(e, k), s);
-  }
+static void gemm_stage(climber_ctx_s* c, int /*stage*/, int cls, const bf16* A, long long lda, long long a_bs,
+                       const bf16* B, long long ldb, long long b_bs, long long M, int N, int K, int batch,
+                       const Epilogue& e, cudaStream_t s) {
+  gemm_g(c, cls, A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
 }
 
 static bool grouped_ok(const climber_ctx_s* c) {
-  const char* g = getenv("CLIMBER_GROUPED");
-  return c->fused && c->attn_mode == 2 && attn_tc_supported(c->D.dh, c->D.nk, false) && !(g && atoi(g) == 0);
+  return c->fused && c->attn_mode == 2 && attn_tc_supported(c->D.dh, c->D.nk, false);
 }
 
 // blocks [k0, k0 + nbk) only (block-parallel serving, NEXT-2); the layouts
@@ -1009,7 +988,7 @@ static void encode_wave_grouped(climber_ctx_s* c, const EventsDev& ev, int u0, i
   if (nbk < 0) nbk = c->D.Nb;
   const Dims& D = c->D;
   const long long rows = (long long)U * D.nk;  // per block
-  const long long d = D.d, F = D.F, pld = c->pld, Nb = D.Nb, Lk = D.L;
+  const long long d = D.d, F = D.F, pld = c->pld, Lk = D.L;
   const int* wslot = c->d_slots + u0;
   const int* wr = c->d_r + u0;
   {
@@ -1111,14 +1090,8 @@ static void score_blocks_grouped(climber_ctx_s* c, const int32_t* items, const i
     {
       Prof p(c, CLIMBER_K_ATTN_SUMI, s, 4.0 * P * (D.nk + 1) * d * nbk,
              ((double)P * d * 2 * 4 + (double)U * D.nk * d * 4) * nbk);
-      if (grouped_mask() & 2) {
-        launch_attn_sumi_tc(QKV, P, wcand, wslot, wr, U, Mmax_wave, (const bf16*)c->pool, c->n_pages * 2 * PAGE,
-                            c->ptab, c->vlen_all, c->tau, O, k0, l, D, s, nbk);
-      } else {
-        for (int k = 0; k < nbk; ++k)
-          launch_attn_sumi_tc(QKV + k * P * 3 * d, P, wcand, wslot, wr, U, Mmax_wave, (const bf16*)c->pool,
-                              c->n_pages * 2 * PAGE, c->ptab, c->vlen_all, c->tau, O + k * P * d, k0 + k, l, D, s, 1);
-      }
+      launch_attn_sumi_tc(QKV, P, wcand, wslot, wr, U, Mmax_wave, (const bf16*)c->pool, c->n_pages * 2 * PAGE,
+                          c->ptab, c->vlen_all, c->tau, O, k0, l, D, s, nbk);
     }
     Epilogue eo = epi_resid_norm(gC, ldC, gCb, gpart, Nb * pld);
     eo.out_bs = d; eo.out_b16_bs = d; eo.part_bs = pld;
@@ -1900,7 +1873,7 @@ static climber_status rank_one_graph(climber_ctx_s* c, long long E, long long P,
     // the score runs in its own scratch rows (after the encode's) so the two
     // streams never share a buffer; without room, one stream
     const long long enc_rows = (long long)c->D.nk * c->D.Nb;
-    const bool overlap = enc_rows + P * c->D.Nb <= c->rows_cap && !getenv("CLIMBER_LATENCY_SERIAL");
+    const bool overlap = enc_rows + P * c->D.Nb <= c->rows_cap;
     if (e == cudaSuccess) e = cudaStreamBeginCapture(c->g_stream, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess && overlap) {
       const long long d = c->D.d;

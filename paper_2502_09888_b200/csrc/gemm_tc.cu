@@ -539,18 +539,6 @@ bool gemm_tc_available() { return tc::get_encode() != nullptr; }
 
 void launch_gemm_tc_batched(const bf16* A, long long lda, long long a_bs, const bf16* B, long long ldb,
                             long long b_bs, long long M, int N, int K, int batch, const Epilogue& e, cudaStream_t s) {
-  // Variant per epilogue cost (measured with tools/bench_gemm.py on B200):
-  //   1: 4 epilogue warps, 4 stages, double-buffered staging (plain store, residual)
-  //   2: 8 epilogue warps, 3 stages, double-buffered staging
-  //   3: 8 epilogue warps, 4 stages, single staging buffer (SiLU / sigmoid:
-  //      MUFU-heavy epilogues need 8 warps to keep up with the MMA)
-  static int forced = -1, cg = -1;
-  if (forced < 0) {
-    const char* v = getenv("CLIMBER_GEMM_VARIANT");
-    forced = v ? atoi(v) : 0;
-    const char* c = getenv("CLIMBER_GEMM_CG");
-    cg = c ? atoi(c) : 2;
-  }
   // small launches: 128 x 128 single-CTA tiles (4x the tiles) below
   // CLIMBER_GEMM_SMALL_WAVES (2) waves of pair CTAs and below
   // CLIMBER_GEMM_SMALL_GFLOP (1.5) GFLOP per launch.  Measured on one request
@@ -578,43 +566,17 @@ void launch_gemm_tc_batched(const bf16* A, long long lda, long long a_bs, const 
     }
     return;
   }
-  if (cg == 2) {  // CTA pairs: 256 x BN tiles, each CTA streams half of B
+  {  // CTA pairs: 256 x BN tiles, each CTA streams half of B
     if (e.kind == EPI_RESID_NORM) {
       if (N % 256 == 0) tc::launch<256, 5, 4, 2, 1, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
       else tc::launch<128, 6, 4, 2, 1, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
       return;
     }
-    // 8 epilogue warps for the plain epilogues too (QKV / K/V-page stores): the
-    // K = 512 launches are paced by the epilogue, 993-1002 vs 895 TFLOP/s for
-    // the QKV class in the large step (CLIMBER_GEMM_EPI8=0: 4 warps, 2 buffers)
-    static const bool epi8 = !(getenv("CLIMBER_GEMM_EPI8") && atoi(getenv("CLIMBER_GEMM_EPI8")) == 0);
-    const bool heavy = ((e.kind == EPI_STORE || e.kind == EPI_STORE_F32) && e.act != ACT_NONE) || epi8;
-    // CLIMBER_GEMM_EPI16=1 (measurement knob): 16 epilogue warps for the activation epilogues
-    static const bool epi16 = getenv("CLIMBER_GEMM_EPI16") && atoi(getenv("CLIMBER_GEMM_EPI16")) == 1;
-    const bool act = (e.kind == EPI_STORE || e.kind == EPI_STORE_F32) && e.act != ACT_NONE;
-    if (N % 256 == 0) {
-      if (epi16 && act) tc::launch<256, 5, 16, 1, 0, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
-      else if (heavy) tc::launch<256, 6, 8, 1, 0, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
-      else tc::launch<256, 6, 4, 2, 0, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
-    } else {
-      tc::launch<128, 8, 4, 2, 0, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
-    }
-    return;
-  }
-  if (e.kind == EPI_RESID_NORM) {  // N % 128 == 0 (checked by the caller)
-    if (N % 256 == 0) tc::launch<256, 3, 4, 2, 1>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
-    else tc::launch<128, 4, 4, 2, 1>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
-    return;
-  }
-  const bool heavy = (e.kind == EPI_STORE || e.kind == EPI_STORE_F32) && e.act != ACT_NONE;
-  int var = forced ? forced : (heavy ? 3 : 1);
-  if (N % 256 == 0) {
-    if (var == 1) tc::launch<256, 4, 4, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
-    else if (var == 2) tc::launch<256, 3, 8, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
-    else tc::launch<256, 4, 8, 1>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
-  } else {
-    if (var == 1) tc::launch<128, 6, 4, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
-    else tc::launch<128, 5, 8, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+    // 8 epilogue warps for every store epilogue (QKV / K/V-page stores and the
+    // activations): the K = 512 launches are paced by the epilogue, 993-1002
+    // vs 895 TFLOP/s for the QKV class in the large step with 4 warps
+    if (N % 256 == 0) tc::launch<256, 6, 8, 1, 0, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+    else tc::launch<128, 8, 4, 2, 0, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
   }
 }
 

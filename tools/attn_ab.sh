@@ -1,7 +1,7 @@
 #!/bin/bash
 # A/B of the attention kernels inside a bounded `large` step (128 users = two
 # waves): kernel_rate of attn_sumi / attn_hist for each setting in "$@"
-# (env assignments, e.g. CLIMBER_GEMM_VARIANT=1; "" = defaults).  Run under gpurun.
+# (env assignments, e.g. CLIMBER_GEMM_SMALL_WAVES=4; "" = defaults).  Run under gpurun.
 CMD="python bench.py --users 128 --steps 3 --warmup 2 --latency-requests 0 --no-cpu-baseline --no-e2e --susi 0"
 for setting in "$@"; do
   out=$(env $setting timeout 600 $CMD 2>&1 | tail -n 1)
