@@ -37,14 +37,16 @@ struct Smem {
   static constexpr int B_BYTES = (BN / CG) * BK * 2;  // CG = 2: this CTA's half of the B tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STG_OFF = STAGES * STAGE_BYTES;  // epilogue staging: 4 warps x 2 x (32 rows x 128 B)
-  // NORM (EPI_RESID_NORM): per warp 2 sets x (fp32 box 32x32 + bf16 box 32x32) = 12 KB
-  static constexpr int STG_WARP = NORM ? 2 * 6144 : SBUF * 32 * 128;
+  // NORM (EPI_RESID_NORM): per warp NORM staging sets x (fp32 box 32x32 + bf16 box 32x32), 6 KB each
+  static constexpr int STG_WARP = NORM ? NORM * 6144 : SBUF * 32 * 128;
   static constexpr int BAR_OFF = STG_OFF + EPIW * STG_WARP;
   static constexpr int TOTAL = BAR_OFF + 512 + 1024;  // barriers + tmem addr, + alignment slack
 };
 
 // EPIW epilogue warps (4 or 8), SBUF staging buffers per epilogue warp (1 or 2),
-// NORM = 1: the EPI_RESID_NORM epilogue (residual add + bf16 copy + row sums of squares)
+// NORM > 0: the EPI_RESID_NORM epilogue (residual add + bf16 copy + row sums of
+// squares) with NORM staging sets per epilogue warp, so NORM - 1 chunks of the
+// old residual are in flight ahead of the one being added
 // CG = 2: CTA pair (2x1 cluster) computing a 256 x BN tile with cta_group::2
 // MMAs issued by the leader; CTA r owns rows 128 r .. 128 r + 127 of the tile
 // (its A half, its TMEM lanes, its epilogue) and loads B rows r BN/2 .. of it.
@@ -60,8 +62,8 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* ldbar = tempty + 2;  // NORM: 2 TMA-load barriers per epilogue warp
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ldbar + 2 * EPIW);
+  uint64_t* ldbar = tempty + 2;  // NORM: one TMA-load barrier per staging set per epilogue warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ldbar + 4 * EPIW);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int crank = CG == 2 ? (int)cluster_rank() : 0;
@@ -86,7 +88,7 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], CG * EPIW);  // one arrival per epilogue warp of the pair (leader's copy)
     }
-    for (int a = 0; a < 2 * EPIW; ++a) mbar_init(&ldbar[a], 1);
+    for (int a = 0; a < 4 * EPIW; ++a) mbar_init(&ldbar[a], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -195,8 +197,11 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       // flight), C += acc in registers (thread = row), the new C is written back
       // in place and as bf16 into a 32x32 box (64B-swizzled), two TMA stores; the
       // row's sum of squares over each 128 columns goes to part[m][n0 / 128].
-      uint64_t* lb = ldbar + (warp - 4) * 2;
-      uint32_t lph[2] = {0u, 0u};
+      constexpr int NS = NORM;  // staging sets per warp
+      uint64_t* lb = ldbar + (warp - 4) * NS;
+      uint32_t lph[NS];
+#pragma unroll
+      for (int i = 0; i < NS; ++i) lph[i] = 0u;
       constexpr int NCH = BN / 32;
       int bt = 0;
       auto issue = [&](long long r0, int n0, int set) {
@@ -212,9 +217,10 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
         const int m_blk = (int)(trm / n_tiles), n_blk = (int)(trm % n_tiles);
         const long long row0 = (long long)(m_blk * CG + crank) * BM + ew * 32;
         const bool rows_ok = row0 < M;  // warp-uniform
-        if (rows_ok) {  // the first two chunks of old residual are requested before the accumulator wait
-          issue(row0, n_blk * BN, 0);
-          issue(row0, n_blk * BN + 32, 1);
+        if (rows_ok) {  // the first NS chunks of old residual are requested before the accumulator wait
+#pragma unroll
+          for (int i = 0; i < NS; ++i)
+            if (i < NCH) issue(row0, n_blk * BN + 32 * i, i);
         }
         mbar_wait(&tfull[acc], acc_phase);
         fence_after();
@@ -222,9 +228,10 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
         float ss = 0.f;
 #pragma unroll 1
         for (int q = 0; q < NCH; ++q) {
-          const int set = q & 1;
+          const int set = q % NS;
           const int n0 = n_blk * BN + q * 32;
-          if (rows_ok && q >= 1 && q + 1 < NCH) issue(row0, n0 + 32, set ^ 1);  // set of chunk q-1
+          // chunk q + NS - 1 into the set of chunk q - 1 (its stores were committed last)
+          if (rows_ok && q >= 1 && q + NS - 1 < NCH) issue(row0, n0 + 32 * (NS - 1), (q - 1) % NS);
           float v[32];
           tmem_ld32(taddr + q * 32, v);
           if (rows_ok) {
@@ -558,7 +565,7 @@ void launch_gemm_tc_batched(const bf16* A, long long lda, long long a_bs, const 
   const double gflop = 2.0 * (double)M * N * K * batch * 1e-9;
   if (pair_ctas < small_waves * tc::num_sms() && gflop < small_gflop) {
     if (e.kind == EPI_RESID_NORM) {
-      tc::launch<128, 4, 4, 2, 1>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+      tc::launch<128, 4, 4, 2, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
     } else {
       const bool heavy = (e.kind == EPI_STORE || e.kind == EPI_STORE_F32) && e.act != ACT_NONE;
       if (heavy) tc::launch<128, 5, 8, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
@@ -568,8 +575,12 @@ void launch_gemm_tc_batched(const bf16* A, long long lda, long long a_bs, const 
   }
   {  // CTA pairs: 256 x BN tiles, each CTA streams half of B
     if (e.kind == EPI_RESID_NORM) {
-      if (N % 256 == 0) tc::launch<256, 5, 4, 2, 1, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
-      else tc::launch<128, 6, 4, 2, 1, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+      // K <= 512 (O-projection): HBM-bound on the residual stream -> four
+      // staging sets per warp (three residual chunks in flight) over three
+      // operand stages; longer K (FFN-down) keeps five operand stages
+      if (N % 256 == 0 && K <= 512) tc::launch<256, 3, 4, 2, 4, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+      else if (N % 256 == 0) tc::launch<256, 5, 4, 2, 2, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
+      else tc::launch<128, 6, 4, 2, 2, 2>(A, lda, a_bs, B, ldb, b_bs, M, N, K, batch, e, s);
       return;
     }
     // 8 epilogue warps for every store epilogue (QKV / K/V-page stores and the
