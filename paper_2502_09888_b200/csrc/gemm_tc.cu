@@ -197,7 +197,8 @@ __global__ void __launch_bounds__(128 + 32 * EPIW, 1)
       // flight), C += acc in registers (thread = row), the new C is written back
       // in place and as bf16 into a 32x32 box (64B-swizzled), two TMA stores; the
       // row's sum of squares over each 128 columns goes to part[m][n0 / 128].
-      constexpr int NS = NORM;  // staging sets per warp
+      constexpr int NS = NORM;  // staging sets per warp (<= 4: the ldbar array)
+      static_assert(NS <= 4, "at most four residual staging sets per warp");
       uint64_t* lb = ldbar + (warp - 4) * NS;
       uint32_t lph[NS];
 #pragma unroll
