@@ -10,9 +10,9 @@
 // chunks of 128 (two 64-token pages); two CTAs per SM, so one CTA's prologue
 // (q tiles) and epilogue overlap the other's chunks.
 //   warp 0      K producer (TMA): q (+ SUMI k_self, v_self, parked in the last
-//               K / V stages until the self term is read) once, then K of each
-//               chunk into a three-stage ring, freed as soon as its Q K^T
-//               completes
+//               K / V stages until the self term is read) and chunk 0's K and V
+//               at once, then K of each further chunk into a three-stage ring,
+//               freed as soon as its Q K^T completes
 //   warp 3      V producer: V of each chunk into a two-stage ring, freed when
 //               its P V completes (K runs ahead of V: Q K_{j+1}^T is needed
 //               before P(j) V_j)
@@ -235,6 +235,18 @@ __global__ void __launch_bounds__(THREADS, 2)
           tma_load_2d(smem + Ly::VS_OFF, &tmQ, bar_q, 2 * D.d + head * DH, (int)rbase);
         }
       }
+      // chunk 0's K and V right behind them (stage 0 of each ring is free):
+      // Q K_0^T needs both q and K_0, so they travel together
+      if (nch > 0) {
+        const int pa = pages[0];
+        const int pb = n_pages > 1 ? pages[1] : pa;
+        mbar_expect_tx(&k_full[0], Ly::KV_B);
+        tma_load_2d(smem + Ly::k_off(0), &tmKV, &k_full[0], head * DH, (int)page_row(pa, 0, 0));
+        tma_load_2d(smem + Ly::k_off(0) + PAGE * Ly::RB, &tmKV, &k_full[0], head * DH, (int)page_row(pb, 0, 0));
+        mbar_expect_tx(&v_full[0], Ly::KV_B);
+        tma_load_2d(smem + Ly::v_off(0), &tmKV, &v_full[0], head * DH, (int)page_row(pa, 1, 0));
+        tma_load_2d(smem + Ly::v_off(0) + PAGE * Ly::RB, &tmKV, &v_full[0], head * DH, (int)page_row(pb, 1, 0));
+      }
     }
   } else if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -264,7 +276,7 @@ __global__ void __launch_bounds__(THREADS, 2)
       uint64_t* full = is_k ? k_full : v_full;
       uint64_t* empty = is_k ? k_empty : v_empty;
       const int kv = is_k ? 0 : 1;
-      for (int j = 0; j < nch; ++j) {
+      for (int j = 1; j < nch; ++j) {  // chunk 0 was issued with the q tiles
         const int st = j % nst;
         mbar_wait(&empty[st], ((j / nst) & 1) ^ 1);
         if (MODE == MODE_SUMI && j == nst - 1) mbar_wait(self_done, 0);  // the last stage held a self tile
@@ -382,7 +394,7 @@ __global__ void __launch_bounds__(THREADS, 2)
             for (int i = 0; i < 8; ++i) vs[cc + i] = 0.f;
           }
         }
-        tmem_st32(tO + lane_off + c, vs);
+        tmem_st32_nw(tO + lane_off + c, vs);  // waited before P(0) is released (or before a rescale)
       }
       l = 1.f;  // the self term's weight
       // the self tiles' stages become K / V stages
@@ -489,6 +501,7 @@ __global__ void __launch_bounds__(THREADS, 2)
       const bool need_pv = j > 0;
       bool pv_seen = false;
       if ((MODE == MODE_SUMI || j > 0) && __any_sync(0xffffffffu, mine)) {
+        if (MODE == MODE_SUMI && j == 0) tmem_st_wait();  // the O = v_self stores
         if (need_pv) {
           mbar_wait(pv_done, (j - 1) & 1);
           fence_after();
