@@ -368,18 +368,26 @@ __global__ void __launch_bounds__(THREADS, 2)
       // XOR-swizzled like the TMA box)
       mbar_wait(bar_q, 0);
       if (trs) trs[126] = clock64();
-      const uint8_t* qrow = smem + Ly::Q_OFF + row * Ly::RB;
-      const uint8_t* krow = smem + Ly::KS_OFF + row * Ly::RB;
-      const uint8_t* vrow = smem + Ly::VS_OFF + row * Ly::RB;
-      float ss = 0.f;
+      // explicit shared loads, all issued before the arithmetic; 8 partial
+      // sums break the dot product's dependence chain
+      const uint32_t qrow = smem_u32(smem + Ly::Q_OFF) + row * Ly::RB;
+      const uint32_t krow = smem_u32(smem + Ly::KS_OFF) + row * Ly::RB;
+      const uint32_t vrow = smem_u32(smem + Ly::VS_OFF) + row * Ly::RB;
+      int4 qv[DH / 8], kv[DH / 8];
 #pragma unroll
       for (int j = 0; j < DH / 8; ++j) {
-        float q[8], k8[8];
-        load8(reinterpret_cast<const bf16*>(qrow + (swz<DH>(row, j) << 4)), q);
-        load8(reinterpret_cast<const bf16*>(krow + (swz<DH>(row, j) << 4)), k8);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) ss = fmaf(q[i], k8[i], ss);
+        qv[j] = lds_v4(qrow + (swz<DH>(row, j) << 4));
+        kv[j] = lds_v4(krow + (swz<DH>(row, j) << 4));
       }
+      float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int j = 0; j < DH / 8; ++j) {
+        const bf16* qb = reinterpret_cast<const bf16*>(&qv[j]);
+        const bf16* kb = reinterpret_cast<const bf16*>(&kv[j]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ps[i] = fmaf(__bfloat162float(qb[i]), __bfloat162float(kb[i]), ps[i]);
+      }
+      float ss = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
       if constexpr (BIAS) ss += sbp[bucket_pos(0)] + sbt[bucket_time32(0)];  // self: offset 0, delta 0
       m_used = valid ? ss * sc : 0.f;
 #pragma unroll
@@ -387,12 +395,10 @@ __global__ void __launch_bounds__(THREADS, 2)
         float vs[32];
 #pragma unroll
         for (int cc = 0; cc < 32; cc += 8) {
-          if (valid) {
-            load8(reinterpret_cast<const bf16*>(vrow + (swz<DH>(row, (c + cc) / 8) << 4)), vs + cc);
-          } else {
+          const int4 vv = lds_v4(vrow + (swz<DH>(row, (c + cc) / 8) << 4));
+          const bf16* vb = reinterpret_cast<const bf16*>(&vv);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) vs[cc + i] = 0.f;
-          }
+          for (int i = 0; i < 8; ++i) vs[cc + i] = valid ? __bfloat162float(vb[i]) : 0.f;
         }
         tmem_st32_nw(tO + lane_off + c, vs);  // waited before P(0) is released (or before a rescale)
       }
@@ -557,6 +563,7 @@ __global__ void __launch_bounds__(THREADS, 2)
       mbar_wait(pv_done, (nch - 1) & 1);
       fence_after();
     }
+    if (trs) trs[27] = clock64();
     const bool have_o = MODE == MODE_SUMI || nch > 0;
     const float inv = (valid && l > 0.f) ? 1.f / l : 0.f;
     uint8_t* qtile = smem + Ly::Q_OFF;
@@ -571,13 +578,18 @@ __global__ void __launch_bounds__(THREADS, 2)
       }
 #pragma unroll
       for (int cc = 0; cc < 32; cc += 8) {
-        float y[8];
+        uint32_t w[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) y[i] = o[cc + i] * inv;
-        store8(reinterpret_cast<bf16*>(qtile + row * Ly::RB + (swz<DH>(row, (c + cc) / 8) << 4)), y);
+        for (int i = 0; i < 4; ++i) {
+          __nv_bfloat162 pp = __floats2bfloat162_rn(o[cc + 2 * i] * inv, o[cc + 2 * i + 1] * inv);
+          w[i] = *reinterpret_cast<uint32_t*>(&pp);
+        }
+        st_shared_v4(qtile + row * Ly::RB + (swz<DH>(row, (c + cc) / 8) << 4), w[0], w[1], w[2], w[3]);
       }
     }
+    if (trs) trs[28] = clock64();
     named_sync(1, 128);
+    if (trs) trs[29] = clock64();
     constexpr int LPR = DH / 8;      // lanes per row, 16 B (8 bf16) each
     constexpr int RPI = 32 / LPR;    // rows per warp instruction
 #pragma unroll
@@ -585,8 +597,8 @@ __global__ void __launch_bounds__(THREADS, 2)
       const int rr = ew * 32 + i + lane / LPR;
       const int cj = lane % LPR;
       if (rr < n_out) {
-        const uint4 val = *reinterpret_cast<const uint4*>(qtile + rr * Ly::RB + (swz<DH>(rr, cj) << 4));
-        *reinterpret_cast<uint4*>(a.O + (rbase + rr) * D.d + head * DH + cj * 8) = val;
+        const int4 val = lds_v4(smem_u32(qtile) + rr * Ly::RB + (swz<DH>(rr, cj) << 4));
+        *reinterpret_cast<int4*>(a.O + (rbase + rr) * D.d + head * DH + cj * 8) = val;
       }
     }
     if (trs) trs[31] = clock64();
@@ -668,7 +680,8 @@ static void trace_end(unsigned long long* buf, long long n_cta, cudaStream_t s) 
   for (int j = 0; j < 12; ++j)
     fprintf(stderr, "[fa trace] chunk %2d: kv %7.0f | S %7.0f ld %7.0f max %7.0f P %7.0f | mma saw P %7.0f\n", j,
             m(96 + j), m(2 * j), m(40 + j), m(52 + j), m(2 * j + 1), m(64 + j));
-  fprintf(stderr, "[fa trace] epilogue %7.0f -> %7.0f\n", m(30), m(31));
+  fprintf(stderr, "[fa trace] epilogue %7.0f: pv_done %7.0f staged %7.0f synced %7.0f end %7.0f\n", m(30), m(27),
+          m(28), m(29), m(31));
   cudaFree(buf);
 }
 
