@@ -611,6 +611,556 @@ __global__ void __launch_bounds__(THREADS, 2)
   }
 }
 
+// ===========================================================================
+// Persistent variant (BIAS = 0): the grid is two CTAs per SM and each CTA
+// walks the tiles t = blockIdx.x, blockIdx.x + gridDim.x, ... in the same
+// (x, head, user x block) order as the one-tile kernel above.  Per CTA the
+// chunk pipeline never drains between tiles:
+//   * q tiles are double-buffered; the producer loads tile i+1's q (and, for
+//     SUMI, its k_self / v_self as items of the K / V rings) while tile i runs;
+//   * the MMA issuer issues S(0) of tile i+1 = Q_{i+1} K_0^T as soon as the
+//     softmax has read S(last) of tile i, so it runs under tile i's last
+//     exponentials;
+//   * the softmax warpgroup goes from P(last) of tile i through its epilogue
+//     (O / l staged in tile i's q buffer, coalesced row stores) and tile
+//     i+1's self term straight into S(0) of tile i+1.
+// The producer (warp 0) computes each tile's geometry once and hands it to
+// the other roles in a descriptor next to the q buffer it fills (published by
+// the q_full barrier; the softmax's q_empty arrival after the epilogue frees
+// both).  Shared memory: 2 q + 3 K + 2 V tiles of 128 rows x 128 B (d_h 64)
+// + 1 KB of barriers / descriptors = 115712 B, exactly half of an SM's
+// 228 KB less the 1 KB each CTA reserves; the dynamic window starts 1024 B
+// aligned (checked at run time).
+// ===========================================================================
+struct PDesc {
+  int done, nch, n_rows, n_out, kend, tile0, head, n_pages;
+  long long rbase;
+  float sc;
+  int pad;
+  int pages[32];
+};
+static_assert(sizeof(PDesc) <= 256, "descriptor slot");
+
+template <int DH>
+struct PLay {
+  static constexpr int RB = DH * 2;
+  static constexpr uint32_t SWZ = (DH == 64) ? 2u : 4u;
+  static constexpr int TILE_B = ROWS * RB;
+  static constexpr int Q_OFF = 0;                          // [2] q tiles, then O staging
+  static constexpr int K_OFF = Q_OFF + 2 * TILE_B;         // [KST] K ring (SUMI: k_self tiles too)
+  static constexpr int V_OFF = K_OFF + KST * TILE_B;       // [VST] V ring (SUMI: v_self tiles too)
+  static constexpr int BAR_OFF = V_OFF + VST * TILE_B;     // barriers (<= 256 B)
+  static constexpr int DESC_OFF = BAR_OFF + 256;           // [2] tile descriptors
+  static constexpr int TOTAL = DESC_OFF + 768;
+  __device__ static constexpr int q_off(int b) { return Q_OFF + b * TILE_B; }
+  __device__ static constexpr int k_off(int i) { return K_OFF + (i % KST) * TILE_B; }
+  __device__ static constexpr int v_off(int i) { return V_OFF + (i % VST) * TILE_B; }
+};
+
+// Producer-side state of one ring: a slot is freed by the MMA (chunk tiles,
+// tcgen05.commit on `empty`) or by the softmax warpgroup (self tiles, 128
+// arrivals on `selff`), so each slot counts its uses of each barrier.
+// Per slot 4 bits in one register: last occupant (bits 0-1: 0 none, 1
+// chunk, 2 self) and the parity of the chunk / self uses so far (bits 2, 3).
+template <int NST>
+struct RingSlots {
+  uint32_t bits = 0;
+  __device__ void init() { bits = 0; }
+  // wait until slot st is free for an item of kind `kind` (1 chunk, 2 self), then record it
+  __device__ void acquire(int st, int kind, uint64_t* empty, uint64_t* selff) {
+    const uint32_t f = (bits >> (4 * st)) & 15u;
+    const uint32_t last = f & 3u, pc = (f >> 2) & 1u, ps = (f >> 3) & 1u;
+    if (last == 1u) mbar_wait(&empty[st], pc ^ 1u);        // the previous chunk use completed
+    else if (last == 2u) mbar_wait(&selff[st], ps ^ 1u);  // the previous self use completed
+    const uint32_t nf = (uint32_t)kind | ((kind == 1 ? pc ^ 1u : pc) << 2) | ((kind == 2 ? ps ^ 1u : ps) << 3);
+    bits = (bits & ~(15u << (4 * st))) | (nf << (4 * st));
+  }
+};
+
+template <int DH, int MODE>
+__global__ void __launch_bounds__(THREADS, 2)
+    k_attn_pers(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, Args a, int ntx,
+                int n_tiles) {
+  using Ly = PLay<DH>;
+  constexpr bool SUMI = MODE == MODE_SUMI;
+  constexpr int SELF = SUMI ? 1 : 0;  // ring items per tile before its chunks
+  extern __shared__ __align__(1024) uint8_t smem[];
+  {
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    if ((smem_u32(smem) & 1023u) != 0u || dyn < (uint32_t)Ly::TOTAL) __trap();
+  }
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Ly::BAR_OFF);
+  uint64_t* q_full = bars;                    // [2]
+  uint64_t* q_empty = q_full + 2;             // [2]
+  uint64_t* k_full = q_empty + 2;             // [KST]
+  uint64_t* k_empty = k_full + KST;           // [KST]
+  uint64_t* k_selff = k_empty + KST;         // [KST] a k_self tile in the slot was read (128 arrivals)
+  uint64_t* v_full = k_selff + KST;           // [VST]
+  uint64_t* v_empty = v_full + VST;           // [VST]
+  uint64_t* v_selff = v_empty + VST;          // [VST]
+  uint64_t* s_full = v_selff + VST;
+  uint64_t* s_read = s_full + 1;
+  uint64_t* p_full = s_read + 1;
+  uint64_t* pv_done = p_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
+  static_assert((2 + 2 + 3 * KST + 3 * VST + 4) * 8 + 4 <= 256, "barrier area");
+  PDesc* desc = reinterpret_cast<PDesc*>(smem + Ly::DESC_OFF);
+
+  const Dims& D = a.D;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmQ) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmKV) : "memory");
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&q_full[b], 1);
+      mbar_init(&q_empty[b], 128);
+    }
+    for (int s = 0; s < KST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&k_selff[s], 128);
+    }
+    for (int s = 0; s < VST; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+      mbar_init(&v_selff[s], 128);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_read, 128);
+    mbar_init(p_full, 128);
+    mbar_init(pv_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  } else if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tS = tmem_base;
+  const uint32_t tP = tmem_base + KEYS;
+  const uint32_t tO = tmem_base + KEYS + KEYS / 2;
+  // clock64 timeline of the first tiles of each CTA (CLIMBER_FA_TRACE), see ptrace_print
+  unsigned long long* tr = a.trace ? a.trace + (long long)blockIdx.x * TRACE_N : nullptr;
+  if (tr && threadIdx.x == 0) tr[127] = clock64();
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
+    if (warp == 0) {
+      // ---------------- q + K producer: tile geometry, q, (k_self), K chunks ----------------
+      int it = 0, kc = 0;
+      RingSlots<KST> ring;
+      ring.init();
+      for (int t = blockIdx.x;; t += gridDim.x) {
+        const bool done = t >= n_tiles;
+        int head = 0, nch = 0, n_rows = 0, n_out = 0, kend = 0, tile0 = 0, n_pages = 0, pg = 0;
+        long long rbase = 0;
+        float sc = 0.f;
+        if (!done) {
+          const int x = t % ntx;
+          head = (t / ntx) % D.h;
+          const int z = t / (ntx * D.h);
+          const int u = z % a.U, kk = z / a.U, kblk = a.k + kk;
+          tile0 = x * ROWS;
+          const int slot = a.wave_slot[u];
+          const int v = a.vlen_all[(long long)slot * D.Nb + kblk];
+          if (SUMI) {
+            const long long p0 = a.cand_off[u], p1 = a.cand_off[u + 1];
+            if (p0 + tile0 >= p1) continue;  // no candidates in this tile: no role ever sees it
+            n_rows = (int)min((long long)ROWS, p1 - p0 - tile0);
+            n_out = n_rows;
+            kend = v;
+            rbase = kk * a.rows_pb + p0 + tile0;
+          } else {
+            n_rows = max(0, min(ROWS, v - tile0));
+            n_out = min(ROWS, D.nk - tile0);
+            kend = D.causal ? min(v, tile0 + ROWS) : v;
+            rbase = kk * a.rows_pb + (long long)u * D.nk + tile0;
+          }
+          nch = (SUMI || n_rows > 0) ? (kend + KEYS - 1) / KEYS : 0;
+          n_pages = min(D.ppb, (nch * KEYS + PAGE - 1) / PAGE);
+          const int* pages = a.ptab + (((long long)slot * D.Nb + kblk) * D.L + a.l) * D.ppb;
+          pg = lane < n_pages ? pages[lane] : 0;
+          sc = LOG2E / (sqrtf((float)DH) * a.tau[((a.l * D.Nb + kblk) * D.R + a.wave_r[u]) * D.h + head]);
+        }
+        const int b = it & 1;
+        mbar_wait(&q_empty[b], ((it >> 1) & 1) ^ 1);
+        PDesc* ds = desc + b;
+        for (int i = 0; i < n_pages; ++i) {
+          const int p = __shfl_sync(0xffffffffu, pg, i);
+          if (lane == 0) ds->pages[i] = p;
+        }
+        if (lane == 0) {
+          ds->done = done;
+          ds->nch = nch;
+          ds->n_rows = n_rows;
+          ds->n_out = n_out;
+          ds->kend = kend;
+          ds->tile0 = tile0;
+          ds->head = head;
+          ds->n_pages = n_pages;
+          ds->rbase = rbase;
+          ds->sc = sc;
+          if (!done && (SUMI || nch > 0)) {
+            mbar_expect_tx(&q_full[b], Ly::TILE_B);
+            tma_load_2d(smem + Ly::q_off(b), &tmQ, &q_full[b], head * DH, (int)rbase);
+          } else {
+            mbar_arrive(&q_full[b]);  // descriptor only
+          }
+        }
+        __syncwarp();
+        if (done) break;
+        if (SUMI) {  // k_self through the K ring (read by the softmax's self term)
+          const int st = kc % KST;
+          ring.acquire(st, 2, k_empty, k_selff);
+          if (lane == 0) {
+            mbar_expect_tx(&k_full[st], Ly::TILE_B);
+            tma_load_2d(smem + Ly::k_off(kc), &tmQ, &k_full[st], D.d + head * DH, (int)rbase);
+          }
+          ++kc;
+        }
+        for (int j = 0; j < nch; ++j, ++kc) {
+          const int st = kc % KST;
+          const int pa = __shfl_sync(0xffffffffu, pg, (2 * j) & 31);
+          const int pb0 = __shfl_sync(0xffffffffu, pg, (2 * j + 1) & 31);
+          const int pb = (2 * j + 1 < n_pages) ? pb0 : pa;  // past the pages: finite, masked keys
+          ring.acquire(st, 1, k_empty, k_selff);
+          if (lane == 0) {
+            mbar_expect_tx(&k_full[st], Ly::TILE_B);
+            tma_load_2d(smem + Ly::k_off(kc), &tmKV, &k_full[st], head * DH, (int)page_row(pa, 0, 0));
+            tma_load_2d(smem + Ly::k_off(kc) + PAGE * Ly::RB, &tmKV, &k_full[st], head * DH,
+                        (int)page_row(pb, 0, 0));
+          }
+        }
+        ++it;
+      }
+    } else if (warp == 3) {
+      // ---------------- V producer: (v_self), V chunks; geometry from the descriptors ----------------
+      int it = 0, vc = 0;
+      RingSlots<VST> ring;
+      ring.init();
+      for (;; ++it) {
+        const int b = it & 1;
+        mbar_wait(&q_full[b], (it >> 1) & 1);
+        const PDesc* ds = desc + b;
+        if (ds->done) break;
+        const int nch = ds->nch, head = ds->head, n_pages = ds->n_pages;
+        const long long rbase = ds->rbase;
+        const int pg = lane < n_pages ? ds->pages[lane] : 0;
+        if (SUMI) {
+          const int st = vc % VST;
+          ring.acquire(st, 2, v_empty, v_selff);
+          if (lane == 0) {
+            mbar_expect_tx(&v_full[st], Ly::TILE_B);
+            tma_load_2d(smem + Ly::v_off(vc), &tmQ, &v_full[st], 2 * D.d + head * DH, (int)rbase);
+          }
+          ++vc;
+        }
+        for (int j = 0; j < nch; ++j, ++vc) {
+          const int st = vc % VST;
+          const int pa = __shfl_sync(0xffffffffu, pg, (2 * j) & 31);
+          const int pb0 = __shfl_sync(0xffffffffu, pg, (2 * j + 1) & 31);
+          const int pb = (2 * j + 1 < n_pages) ? pb0 : pa;
+          ring.acquire(st, 1, v_empty, v_selff);
+          if (lane == 0) {
+            mbar_expect_tx(&v_full[st], Ly::TILE_B);
+            tma_load_2d(smem + Ly::v_off(vc), &tmKV, &v_full[st], head * DH, (int)page_row(pa, 1, 0));
+            tma_load_2d(smem + Ly::v_off(vc) + PAGE * Ly::RB, &tmKV, &v_full[st], head * DH,
+                        (int)page_row(pb, 1, 0));
+          }
+        }
+      }
+    } else if (warp == 1 && lane == 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t idesc_qk = idesc_bf16_major(ROWS, KEYS, 0, 0);
+      constexpr uint32_t idesc_pv = idesc_bf16_major(ROWS, DH, 0, 1);
+      int n_qk = 0;  // Q K^T issued so far (S(n) may be written once S(n-1) was read)
+      auto qk = [&](int b, int item) {
+        if (n_qk > 0) mbar_wait(s_read, (n_qk - 1) & 1);
+        mbar_wait(&k_full[item % KST], (item / KST) & 1);
+        fence_after();
+        const uint64_t qd = make_sdesc(smem_u32(smem + Ly::q_off(b)), 16, 8 * Ly::RB, Ly::SWZ);
+        const uint64_t kd = make_sdesc(smem_u32(smem + Ly::k_off(item)), 16, 8 * Ly::RB, Ly::SWZ);
+#pragma unroll
+        for (int s = 0; s < DH / 16; ++s) mma_bf16(tS, qd + 2 * s, kd + 2 * s, idesc_qk, s > 0 ? 1u : 0u);
+        mma_commit(&k_empty[item % KST]);
+        mma_commit(s_full);
+        if (tr && n_qk < 16) tr[96 + n_qk] = clock64();
+        ++n_qk;
+      };
+      int it = 0, kc = 0, n = 0;
+      mbar_wait(&q_full[0], 0);
+      int done = desc[0].done, nch = desc[0].nch;
+      bool first_issued = false;
+      while (!done) {
+        const int b = it & 1;
+        const int c0 = kc + SELF;  // ring item of chunk 0
+        if (nch > 0 && !first_issued) qk(b, c0);
+        int done2 = 1, nch2 = 0;
+        bool peeked = false, issued2 = false;
+        for (int j = 0; j < nch; ++j) {
+          if (j + 1 < nch) {
+            qk(b, c0 + j + 1);
+          } else {  // S(0) of the next tile under this tile's last exponentials
+            const int b2 = (it + 1) & 1;
+            mbar_wait(&q_full[b2], ((it + 1) >> 1) & 1);
+            done2 = desc[b2].done;
+            nch2 = desc[b2].nch;
+            peeked = true;
+            if (!done2 && nch2 > 0) {
+              qk(b2, c0 + nch + SELF);
+              issued2 = true;
+            }
+          }
+          mbar_wait(p_full, n & 1);
+          const int item = c0 + j;
+          mbar_wait(&v_full[item % VST], (item / VST) & 1);
+          fence_after();
+          if (tr && n < 12) tr[112 + n] = clock64();
+          const uint64_t vd = make_sdesc(smem_u32(smem + Ly::v_off(item)), 16, 8 * Ly::RB, Ly::SWZ);
+#pragma unroll 1
+          for (int s = 0; s < KEYS / 16; ++s) {
+            const uint64_t vds = vd + (uint64_t)((16 * Ly::RB) >> 4) * s;
+            const uint32_t acc = (SUMI || j > 0 || s > 0) ? 1u : 0u;
+            mma_bf16_ts(tO, tP + 8 * s, vds, idesc_pv, acc);
+          }
+          mma_commit(&v_empty[item % VST]);
+          mma_commit(pv_done);
+          ++n;
+        }
+        if (!peeked) {
+          const int b2 = (it + 1) & 1;
+          mbar_wait(&q_full[b2], ((it + 1) >> 1) & 1);
+          done2 = desc[b2].done;
+          nch2 = desc[b2].nch;
+        }
+        kc = c0 + nch;
+        ++it;
+        done = done2;
+        nch = nch2;
+        first_issued = issued2;
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 192;");
+    // ---------------- softmax + epilogue ----------------
+    const int ew = warp & 3;
+    const int row = ew * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
+    int it = 0, kc = 0, n = 0;
+    for (;; ++it) {
+      const int b = it & 1;
+      mbar_wait(&q_full[b], (it >> 1) & 1);
+      const PDesc* ds = desc + b;
+      if (ds->done) break;
+      unsigned long long* tt = (tr && threadIdx.x == 128 && it < 4) ? tr + it * 24 : nullptr;
+      if (tt) tt[0] = clock64();
+      const int nch = ds->nch, n_rows = ds->n_rows, n_out = ds->n_out, kend = ds->kend;
+      const int head = ds->head;
+      const long long rbase = ds->rbase;
+      const float sc = ds->sc;
+      const bool valid = row < n_rows;
+      const int t_row = ds->tile0 + row;
+      const uint32_t qbuf = smem_u32(smem + Ly::q_off(b));
+      float m_used = -INFINITY, l = 0.f;
+      if (SUMI) {
+        // self term: m = s_self, l = 1, O = v_self (k_self / v_self are this
+        // tile's first ring items; released once every row has read them)
+        const int st_k = kc % KST, st_v = kc % VST;
+        mbar_wait(&k_full[st_k], (kc / KST) & 1);
+        if (tt) tt[13] = clock64();
+        const uint32_t qrow = qbuf + row * Ly::RB;
+        const uint32_t krow = smem_u32(smem + Ly::k_off(kc)) + row * Ly::RB;
+        const uint32_t vrow = smem_u32(smem + Ly::v_off(kc)) + row * Ly::RB;
+        int4 qv[DH / 8], kv[DH / 8];
+#pragma unroll
+        for (int j = 0; j < DH / 8; ++j) {
+          qv[j] = lds_v4(qrow + (swz<DH>(row, j) << 4));
+          kv[j] = lds_v4(krow + (swz<DH>(row, j) << 4));
+        }
+        float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < DH / 8; ++j) {
+          const bf16* qb = reinterpret_cast<const bf16*>(&qv[j]);
+          const bf16* kb = reinterpret_cast<const bf16*>(&kv[j]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) ps[i] = fmaf(__bfloat162float(qb[i]), __bfloat162float(kb[i]), ps[i]);
+        }
+        const float ss = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
+        m_used = valid ? ss * sc : 0.f;
+        // generic reads of a TMA-written tile (consumed above), released to
+        // the next TMA write by every row (no proxy fence needed for reads)
+        mbar_arrive(&k_selff[st_k]);
+        if (tt) tt[14] = clock64();
+        mbar_wait(&v_full[st_v], (kc / VST) & 1);
+        if (tt) tt[15] = clock64();
+#pragma unroll
+        for (int c = 0; c < DH; c += 32) {
+          float vs[32];
+#pragma unroll
+          for (int cc = 0; cc < 32; cc += 8) {
+            const int4 vv = lds_v4(vrow + (swz<DH>(row, (c + cc) / 8) << 4));
+            const bf16* vb = reinterpret_cast<const bf16*>(&vv);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) vs[cc + i] = valid ? __bfloat162float(vb[i]) : 0.f;
+          }
+          tmem_st32_nw(tO + lane_off + c, vs);  // waited before P(0) is released (or before a rescale)
+        }
+        l = 1.f;
+        mbar_arrive(&v_selff[st_v]);  // the v_self values were consumed by the TMEM stores
+        if (tt) tt[1] = clock64();
+      }
+      for (int j = 0; j < nch; ++j, ++n) {
+        mbar_wait(s_full, n & 1);
+        fence_after();
+        const int key0 = j * KEYS;
+        int lim = kend - key0;
+        if (!SUMI && D.causal) lim = min(lim, t_row - key0 + 1);
+        uint32_t sr[KEYS];
+#pragma unroll
+        for (int c = 0; c < KEYS; c += 32) tmem_ld32_nw(tS + lane_off + c, sr + c);
+        tmem_ld_wait();
+        fence_before();
+        mbar_arrive(s_read);
+        if (tt && j < 4) tt[2 + 2 * j] = clock64();
+        if (lim < KEYS) {
+#pragma unroll
+          for (int i = 0; i < KEYS; ++i)
+            if (i >= lim) sr[i] = __float_as_uint(-INFINITY);
+        }
+        float mx8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < KEYS; i += 2)
+          mx8[(i >> 1) & 7] = max3(mx8[(i >> 1) & 7], __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
+        const float mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                 fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        const float mx = mraw * sc;
+        const bool mine = mx > m_used + RESCALE_LOG2;
+        const float alpha = mine ? exp2f(m_used - mx) : 1.f;
+        if (mine) {
+          l *= alpha;
+          m_used = mx;
+        }
+        const bool need_pv = j > 0;  // P(j-1) V_{j-1} of this tile (the previous tile's were waited)
+        bool pv_seen = false;
+        if ((SUMI || j > 0) && __any_sync(0xffffffffu, mine)) {
+          if (SUMI && j == 0) tmem_st_wait();
+          if (need_pv) {
+            mbar_wait(pv_done, (n - 1) & 1);
+            fence_after();
+            pv_seen = true;
+          }
+#pragma unroll
+          for (int c = 0; c < DH; c += 16) {
+            uint32_t o[16];
+            tmem_ld16_nw(tO + lane_off + c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st16u(tO + lane_off + c, o);
+          }
+        }
+        const float nb = (m_used == -INFINITY) ? 0.f : -m_used;
+        const uint64_t sc2 = f2_pack(sc, sc), nb2 = f2_pack(nb, nb);
+        uint64_t ls2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+        for (int c = 0; c < KEYS; c += 32) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float2 x = f2_unpack(
+                f2_fma(f2_pack(__uint_as_float(sr[c + i]), __uint_as_float(sr[c + i + 1])), sc2, nb2));
+            const float e0 = ex2_approx(x.x);
+            const float e1 = ex2_approx(x.y);
+            ls2[(i >> 1) & 3] = f2_add(ls2[(i >> 1) & 3], f2_pack(e0, e1));
+            __nv_bfloat162 pp = __floats2bfloat162_rn(e0, e1);
+            pk[i >> 1] = *reinterpret_cast<uint32_t*>(&pp);
+          }
+          if (c == 0 && need_pv && !pv_seen) {
+            mbar_wait(pv_done, (n - 1) & 1);
+            fence_after();
+          }
+          tmem_st16u(tP + lane_off + c / 2, pk);
+        }
+        {
+          const float2 a0 = f2_unpack(f2_add(ls2[0], ls2[1])), a1 = f2_unpack(f2_add(ls2[2], ls2[3]));
+          l += (a0.x + a0.y) + (a1.x + a1.y);
+        }
+        tmem_st_wait();
+        fence_before();
+        mbar_arrive(p_full);
+        if (tt && j < 4) tt[3 + 2 * j] = clock64();
+      }
+      // ---- epilogue: O / l -> bf16 staged in this tile's q buffer, coalesced row stores
+      if (nch > 0) {
+        mbar_wait(pv_done, (n - 1) & 1);
+        fence_after();
+      } else if (SUMI) {
+        tmem_st_wait();  // O = v_self
+      }
+      if (tt) tt[10] = clock64();
+      const bool have_o = SUMI || nch > 0;
+      const float inv = (valid && l > 0.f) ? 1.f / l : 0.f;
+#pragma unroll
+      for (int c = 0; c < DH; c += 32) {
+        float o[32];
+        if (have_o) {
+          tmem_ld32(tO + lane_off + c, o);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = 0.f;
+        }
+#pragma unroll
+        for (int cc = 0; cc < 32; cc += 8) {
+          uint32_t w[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            __nv_bfloat162 pp = __floats2bfloat162_rn(o[cc + 2 * i] * inv, o[cc + 2 * i + 1] * inv);
+            w[i] = *reinterpret_cast<uint32_t*>(&pp);
+          }
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(qbuf + row * Ly::RB +
+                                                                         (swz<DH>(row, (c + cc) / 8) << 4)),
+                       "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                       : "memory");
+        }
+      }
+      fence_before();  // the O reads are complete before the next tile's first P V may overwrite O
+      // the staging writes are ordered before the producer's next TMA write
+      // into this buffer; fenced before the global stores are issued (the
+      // fence would otherwise wait for them)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();  // each warp stores the 32 rows it staged
+      if (tt) tt[11] = clock64();
+      constexpr int LPR = DH / 8;
+      constexpr int RPI = 32 / LPR;
+#pragma unroll
+      for (int i = 0; i < 32; i += RPI) {
+        const int rr = ew * 32 + i + lane / LPR;
+        const int cj = lane % LPR;
+        if (rr < n_out) {
+          const int4 val = lds_v4(qbuf + rr * Ly::RB + (swz<DH>(rr, cj) << 4));
+          *reinterpret_cast<int4*>(a.O + (rbase + rr) * D.d + head * DH + cj * 8) = val;
+        }
+      }
+      // the buffer (and its descriptor) go back to the producer
+      mbar_arrive(&q_empty[b]);
+      if (tt) tt[12] = clock64();
+      kc += SELF + nch;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
+  }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -639,10 +1189,37 @@ static bool map2d(CUtensorMap* m, const void* base, long long rows, int cols, lo
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+static int sm_count() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+// CLIMBER_ATTN_PERSIST=0 selects the one-tile-per-CTA kernel for SUMI without the bias (A/B, tested)
+static bool use_persistent() {
+  static const bool on = [] { const char* e = getenv("CLIMBER_ATTN_PERSIST"); return !e || atoi(e) != 0; }();
+  return on;
+}
+
 template <int DH, int MODE>
 static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s) {
   constexpr int smem = Lay<DH>::TOTAL;
   static_assert(2 * (smem + 1024) <= 233472, "two CTAs per SM");
+  static_assert(2 * (PLay<DH>::TOTAL + 1024) <= 233472, "two persistent CTAs per SM");
+  // persistent for SUMI (uniform 4-chunk tiles at `large`: 400-437 vs 391-407
+  // TFLOP/s in A/B runs); causal history tiles (1-4 chunks, most of them short)
+  // measured faster one tile per CTA (250-262 vs 233-250)
+  if constexpr (MODE == MODE_SUMI) {
+    if (!a.D.bpos && use_persistent()) {
+      const int n_tiles = (int)(grid.x * grid.y * grid.z);
+      const int n_cta = min(n_tiles, 2 * sm_count());
+      if (n_cta <= 0) return;
+      constexpr int psmem = PLay<DH>::TOTAL;
+      ensure_smem_attr((const void*)k_attn_pers<DH, MODE>, psmem);
+      k_attn_pers<DH, MODE><<<n_cta, THREADS, psmem, s>>>(mq, mkv, a, (int)grid.x, n_tiles);
+      return;
+    }
+  }
   if (a.D.bpos) {
     ensure_smem_attr((const void*)k_attn_fa<DH, MODE, 1>, smem);
     k_attn_fa<DH, MODE, 1><<<grid, THREADS, smem, s>>>(mq, mkv, a);
@@ -652,6 +1229,8 @@ static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a,
   }
 }
 
+static bool g_trace_bias = false;  // the traced launch ran the relative-bias (one-tile) kernel
+static bool g_trace_sumi = false;  // ... a SUMI launch (persistent unless CLIMBER_ATTN_PERSIST=0)
 // CLIMBER_FA_TRACE=n: record the n-th launch of this process (clock64 per CTA)
 // and print the mean timeline relative to each CTA's start
 static unsigned long long* trace_begin(long long n_cta) {
@@ -663,9 +1242,36 @@ static unsigned long long* trace_begin(long long n_cta) {
   cudaMemset(buf, 0, n_cta * TRACE_N * 8);
   return buf;
 }
+static void ptrace_print(const unsigned long long* buf, long long n_cta) {
+  double acc[TRACE_N] = {0};
+  long long cnt[TRACE_N] = {0};
+  for (long long c = 0; c < n_cta; ++c) {
+    const unsigned long long* t = buf + c * TRACE_N;
+    if (!t[127]) continue;
+    for (int i = 0; i < 127; ++i)
+      if (t[i]) acc[i] += (double)(long long)(t[i] - t[127]), cnt[i]++;
+  }
+  auto m = [&](int i) { return cnt[i] ? acc[i] / cnt[i] : -1.0; };
+  fprintf(stderr, "[fa ptrace] persistent kernel (cycles since CTA start)\n");
+  for (int it = 0; it < 4; ++it) {
+    const int b = it * 24;
+    fprintf(stderr, "[fa ptrace] tile %d: q %7.0f self %7.0f | S0 %7.0f P0 %7.0f S1 %7.0f P1 %7.0f S2 %7.0f P2 %7.0f "
+                    "S3 %7.0f P3 %7.0f | pv_done %7.0f staged %7.0f released %7.0f | kself %7.0f dot %7.0f vself "
+                    "%7.0f\n",
+            it, m(b), m(b + 1), m(b + 2), m(b + 3), m(b + 4), m(b + 5), m(b + 6), m(b + 7), m(b + 8), m(b + 9),
+            m(b + 10), m(b + 11), m(b + 12), m(b + 13), m(b + 14), m(b + 15));
+  }
+  for (int i = 0; i < 16; ++i) fprintf(stderr, "[fa ptrace] QK %2d issued %7.0f%s", i, m(96 + i), i % 4 == 3 ? "\n" : " |");
+  for (int i = 0; i < 12; ++i) fprintf(stderr, "[fa ptrace] PV %2d issued %7.0f%s", i, m(112 + i), i % 4 == 3 ? "\n" : " |");
+}
 static void trace_end(unsigned long long* buf, long long n_cta, cudaStream_t s) {
   if (!buf) return;
   cudaStreamSynchronize(s);
+  if (use_persistent() && !g_trace_bias && g_trace_sumi) {
+    ptrace_print(buf, n_cta);
+    cudaFree(buf);
+    return;
+  }
   double acc[TRACE_N] = {0};
   long long cnt[TRACE_N] = {0};
   for (long long c = 0; c < n_cta; ++c) {
@@ -690,7 +1296,7 @@ static void trace_end(unsigned long long* buf, long long n_cta, cudaStream_t s) 
 // d_h 32 / 64 and whole pages (the history kernel covers n_k % 128 == 64 with a
 // half-empty last tile)
 bool attn_tc_supported(int dh, int nk, bool /*hist*/) {
-  return (dh == 32 || dh == 64) && nk % PAGE == 0 && fa::encoder() != nullptr;
+  return (dh == 32 || dh == 64) && nk % PAGE == 0 && nk <= 32 * PAGE && fa::encoder() != nullptr;
 }
 
 void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, const int* wave_slot,
@@ -707,6 +1313,8 @@ void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, 
   dim3 grid((Mmax + fa::ROWS - 1) / fa::ROWS, D.h, U * nbk);
   const long long n_cta = (long long)grid.x * grid.y * grid.z;
   a.trace = fa::trace_begin(n_cta);
+  fa::g_trace_bias = D.bpos != nullptr;
+  fa::g_trace_sumi = true;
   if (D.dh == 64) fa::launch<64, fa::MODE_SUMI>(mq, mkv, a, grid, s);
   else fa::launch<32, fa::MODE_SUMI>(mq, mkv, a, grid, s);
   fa::trace_end(a.trace, n_cta, s);
@@ -725,6 +1333,8 @@ void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r,
   dim3 grid((D.nk + fa::ROWS - 1) / fa::ROWS, D.h, U * nbk);
   const long long n_cta = (long long)grid.x * grid.y * grid.z;
   a.trace = fa::trace_begin(n_cta);
+  fa::g_trace_bias = D.bpos != nullptr;
+  fa::g_trace_sumi = false;
   if (D.dh == 64) fa::launch<64, fa::MODE_HIST>(mq, mkv, a, grid, s);
   else fa::launch<32, fa::MODE_HIST>(mq, mkv, a, grid, s);
   fa::trace_end(a.trace, n_cta, s);

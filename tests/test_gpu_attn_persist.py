@@ -1,0 +1,63 @@
+"""The persistent tcgen05 SUMI attention kernel (k_attn_pers, the default for
+the bf16 path without the relative bias) against the one-tile-per-CTA kernel
+(k_attn_fa, CLIMBER_ATTN_PERSIST=0).  Both kernels do the same arithmetic per
+query row in the same order, so the scores must agree bit for bit (the
+other parity tests bound the default path against the fp64 oracle).  Cases
+cover d_h 32 and 64, ragged candidate counts (tiles without candidates, partial
+tiles), blocks with v_k = 0 (self term only), M = 1, causal and bidirectional
+history.  P:L255 (SUMI masks), Eq. 3 (f_b = 0).
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+_CODE = r"""
+import sys, numpy as np
+sys.path[:0] = [{root!r}, {tests!r}]
+import synth
+from helpers import gpu_scores, make_gpu
+case = {case!r}
+if case == "small":
+    cfg = synth.preset("small"); B = 5
+    batch = synth.make_batch(cfg, 3, B=B)
+elif case in ("medium", "medium_bidir"):
+    cfg = synth.preset("medium", hist_causal=0 if case == "medium_bidir" else 1); B = 6
+    batch = synth.make_batch(cfg, 4, B=B, M=200)
+elif case == "medium_empty":
+    cfg = synth.preset("medium"); B = 1
+    batch = synth.make_user(cfg, np.random.default_rng(8), n_s=1500, M=1,
+                            action_probs=(0.93, 0.0, 0.0, 0.07, 0.0, 0.0))
+else:  # large: d_h 64, two candidate tiles + a partial one, ragged candidate counts
+    cfg = synth.preset("large", L=2); B = 3
+    batch = synth.make_batch(cfg, 5, B=B, M=300)
+w = synth.make_weights(cfg, 0)
+cl = make_gpu(cfg, w, B)
+got = gpu_scores(cl, batch)
+cl.stream_status()
+np.save({out!r}, got)
+"""
+
+
+def _run(case, persist, tmp_path):
+    out = str(tmp_path / f"{case}_{persist}.npy")
+    code = _CODE.format(root=ROOT, tests=os.path.join(ROOT, "tests"), case=case, out=out)
+    env = dict(os.environ, CLIMBER_ATTN_PERSIST=str(persist))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return np.load(out)
+
+
+@pytest.mark.parametrize("case", ["small", "medium", "medium_bidir", "medium_empty", "large"])
+def test_persistent_attention_bitwise_equal_one_tile_kernel(case, tmp_path):
+    a = _run(case, 1, tmp_path)
+    b = _run(case, 0, tmp_path)
+    assert np.all(np.isfinite(a))
+    assert a.shape == b.shape and np.array_equal(a.view(np.uint32), b.view(np.uint32)), \
+        (case, float(np.abs(a - b).max()))
