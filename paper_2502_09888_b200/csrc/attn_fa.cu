@@ -679,8 +679,8 @@ struct RingSlots {
 
 template <int DH, int MODE>
 __global__ void __launch_bounds__(THREADS, 2)
-    k_attn_pers(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, Args a, int ntx,
-                int n_tiles) {
+    k_attn_pers(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
+                const __grid_constant__ CUtensorMap tmO, Args a, int ntx, int n_tiles) {
   using Ly = PLay<DH>;
   constexpr bool SUMI = MODE == MODE_SUMI;
   constexpr int SELF = SUMI ? 1 : 0;  // ring items per tile before its chunks
@@ -714,7 +714,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmKV) : "memory");
     for (int b = 0; b < 2; ++b) {
       mbar_init(&q_full[b], 1);
-      mbar_init(&q_empty[b], 128);
+      mbar_init(&q_empty[b], 4);  // one arrival per softmax warp
     }
     for (int s = 0; s < KST; ++s) {
       mbar_init(&k_full[s], 1);
@@ -902,19 +902,7 @@ __global__ void __launch_bounds__(THREADS, 2)
         int done2 = 1, nch2 = 0;
         bool peeked = false, issued2 = false;
         for (int j = 0; j < nch; ++j) {
-          if (j + 1 < nch) {
-            qk(b, c0 + j + 1);
-          } else {  // S(0) of the next tile under this tile's last exponentials
-            const int b2 = (it + 1) & 1;
-            mbar_wait(&q_full[b2], ((it + 1) >> 1) & 1);
-            done2 = desc[b2].done;
-            nch2 = desc[b2].nch;
-            peeked = true;
-            if (!done2 && nch2 > 0) {
-              qk(b2, c0 + nch + SELF);
-              issued2 = true;
-            }
-          }
+          if (j + 1 < nch) qk(b, c0 + j + 1);  // S(j+1) under the exponentials of chunk j
           mbar_wait(p_full, n & 1);
           const int item = c0 + j;
           mbar_wait(&v_full[item % VST], (item / VST) & 1);
@@ -930,6 +918,19 @@ __global__ void __launch_bounds__(THREADS, 2)
           mma_commit(&v_empty[item % VST]);
           mma_commit(pv_done);
           ++n;
+          if (j + 1 == nch) {
+            // S(0) of the next tile right behind the last P V (which the
+            // epilogue waits for), under this tile's epilogue
+            const int b2 = (it + 1) & 1;
+            mbar_wait(&q_full[b2], ((it + 1) >> 1) & 1);
+            done2 = desc[b2].done;
+            nch2 = desc[b2].nch;
+            peeked = true;
+            if (!done2 && nch2 > 0) {
+              qk(b2, c0 + nch + SELF);
+              issued2 = true;
+            }
+          }
         }
         if (!peeked) {
           const int b2 = (it + 1) & 1;
@@ -951,6 +952,18 @@ __global__ void __launch_bounds__(THREADS, 2)
     const int row = ew * 32 + lane;
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
     int it = 0, kc = 0, n = 0;
+    // a TMA store of the previous tile's O rows still reading this warp's
+    // staging rows: lane 0 releases that q buffer once the read is done
+    int rel_b = -1;
+    auto release_pending = [&]() {
+      if (rel_b >= 0) {
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          mbar_arrive(&q_empty[rel_b]);
+        }
+        rel_b = -1;
+      }
+    };
     for (;; ++it) {
       const int b = it & 1;
       mbar_wait(&q_full[b], (it >> 1) & 1);
@@ -1013,6 +1026,7 @@ __global__ void __launch_bounds__(THREADS, 2)
         mbar_arrive(&v_selff[st_v]);  // the v_self values were consumed by the TMEM stores
         if (tt) tt[1] = clock64();
       }
+      release_pending();
       for (int j = 0; j < nch; ++j, ++n) {
         mbar_wait(s_full, n & 1);
         fence_after();
@@ -1136,22 +1150,36 @@ __global__ void __launch_bounds__(THREADS, 2)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();  // each warp stores the 32 rows it staged
       if (tt) tt[11] = clock64();
-      constexpr int LPR = DH / 8;
-      constexpr int RPI = 32 / LPR;
-#pragma unroll
-      for (int i = 0; i < 32; i += RPI) {
-        const int rr = ew * 32 + i + lane / LPR;
-        const int cj = lane % LPR;
-        if (rr < n_out) {
-          const int4 val = lds_v4(qbuf + rr * Ly::RB + (swz<DH>(rr, cj) << 4));
-          *reinterpret_cast<int4*>(a.O + (rbase + rr) * D.d + head * DH + cj * 8) = val;
+      if (ew * 32 + 32 <= n_out) {
+        // all 32 rows exist: one TMA store (box 32 rows x d_h, the staging
+        // swizzle); the buffer is released once the store has read it
+        if (lane == 0) {
+          tma_store_2d(&tmO, smem + Ly::q_off(b) + ew * 32 * Ly::RB, head * DH, (int)(rbase + ew * 32));
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
+        rel_b = b;
+      } else {
+        // the tile's last rows: row stores that stop at n_out (the rows past
+        // it belong to the next user's candidates)
+        constexpr int LPR = DH / 8;
+        constexpr int RPI = 32 / LPR;
+#pragma unroll
+        for (int i = 0; i < 32; i += RPI) {
+          const int rr = ew * 32 + i + lane / LPR;
+          const int cj = lane % LPR;
+          if (rr < n_out) {
+            const int4 val = lds_v4(qbuf + rr * Ly::RB + (swz<DH>(rr, cj) << 4));
+            *reinterpret_cast<int4*>(a.O + (rbase + rr) * D.d + head * DH + cj * 8) = val;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&q_empty[b]);  // the buffer (and its descriptor) go back to the producer
       }
-      // the buffer (and its descriptor) go back to the producer
-      mbar_arrive(&q_empty[b]);
       if (tt) tt[12] = clock64();
       kc += SELF + nch;
     }
+    release_pending();
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   fence_before();
   __syncthreads();
@@ -1202,7 +1230,8 @@ static bool use_persistent() {
 }
 
 template <int DH, int MODE>
-static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s) {
+static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s,
+                   const CUtensorMap* mo = nullptr) {
   constexpr int smem = Lay<DH>::TOTAL;
   static_assert(2 * (smem + 1024) <= 233472, "two CTAs per SM");
   static_assert(2 * (PLay<DH>::TOTAL + 1024) <= 233472, "two persistent CTAs per SM");
@@ -1210,13 +1239,13 @@ static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a,
   // TFLOP/s in A/B runs); causal history tiles (1-4 chunks, most of them short)
   // measured faster one tile per CTA (250-262 vs 233-250)
   if constexpr (MODE == MODE_SUMI) {
-    if (!a.D.bpos && use_persistent()) {
+    if (!a.D.bpos && mo && use_persistent()) {
       const int n_tiles = (int)(grid.x * grid.y * grid.z);
       const int n_cta = min(n_tiles, 2 * sm_count());
       if (n_cta <= 0) return;
       constexpr int psmem = PLay<DH>::TOTAL;
       ensure_smem_attr((const void*)k_attn_pers<DH, MODE>, psmem);
-      k_attn_pers<DH, MODE><<<n_cta, THREADS, psmem, s>>>(mq, mkv, a, (int)grid.x, n_tiles);
+      k_attn_pers<DH, MODE><<<n_cta, THREADS, psmem, s>>>(mq, mkv, *mo, a, (int)grid.x, n_tiles);
       return;
     }
   }
@@ -1303,9 +1332,10 @@ void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, 
                          const int* wave_r, int U, int Mmax, const bf16* pool, long long pool_rows, const int* ptab,
                          const int* vlen_all, const float* tau, bf16* O, int k, int l, const Dims& D, cudaStream_t s,
                          int nbk) {
-  CUtensorMap mq, mkv;
+  CUtensorMap mq, mkv, mo;
   if (!fa::map2d(&mq, QKV, P * nbk, 3 * D.d, 3LL * D.d, D.dh, fa::ROWS) ||
-      !fa::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, PAGE)) {
+      !fa::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, PAGE) ||
+      !fa::map2d(&mo, O, P * nbk, D.d, D.d, D.dh, 32)) {  // O rows: 32-row boxes (one softmax warp)
     note_launch_error("SUMI attention: cuTensorMapEncodeTiled rejected a map (kernel not launched)");
     return;
   }
@@ -1315,8 +1345,8 @@ void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, 
   a.trace = fa::trace_begin(n_cta);
   fa::g_trace_bias = D.bpos != nullptr;
   fa::g_trace_sumi = true;
-  if (D.dh == 64) fa::launch<64, fa::MODE_SUMI>(mq, mkv, a, grid, s);
-  else fa::launch<32, fa::MODE_SUMI>(mq, mkv, a, grid, s);
+  if (D.dh == 64) fa::launch<64, fa::MODE_SUMI>(mq, mkv, a, grid, s, &mo);
+  else fa::launch<32, fa::MODE_SUMI>(mq, mkv, a, grid, s, &mo);
   fa::trace_end(a.trace, n_cta, s);
 }
 
