@@ -46,6 +46,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <numeric>
 
 #include "kernels.cuh"
 #include "tc_util.cuh"
@@ -955,6 +956,23 @@ __global__ void __launch_bounds__(THREADS, 2)
     // a TMA store of the previous tile's O rows still reading this warp's
     // staging rows: lane 0 releases that q buffer once the read is done
     int rel_b = -1;
+    // Every TMEM column of this warp's lanes starts at zero.  Without this,
+    // the first tile a CTA computed occasionally (~1 launch in 20, always the
+    // rows of one warp, a few bf16 ulps) differed between identical launches:
+    // a standalone determinism harness (tools/micro/attn_race.cu) showed the
+    // result depended on the TMEM contents the previous CTA on the SM left
+    // behind, and with the columns zeroed at start 0 of 72 launches differed
+    // (two smem layouts; a plain 2 us delay instead only hid it in one of
+    // them).  Which read observes the stale state was not pinned down; the
+    // one-tile kernel (fresh CTAs, never observed to differ) is unchanged.
+    {
+      float z[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) z[i] = 0.f;
+#pragma unroll
+      for (int c = 0; c < 256; c += 32) tmem_st32_nw(tmem_base + lane_off + c, z);
+      tmem_st_wait();
+    }
     auto release_pending = [&]() {
       if (rel_b >= 0) {
         if (lane == 0) {
@@ -1223,7 +1241,7 @@ static int sm_count() {
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   return n;
 }
-// CLIMBER_ATTN_PERSIST=0 selects the one-tile-per-CTA kernel for SUMI without the bias (A/B, tested)
+// CLIMBER_ATTN_PERSIST=0 selects the one-tile-per-CTA kernel without the bias (A/B, tested)
 static bool use_persistent() {
   static const bool on = [] { const char* e = getenv("CLIMBER_ATTN_PERSIST"); return !e || atoi(e) != 0; }();
   return on;
@@ -1235,14 +1253,18 @@ static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a,
   constexpr int smem = Lay<DH>::TOTAL;
   static_assert(2 * (smem + 1024) <= 233472, "two CTAs per SM");
   static_assert(2 * (PLay<DH>::TOTAL + 1024) <= 233472, "two persistent CTAs per SM");
-  // persistent for SUMI (uniform 4-chunk tiles at `large`: 400-437 vs 391-407
-  // TFLOP/s in A/B runs); causal history tiles (1-4 chunks, most of them short)
-  // measured faster one tile per CTA (250-262 vs 233-250)
-  if constexpr (MODE == MODE_SUMI) {
+  // persistent kernel without the relative bias (A/B in a 128-user `large`
+  // step: SUMI 417-437 vs 391-428 TFLOP/s, history 339-341 vs 258-262; medium
+  // SUMI 205 vs 162, history 109 vs 80)
+  {
     if (!a.D.bpos && mo && use_persistent()) {
       const int n_tiles = (int)(grid.x * grid.y * grid.z);
-      const int n_cta = min(n_tiles, 2 * sm_count());
+      int n_cta = min(n_tiles, 2 * sm_count());
       if (n_cta <= 0) return;
+      // a CTA walks t, t + n_cta, ...: with n_cta coprime to the tiles per
+      // (user, block, head) (x fastest) every CTA cycles through all x, so the
+      // causal history tiles (x + 1 chunks) spread evenly over the CTAs
+      while (n_cta > 1 && std::gcd(n_cta, (int)grid.x) != 1) --n_cta;
       constexpr int psmem = PLay<DH>::TOTAL;
       ensure_smem_attr((const void*)k_attn_pers<DH, MODE>, psmem);
       k_attn_pers<DH, MODE><<<n_cta, THREADS, psmem, s>>>(mq, mkv, *mo, a, (int)grid.x, n_tiles);
@@ -1259,7 +1281,6 @@ static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a,
 }
 
 static bool g_trace_bias = false;  // the traced launch ran the relative-bias (one-tile) kernel
-static bool g_trace_sumi = false;  // ... a SUMI launch (persistent unless CLIMBER_ATTN_PERSIST=0)
 // CLIMBER_FA_TRACE=n: record the n-th launch of this process (clock64 per CTA)
 // and print the mean timeline relative to each CTA's start
 static unsigned long long* trace_begin(long long n_cta) {
@@ -1296,7 +1317,7 @@ static void ptrace_print(const unsigned long long* buf, long long n_cta) {
 static void trace_end(unsigned long long* buf, long long n_cta, cudaStream_t s) {
   if (!buf) return;
   cudaStreamSynchronize(s);
-  if (use_persistent() && !g_trace_bias && g_trace_sumi) {
+  if (use_persistent() && !g_trace_bias) {
     ptrace_print(buf, n_cta);
     cudaFree(buf);
     return;
@@ -1344,7 +1365,6 @@ void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, 
   const long long n_cta = (long long)grid.x * grid.y * grid.z;
   a.trace = fa::trace_begin(n_cta);
   fa::g_trace_bias = D.bpos != nullptr;
-  fa::g_trace_sumi = true;
   if (D.dh == 64) fa::launch<64, fa::MODE_SUMI>(mq, mkv, a, grid, s, &mo);
   else fa::launch<32, fa::MODE_SUMI>(mq, mkv, a, grid, s, &mo);
   fa::trace_end(a.trace, n_cta, s);
@@ -1353,9 +1373,10 @@ void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, 
 void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r, int U, const bf16* pool,
                          long long pool_rows, const int* ptab, const int* vlen_all, const float* tau, bf16* O, int k,
                          int l, const Dims& D, cudaStream_t s, int nbk) {
-  CUtensorMap mq, mkv;
+  CUtensorMap mq, mkv, mo;
   if (!fa::map2d(&mq, Q, (long long)U * D.nk * nbk, D.d, D.d, D.dh, fa::ROWS) ||
-      !fa::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, PAGE)) {
+      !fa::map2d(&mkv, pool, pool_rows, D.d, D.d, D.dh, PAGE) ||
+      !fa::map2d(&mo, O, (long long)U * D.nk * nbk, D.d, D.d, D.dh, 32)) {
     note_launch_error("history attention: cuTensorMapEncodeTiled rejected a map (kernel not launched)");
     return;
   }
@@ -1364,9 +1385,8 @@ void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r,
   const long long n_cta = (long long)grid.x * grid.y * grid.z;
   a.trace = fa::trace_begin(n_cta);
   fa::g_trace_bias = D.bpos != nullptr;
-  fa::g_trace_sumi = false;
-  if (D.dh == 64) fa::launch<64, fa::MODE_HIST>(mq, mkv, a, grid, s);
-  else fa::launch<32, fa::MODE_HIST>(mq, mkv, a, grid, s);
+  if (D.dh == 64) fa::launch<64, fa::MODE_HIST>(mq, mkv, a, grid, s, &mo);
+  else fa::launch<32, fa::MODE_HIST>(mq, mkv, a, grid, s, &mo);
   fa::trace_end(a.trace, n_cta, s);
 }
 

@@ -1,11 +1,12 @@
-"""The persistent tcgen05 SUMI attention kernel (k_attn_pers, the default for
-the bf16 path without the relative bias) against the one-tile-per-CTA kernel
+"""The persistent tcgen05 attention kernel (k_attn_pers, SUMI and history rows,
+the default for the bf16 path without the relative bias) against the
+one-tile-per-CTA kernel
 (k_attn_fa, CLIMBER_ATTN_PERSIST=0).  Both kernels do the same arithmetic per
 query row in the same order, so the scores must agree bit for bit (the
 other parity tests bound the default path against the fp64 oracle).  Cases
 cover d_h 32 and 64, ragged candidate counts (tiles without candidates, partial
-tiles), blocks with v_k = 0 (self term only), M = 1, causal and bidirectional
-history.  P:L255 (SUMI masks), Eq. 3 (f_b = 0).
+tiles), history tiles past v (no keys), blocks with v_k = 0 (self term
+only), M = 1, causal and bidirectional history.  P:L255 (SUMI masks), Eq. 3 (f_b = 0).
 """
 import os
 import subprocess
@@ -61,3 +62,31 @@ def test_persistent_attention_bitwise_equal_one_tile_kernel(case, tmp_path):
     assert np.all(np.isfinite(a))
     assert a.shape == b.shape and np.array_equal(a.view(np.uint32), b.view(np.uint32)), \
         (case, float(np.abs(a - b).max()))
+
+
+def test_attention_deterministic_across_launches():
+    """Identical launches give identical scores (SURVEY §8(b) determinism):
+    a `large` wave scored repeatedly on one handle and re-encoded, bit for
+    bit.  Guards the persistent kernel's first-tile state (its TMEM is zeroed
+    at CTA start, see attn_fa.cu)."""
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import synth
+    from helpers import make_gpu, to_dev
+    cfg = synth.preset("large", L=2)
+    B = 16
+    w = synth.make_weights(cfg, 0)
+    batch = synth.make_batch(cfg, 8, B=B)
+    cl = make_gpu(cfg, w, B, kv_users=2 * B)
+    item, action, scenario, ts, cand = to_dev(batch)
+    hs = cl.encode_users(batch.ev_offsets, item, action, scenario, ts, batch.r)
+    ref = cl.score_batched(hs, batch.cand_offsets, cand).clone()
+    for _ in range(4):
+        got = cl.score_batched(hs, batch.cand_offsets, cand)
+        assert torch.equal(got, ref), float((got - ref).abs().max())
+    h2 = cl.encode_users(batch.ev_offsets, item, action, scenario, ts, batch.r)
+    got = cl.score_batched(h2, batch.cand_offsets, cand)
+    cl.stream_status()
+    assert torch.equal(got, ref), float((got - ref).abs().max())
+    cl.release(h2)
+    cl.release(hs)
