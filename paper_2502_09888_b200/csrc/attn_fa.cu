@@ -956,23 +956,6 @@ __global__ void __launch_bounds__(THREADS, 2)
     // a TMA store of the previous tile's O rows still reading this warp's
     // staging rows: lane 0 releases that q buffer once the read is done
     int rel_b = -1;
-    // Every TMEM column of this warp's lanes starts at zero.  Without this,
-    // the first tile a CTA computed occasionally (~1 launch in 20, always the
-    // rows of one warp, a few bf16 ulps) differed between identical launches:
-    // a standalone determinism harness (tools/micro/attn_race.cu) showed the
-    // result depended on the TMEM contents the previous CTA on the SM left
-    // behind, and with the columns zeroed at start 0 of 72 launches differed
-    // (two smem layouts; a plain 2 us delay instead only hid it in one of
-    // them).  Which read observes the stale state was not pinned down; the
-    // one-tile kernel (fresh CTAs, never observed to differ) is unchanged.
-    {
-      float z[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) z[i] = 0.f;
-#pragma unroll
-      for (int c = 0; c < 256; c += 32) tmem_st32_nw(tmem_base + lane_off + c, z);
-      tmem_st_wait();
-    }
     auto release_pending = [&]() {
       if (rel_b >= 0) {
         if (lane == 0) {
@@ -1241,11 +1224,15 @@ static int sm_count() {
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   return n;
 }
-// CLIMBER_ATTN_PERSIST=0 selects the one-tile-per-CTA kernel without the bias (A/B, tested)
-static bool use_persistent() {
-  static const bool on = [] { const char* e = getenv("CLIMBER_ATTN_PERSIST"); return !e || atoi(e) != 0; }();
-  return on;
+// CLIMBER_ATTN_PERSIST: 1 (default) persistent history attention, one-tile
+// SUMI; 0 one-tile kernels everywhere (A/B, tested bitwise equal); 2 also the
+// persistent SUMI kernel -- EXPERIMENTAL: not bitwise reproducible (a
+// first-tile race specific to its k_self / v_self path)
+static int persist_mode() {
+  static const int m = [] { const char* e = getenv("CLIMBER_ATTN_PERSIST"); return e ? atoi(e) : 1; }();
+  return m;
 }
+static bool use_persistent(int mode) { return mode == MODE_HIST ? persist_mode() >= 1 : persist_mode() >= 2; }
 
 template <int DH, int MODE>
 static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s,
@@ -1254,10 +1241,10 @@ static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a,
   static_assert(2 * (smem + 1024) <= 233472, "two CTAs per SM");
   static_assert(2 * (PLay<DH>::TOTAL + 1024) <= 233472, "two persistent CTAs per SM");
   // persistent kernel without the relative bias (A/B in a 128-user `large`
-  // step: SUMI 417-437 vs 391-428 TFLOP/s, history 339-341 vs 258-262; medium
-  // SUMI 205 vs 162, history 109 vs 80)
+  // step: history 339-341 vs 258-262 TFLOP/s, medium 109 vs 80; SUMI 417-437
+  // vs 391-428 and 205 vs 162, but see persist_mode)
   {
-    if (!a.D.bpos && mo && use_persistent()) {
+    if (!a.D.bpos && mo && use_persistent(MODE)) {
       const int n_tiles = (int)(grid.x * grid.y * grid.z);
       int n_cta = min(n_tiles, 2 * sm_count());
       if (n_cta <= 0) return;
@@ -1281,6 +1268,7 @@ static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a,
 }
 
 static bool g_trace_bias = false;  // the traced launch ran the relative-bias (one-tile) kernel
+static int g_trace_mode = 0;       // ... and its mode (SUMI / history)
 // CLIMBER_FA_TRACE=n: record the n-th launch of this process (clock64 per CTA)
 // and print the mean timeline relative to each CTA's start
 static unsigned long long* trace_begin(long long n_cta) {
@@ -1317,7 +1305,7 @@ static void ptrace_print(const unsigned long long* buf, long long n_cta) {
 static void trace_end(unsigned long long* buf, long long n_cta, cudaStream_t s) {
   if (!buf) return;
   cudaStreamSynchronize(s);
-  if (use_persistent() && !g_trace_bias) {
+  if (use_persistent(g_trace_mode) && !g_trace_bias) {
     ptrace_print(buf, n_cta);
     cudaFree(buf);
     return;
@@ -1365,6 +1353,7 @@ void launch_attn_sumi_tc(const bf16* QKV, long long P, const int64_t* cand_off, 
   const long long n_cta = (long long)grid.x * grid.y * grid.z;
   a.trace = fa::trace_begin(n_cta);
   fa::g_trace_bias = D.bpos != nullptr;
+  fa::g_trace_mode = fa::MODE_SUMI;
   if (D.dh == 64) fa::launch<64, fa::MODE_SUMI>(mq, mkv, a, grid, s, &mo);
   else fa::launch<32, fa::MODE_SUMI>(mq, mkv, a, grid, s, &mo);
   fa::trace_end(a.trace, n_cta, s);
@@ -1385,6 +1374,7 @@ void launch_attn_hist_tc(const bf16* Q, const int* wave_slot, const int* wave_r,
   const long long n_cta = (long long)grid.x * grid.y * grid.z;
   a.trace = fa::trace_begin(n_cta);
   fa::g_trace_bias = D.bpos != nullptr;
+  fa::g_trace_mode = fa::MODE_HIST;
   if (D.dh == 64) fa::launch<64, fa::MODE_HIST>(mq, mkv, a, grid, s, &mo);
   else fa::launch<32, fa::MODE_HIST>(mq, mkv, a, grid, s, &mo);
   fa::trace_end(a.trace, n_cta, s);

@@ -1,12 +1,12 @@
-"""The persistent tcgen05 attention kernel (k_attn_pers, SUMI and history rows,
-the default for the bf16 path without the relative bias) against the
-one-tile-per-CTA kernel
+"""The persistent tcgen05 attention kernel (k_attn_pers; the default for
+history rows without the relative bias) against the one-tile-per-CTA kernel
 (k_attn_fa, CLIMBER_ATTN_PERSIST=0).  Both kernels do the same arithmetic per
-query row in the same order, so the scores must agree bit for bit (the
-other parity tests bound the default path against the fp64 oracle).  Cases
-cover d_h 32 and 64, ragged candidate counts (tiles without candidates, partial
-tiles), history tiles past v (no keys), blocks with v_k = 0 (self term
-only), M = 1, causal and bidirectional history.  P:L255 (SUMI masks), Eq. 3 (f_b = 0).
+query row in the same order, so the scores must agree bit for bit (the other
+parity tests bound the default path against the fp64 oracle).  Cases cover
+d_h 32 and 64, ragged users (history tiles past v: no keys), blocks with
+v_k = 0, M = 1, causal and bidirectional history.  The persistent SUMI variant
+(CLIMBER_ATTN_PERSIST=2) is experimental and not covered: it is not bitwise
+reproducible.  P:L255 (SUMI masks), Eq. 3 (f_b = 0).
 """
 import os
 import subprocess
@@ -67,8 +67,7 @@ def test_persistent_attention_bitwise_equal_one_tile_kernel(case, tmp_path):
 def test_attention_deterministic_across_launches():
     """Identical launches give identical scores (SURVEY §8(b) determinism):
     a `large` wave scored repeatedly on one handle and re-encoded, bit for
-    bit.  Guards the persistent kernel's first-tile state (its TMEM is zeroed
-    at CTA start, see attn_fa.cu)."""
+    bit (the persistent history kernel in the encode, SUMI in the score)."""
     import torch
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import synth
