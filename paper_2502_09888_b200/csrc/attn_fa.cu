@@ -647,10 +647,17 @@ struct PLay {
   static constexpr int RB = DH * 2;
   static constexpr uint32_t SWZ = (DH == 64) ? 2u : 4u;
   static constexpr int TILE_B = ROWS * RB;
+#ifdef FA_LAYOUT_KFIRST  // determinism stress layout (tools/micro/race_variants.sh)
+  static constexpr int K_OFF = 0;
+  static constexpr int V_OFF = K_OFF + KST * TILE_B;
+  static constexpr int Q_OFF = V_OFF + VST * TILE_B;
+  static constexpr int BAR_OFF = Q_OFF + 2 * TILE_B;
+#else
   static constexpr int Q_OFF = 0;                          // [2] q tiles, then O staging
   static constexpr int K_OFF = Q_OFF + 2 * TILE_B;         // [KST] K ring (SUMI: k_self tiles too)
   static constexpr int V_OFF = K_OFF + KST * TILE_B;       // [VST] V ring (SUMI: v_self tiles too)
   static constexpr int BAR_OFF = V_OFF + VST * TILE_B;     // barriers (<= 256 B)
+#endif
   static constexpr int DESC_OFF = BAR_OFF + 256;           // [2] tile descriptors
   static constexpr int TOTAL = DESC_OFF + 768;
   __device__ static constexpr int q_off(int b) { return Q_OFF + b * TILE_B; }
