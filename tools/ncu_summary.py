@@ -16,6 +16,9 @@ def launches(path):
             name = "k_attn<" + r[ki].split("k_attn<")[1].split(">")[0] + ">"
         if "k_attn_fusion_pair" in r[ki]:
             name = "k_attn_fusion_pair"
+        elif "k_attn_pers<" in r[ki]:
+            args = r[ki].split("k_attn_pers<")[1].split(">")[0].replace("(int)", "").split(",")
+            name = "k_attn_pers<d_h=%s, %s>" % (args[0].strip(), "SUMI" if args[1].strip() == "0" else "HIST")
         elif "k_attn_fa<" in r[ki]:
             args = r[ki].split("k_attn_fa<")[1].split(">")[0].replace("(int)", "").split(",")
             name = "k_attn_fa<d_h=%s, %s>" % (args[0].strip(), "SUMI" if args[1].strip() == "0" else "HIST")
