@@ -15,7 +15,8 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libclimber.so")
+# CLIMBER_LIB: another build of the library (A/B measurements); default in-tree
+LIB_PATH = os.environ.get("CLIMBER_LIB") or os.path.join(_HERE, "lib", "libclimber.so")
 
 ABI_VERSION = 2
 BF16, FP32 = 0, 1
