@@ -617,14 +617,15 @@ __global__ void __launch_bounds__(THREADS, 2)
 // walks the tiles t = blockIdx.x, blockIdx.x + gridDim.x, ... in the same
 // (x, head, user x block) order as the one-tile kernel above.  Per CTA the
 // chunk pipeline never drains between tiles:
-//   * q tiles are double-buffered; the producer loads tile i+1's q (and, for
-//     SUMI, its k_self / v_self as items of the K / V rings) while tile i runs;
-//   * the MMA issuer issues S(0) of tile i+1 = Q_{i+1} K_0^T as soon as the
-//     softmax has read S(last) of tile i, so it runs under tile i's last
-//     exponentials;
+//   * q tiles are double-buffered; the producer loads tile i+1's q while
+//     tile i runs;
+//   * the MMA issuer issues S(0) of tile i+1 = Q_{i+1} K_0^T right behind
+//     tile i's last P V, so it runs under tile i's epilogue;
 //   * the softmax warpgroup goes from P(last) of tile i through its epilogue
-//     (O / l staged in tile i's q buffer, coalesced row stores) and tile
-//     i+1's self term straight into S(0) of tile i+1.
+//     (SUMI: the self term merged into the row state, k_self / v_self rows
+//     loaded from global memory under the last P V; O / l staged in tile i's
+//     q buffer, TMA stores of full 32-row boxes) straight into S(0) of tile
+//     i+1.
 // The producer (warp 0) computes each tile's geometry once and hands it to
 // the other roles in a descriptor next to the q buffer it fills (published by
 // the q_full barrier; the softmax's q_empty arrival after the epilogue frees
@@ -654,8 +655,8 @@ struct PLay {
   static constexpr int BAR_OFF = Q_OFF + 2 * TILE_B;
 #else
   static constexpr int Q_OFF = 0;                          // [2] q tiles, then O staging
-  static constexpr int K_OFF = Q_OFF + 2 * TILE_B;         // [KST] K ring (SUMI: k_self tiles too)
-  static constexpr int V_OFF = K_OFF + KST * TILE_B;       // [VST] V ring (SUMI: v_self tiles too)
+  static constexpr int K_OFF = Q_OFF + 2 * TILE_B;         // [KST] K ring
+  static constexpr int V_OFF = K_OFF + KST * TILE_B;       // [VST] V ring
   static constexpr int BAR_OFF = V_OFF + VST * TILE_B;     // barriers (<= 256 B)
 #endif
   static constexpr int DESC_OFF = BAR_OFF + 256;           // [2] tile descriptors
@@ -665,33 +666,18 @@ struct PLay {
   __device__ static constexpr int v_off(int i) { return V_OFF + (i % VST) * TILE_B; }
 };
 
-// Producer-side state of one ring: a slot is freed by the MMA (chunk tiles,
-// tcgen05.commit on `empty`) or by the softmax warpgroup (self tiles, 128
-// arrivals on `selff`), so each slot counts its uses of each barrier.
-// Per slot 4 bits in one register: last occupant (bits 0-1: 0 none, 1
-// chunk, 2 self) and the parity of the chunk / self uses so far (bits 2, 3).
-template <int NST>
-struct RingSlots {
-  uint32_t bits = 0;
-  __device__ void init() { bits = 0; }
-  // wait until slot st is free for an item of kind `kind` (1 chunk, 2 self), then record it
-  __device__ void acquire(int st, int kind, uint64_t* empty, uint64_t* selff) {
-    const uint32_t f = (bits >> (4 * st)) & 15u;
-    const uint32_t last = f & 3u, pc = (f >> 2) & 1u, ps = (f >> 3) & 1u;
-    if (last == 1u) mbar_wait(&empty[st], pc ^ 1u);        // the previous chunk use completed
-    else if (last == 2u) mbar_wait(&selff[st], ps ^ 1u);  // the previous self use completed
-    const uint32_t nf = (uint32_t)kind | ((kind == 1 ? pc ^ 1u : pc) << 2) | ((kind == 2 ? ps ^ 1u : ps) << 3);
-    bits = (bits & ~(15u << (4 * st))) | (nf << (4 * st));
-  }
-};
-
 template <int DH, int MODE>
 __global__ void __launch_bounds__(THREADS, 2)
     k_attn_pers(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
                 const __grid_constant__ CUtensorMap tmO, Args a, int ntx, int n_tiles) {
   using Ly = PLay<DH>;
   constexpr bool SUMI = MODE == MODE_SUMI;
-  constexpr int SELF = SUMI ? 1 : 0;  // ring items per tile before its chunks
+  // SUMI k_self / v_self are not ring items: each row's self term is merged
+  // into its online-softmax state in the epilogue (k_self / v_self rows read
+  // from global memory under the last P V), so both modes run the same chunk
+  // pipeline.  (A first version carried them through the K / V rings as
+  // items released by the softmax warps; it was not bitwise reproducible,
+  // DESIGN.md §6.)
   extern __shared__ __align__(1024) uint8_t smem[];
   {
     uint32_t dyn;
@@ -703,16 +689,14 @@ __global__ void __launch_bounds__(THREADS, 2)
   uint64_t* q_empty = q_full + 2;             // [2]
   uint64_t* k_full = q_empty + 2;             // [KST]
   uint64_t* k_empty = k_full + KST;           // [KST]
-  uint64_t* k_selff = k_empty + KST;         // [KST] a k_self tile in the slot was read (128 arrivals)
-  uint64_t* v_full = k_selff + KST;           // [VST]
+  uint64_t* v_full = k_empty + KST;           // [VST]
   uint64_t* v_empty = v_full + VST;           // [VST]
-  uint64_t* v_selff = v_empty + VST;          // [VST]
-  uint64_t* s_full = v_selff + VST;
+  uint64_t* s_full = v_empty + VST;
   uint64_t* s_read = s_full + 1;
   uint64_t* p_full = s_read + 1;
   uint64_t* pv_done = p_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
-  static_assert((2 + 2 + 3 * KST + 3 * VST + 4) * 8 + 4 <= 256, "barrier area");
+  static_assert((2 + 2 + 2 * KST + 2 * VST + 4) * 8 + 4 <= 256, "barrier area");
   PDesc* desc = reinterpret_cast<PDesc*>(smem + Ly::DESC_OFF);
 
   const Dims& D = a.D;
@@ -727,12 +711,10 @@ __global__ void __launch_bounds__(THREADS, 2)
     for (int s = 0; s < KST; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
-      mbar_init(&k_selff[s], 128);
     }
     for (int s = 0; s < VST; ++s) {
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
-      mbar_init(&v_selff[s], 128);
     }
     mbar_init(s_full, 1);
     mbar_init(s_read, 128);
@@ -758,10 +740,8 @@ __global__ void __launch_bounds__(THREADS, 2)
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
     if (warp == 0) {
-      // ---------------- q + K producer: tile geometry, q, (k_self), K chunks ----------------
+      // ---------------- q + K producer: tile geometry, q, K chunks ----------------
       int it = 0, kc = 0;
-      RingSlots<KST> ring;
-      ring.init();
       for (int t = blockIdx.x;; t += gridDim.x) {
         const bool done = t >= n_tiles;
         int head = 0, nch = 0, n_rows = 0, n_out = 0, kend = 0, tile0 = 0, n_pages = 0, pg = 0;
@@ -821,21 +801,12 @@ __global__ void __launch_bounds__(THREADS, 2)
         }
         __syncwarp();
         if (done) break;
-        if (SUMI) {  // k_self through the K ring (read by the softmax's self term)
-          const int st = kc % KST;
-          ring.acquire(st, 2, k_empty, k_selff);
-          if (lane == 0) {
-            mbar_expect_tx(&k_full[st], Ly::TILE_B);
-            tma_load_2d(smem + Ly::k_off(kc), &tmQ, &k_full[st], D.d + head * DH, (int)rbase);
-          }
-          ++kc;
-        }
         for (int j = 0; j < nch; ++j, ++kc) {
           const int st = kc % KST;
           const int pa = __shfl_sync(0xffffffffu, pg, (2 * j) & 31);
           const int pb0 = __shfl_sync(0xffffffffu, pg, (2 * j + 1) & 31);
           const int pb = (2 * j + 1 < n_pages) ? pb0 : pa;  // past the pages: finite, masked keys
-          ring.acquire(st, 1, k_empty, k_selff);
+          mbar_wait(&k_empty[st], ((kc / KST) & 1) ^ 1);
           if (lane == 0) {
             mbar_expect_tx(&k_full[st], Ly::TILE_B);
             tma_load_2d(smem + Ly::k_off(kc), &tmKV, &k_full[st], head * DH, (int)page_row(pa, 0, 0));
@@ -846,33 +817,21 @@ __global__ void __launch_bounds__(THREADS, 2)
         ++it;
       }
     } else if (warp == 3) {
-      // ---------------- V producer: (v_self), V chunks; geometry from the descriptors ----------------
+      // ---------------- V producer: V chunks; geometry from the descriptors ----------------
       int it = 0, vc = 0;
-      RingSlots<VST> ring;
-      ring.init();
       for (;; ++it) {
         const int b = it & 1;
         mbar_wait(&q_full[b], (it >> 1) & 1);
         const PDesc* ds = desc + b;
         if (ds->done) break;
         const int nch = ds->nch, head = ds->head, n_pages = ds->n_pages;
-        const long long rbase = ds->rbase;
         const int pg = lane < n_pages ? ds->pages[lane] : 0;
-        if (SUMI) {
-          const int st = vc % VST;
-          ring.acquire(st, 2, v_empty, v_selff);
-          if (lane == 0) {
-            mbar_expect_tx(&v_full[st], Ly::TILE_B);
-            tma_load_2d(smem + Ly::v_off(vc), &tmQ, &v_full[st], 2 * D.d + head * DH, (int)rbase);
-          }
-          ++vc;
-        }
         for (int j = 0; j < nch; ++j, ++vc) {
           const int st = vc % VST;
           const int pa = __shfl_sync(0xffffffffu, pg, (2 * j) & 31);
           const int pb0 = __shfl_sync(0xffffffffu, pg, (2 * j + 1) & 31);
           const int pb = (2 * j + 1 < n_pages) ? pb0 : pa;
-          ring.acquire(st, 1, v_empty, v_selff);
+          mbar_wait(&v_empty[st], ((vc / VST) & 1) ^ 1);
           if (lane == 0) {
             mbar_expect_tx(&v_full[st], Ly::TILE_B);
             tma_load_2d(smem + Ly::v_off(vc), &tmKV, &v_full[st], head * DH, (int)page_row(pa, 1, 0));
@@ -905,7 +864,7 @@ __global__ void __launch_bounds__(THREADS, 2)
       bool first_issued = false;
       while (!done) {
         const int b = it & 1;
-        const int c0 = kc + SELF;  // ring item of chunk 0
+        const int c0 = kc;  // ring item of chunk 0
         if (nch > 0 && !first_issued) qk(b, c0);
         int done2 = 1, nch2 = 0;
         bool peeked = false, issued2 = false;
@@ -920,7 +879,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 #pragma unroll 1
           for (int s = 0; s < KEYS / 16; ++s) {
             const uint64_t vds = vd + (uint64_t)((16 * Ly::RB) >> 4) * s;
-            const uint32_t acc = (SUMI || j > 0 || s > 0) ? 1u : 0u;
+            const uint32_t acc = (j > 0 || s > 0) ? 1u : 0u;
             mma_bf16_ts(tO, tP + 8 * s, vds, idesc_pv, acc);
           }
           mma_commit(&v_empty[item % VST]);
@@ -935,7 +894,7 @@ __global__ void __launch_bounds__(THREADS, 2)
             nch2 = desc[b2].nch;
             peeked = true;
             if (!done2 && nch2 > 0) {
-              qk(b2, c0 + nch + SELF);
+              qk(b2, c0 + nch);
               issued2 = true;
             }
           }
@@ -987,53 +946,6 @@ __global__ void __launch_bounds__(THREADS, 2)
       const int t_row = ds->tile0 + row;
       const uint32_t qbuf = smem_u32(smem + Ly::q_off(b));
       float m_used = -INFINITY, l = 0.f;
-      if (SUMI) {
-        // self term: m = s_self, l = 1, O = v_self (k_self / v_self are this
-        // tile's first ring items; released once every row has read them)
-        const int st_k = kc % KST, st_v = kc % VST;
-        mbar_wait(&k_full[st_k], (kc / KST) & 1);
-        if (tt) tt[13] = clock64();
-        const uint32_t qrow = qbuf + row * Ly::RB;
-        const uint32_t krow = smem_u32(smem + Ly::k_off(kc)) + row * Ly::RB;
-        const uint32_t vrow = smem_u32(smem + Ly::v_off(kc)) + row * Ly::RB;
-        int4 qv[DH / 8], kv[DH / 8];
-#pragma unroll
-        for (int j = 0; j < DH / 8; ++j) {
-          qv[j] = lds_v4(qrow + (swz<DH>(row, j) << 4));
-          kv[j] = lds_v4(krow + (swz<DH>(row, j) << 4));
-        }
-        float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int j = 0; j < DH / 8; ++j) {
-          const bf16* qb = reinterpret_cast<const bf16*>(&qv[j]);
-          const bf16* kb = reinterpret_cast<const bf16*>(&kv[j]);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) ps[i] = fmaf(__bfloat162float(qb[i]), __bfloat162float(kb[i]), ps[i]);
-        }
-        const float ss = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
-        m_used = valid ? ss * sc : 0.f;
-        // generic reads of a TMA-written tile (consumed above), released to
-        // the next TMA write by every row (no proxy fence needed for reads)
-        mbar_arrive(&k_selff[st_k]);
-        if (tt) tt[14] = clock64();
-        mbar_wait(&v_full[st_v], (kc / VST) & 1);
-        if (tt) tt[15] = clock64();
-#pragma unroll
-        for (int c = 0; c < DH; c += 32) {
-          float vs[32];
-#pragma unroll
-          for (int cc = 0; cc < 32; cc += 8) {
-            const int4 vv = lds_v4(vrow + (swz<DH>(row, (c + cc) / 8) << 4));
-            const bf16* vb = reinterpret_cast<const bf16*>(&vv);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) vs[cc + i] = valid ? __bfloat162float(vb[i]) : 0.f;
-          }
-          tmem_st32_nw(tO + lane_off + c, vs);  // waited before P(0) is released (or before a rescale)
-        }
-        l = 1.f;
-        mbar_arrive(&v_selff[st_v]);  // the v_self values were consumed by the TMEM stores
-        if (tt) tt[1] = clock64();
-      }
       release_pending();
       for (int j = 0; j < nch; ++j, ++n) {
         mbar_wait(s_full, n & 1);
@@ -1070,8 +982,7 @@ __global__ void __launch_bounds__(THREADS, 2)
         }
         const bool need_pv = j > 0;  // P(j-1) V_{j-1} of this tile (the previous tile's were waited)
         bool pv_seen = false;
-        if ((SUMI || j > 0) && __any_sync(0xffffffffu, mine)) {
-          if (SUMI && j == 0) tmem_st_wait();
+        if (j > 0 && __any_sync(0xffffffffu, mine)) {
           if (need_pv) {
             mbar_wait(pv_done, (n - 1) & 1);
             fence_after();
@@ -1118,16 +1029,47 @@ __global__ void __launch_bounds__(THREADS, 2)
         mbar_arrive(p_full);
         if (tt && j < 4) tt[3 + 2 * j] = clock64();
       }
+      // ---- SUMI self term, merged into the row's state (every
+      // candidate also sees itself): x = q . k_self / (sqrt(d_h) tau) in log2
+      // units, m' = max(m, x), O' = O 2^(m - m') + v_self 2^(x - m'),
+      // l' = l 2^(m - m') + 2^(x - m').  k_self / v_self rows come from the
+      // QKV rows in global memory, loaded while the last P V runs; q from the
+      // tile's q buffer (still intact: the staging below overwrites it)
+      float oa = 1.f, vb = 0.f;     // O' = O oa + v_self vb (before 1 / l')
+      int4 vsv[DH / 8];
+      if (SUMI) {
+        int4 ksv[DH / 8];
+        const bf16* krow_g = a.Q + (rbase + row) * 3LL * D.d + D.d + head * DH;
+#pragma unroll
+        for (int j = 0; j < DH / 8; ++j) {
+          ksv[j] = valid ? __ldg(reinterpret_cast<const int4*>(krow_g) + j) : make_int4(0, 0, 0, 0);
+          vsv[j] = valid ? __ldg(reinterpret_cast<const int4*>(krow_g + D.d) + j) : make_int4(0, 0, 0, 0);
+        }
+        const uint32_t qrow = qbuf + row * Ly::RB;
+        float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < DH / 8; ++j) {
+          const int4 qv = lds_v4(qrow + (swz<DH>(row, j) << 4));
+          const bf16* qb = reinterpret_cast<const bf16*>(&qv);
+          const bf16* kb = reinterpret_cast<const bf16*>(&ksv[j]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) ps[i] = fmaf(__bfloat162float(qb[i]), __bfloat162float(kb[i]), ps[i]);
+        }
+        const float x = (((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]))) * sc;
+        const float m2 = fmaxf(m_used, x);
+        oa = (m_used == -INFINITY) ? 0.f : exp2f(m_used - m2);
+        vb = exp2f(x - m2);
+        l = l * oa + vb;
+      }
       // ---- epilogue: O / l -> bf16 staged in this tile's q buffer, coalesced row stores
       if (nch > 0) {
         mbar_wait(pv_done, (n - 1) & 1);
         fence_after();
-      } else if (SUMI) {
-        tmem_st_wait();  // O = v_self
       }
       if (tt) tt[10] = clock64();
-      const bool have_o = SUMI || nch > 0;
+      const bool have_o = nch > 0;
       const float inv = (valid && l > 0.f) ? 1.f / l : 0.f;
+      const float oai = oa * inv, vbi = vb * inv;
 #pragma unroll
       for (int c = 0; c < DH; c += 32) {
         float o[32];
@@ -1137,12 +1079,23 @@ __global__ void __launch_bounds__(THREADS, 2)
 #pragma unroll
           for (int i = 0; i < 32; ++i) o[i] = 0.f;
         }
+        if (SUMI) {
+#pragma unroll
+          for (int cc = 0; cc < 32; cc += 8) {
+            const bf16* vv = reinterpret_cast<const bf16*>(&vsv[(c + cc) / 8]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[cc + i] = fmaf(o[cc + i], oai, __bfloat162float(vv[i]) * vbi);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] *= inv;
+        }
 #pragma unroll
         for (int cc = 0; cc < 32; cc += 8) {
           uint32_t w[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            __nv_bfloat162 pp = __floats2bfloat162_rn(o[cc + 2 * i] * inv, o[cc + 2 * i + 1] * inv);
+            __nv_bfloat162 pp = __floats2bfloat162_rn(o[cc + 2 * i], o[cc + 2 * i + 1]);
             w[i] = *reinterpret_cast<uint32_t*>(&pp);
           }
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(qbuf + row * Ly::RB +
@@ -1184,7 +1137,7 @@ __global__ void __launch_bounds__(THREADS, 2)
         if (lane == 0) mbar_arrive(&q_empty[b]);  // the buffer (and its descriptor) go back to the producer
       }
       if (tt) tt[12] = clock64();
-      kc += SELF + nch;
+      kc += nch;
     }
     release_pending();
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -1231,15 +1184,13 @@ static int sm_count() {
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   return n;
 }
-// CLIMBER_ATTN_PERSIST: 1 (default) persistent history attention, one-tile
-// SUMI; 0 one-tile kernels everywhere (A/B, tested bitwise equal); 2 also the
-// persistent SUMI kernel -- EXPERIMENTAL: not bitwise reproducible (a
-// first-tile race specific to its k_self / v_self path)
-static int persist_mode() {
-  static const int m = [] { const char* e = getenv("CLIMBER_ATTN_PERSIST"); return e ? atoi(e) : 1; }();
-  return m;
+// CLIMBER_ATTN_PERSIST=0 selects the one-tile kernels (A/B; tested: bitwise
+// equal for history rows, within the parity tolerance for SUMI rows, whose
+// self term the persistent kernel merges at the end instead of first)
+static bool use_persistent(int /*mode*/) {
+  static const bool on = [] { const char* e = getenv("CLIMBER_ATTN_PERSIST"); return !e || atoi(e) != 0; }();
+  return on;
 }
-static bool use_persistent(int mode) { return mode == MODE_HIST ? persist_mode() >= 1 : persist_mode() >= 2; }
 
 template <int DH, int MODE>
 static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a, dim3 grid, cudaStream_t s,
@@ -1248,8 +1199,8 @@ static void launch(const CUtensorMap& mq, const CUtensorMap& mkv, const Args& a,
   static_assert(2 * (smem + 1024) <= 233472, "two CTAs per SM");
   static_assert(2 * (PLay<DH>::TOTAL + 1024) <= 233472, "two persistent CTAs per SM");
   // persistent kernel without the relative bias (A/B in a 128-user `large`
-  // step: history 339-341 vs 258-262 TFLOP/s, medium 109 vs 80; SUMI 417-437
-  // vs 391-428 and 205 vs 162, but see persist_mode)
+  // step: history 339-341 vs 258-262 TFLOP/s, medium 109 vs 80; SUMI see
+  // DESIGN.md §6)
   {
     if (!a.D.bpos && mo && use_persistent(MODE)) {
       const int n_tiles = (int)(grid.x * grid.y * grid.z);

@@ -1,12 +1,15 @@
-"""The persistent tcgen05 attention kernel (k_attn_pers; the default for
-history rows without the relative bias) against the one-tile-per-CTA kernel
-(k_attn_fa, CLIMBER_ATTN_PERSIST=0).  Both kernels do the same arithmetic per
-query row in the same order, so the scores must agree bit for bit (the other
-parity tests bound the default path against the fp64 oracle).  Cases cover
-d_h 32 and 64, ragged users (history tiles past v: no keys), blocks with
-v_k = 0, M = 1, causal and bidirectional history.  The persistent SUMI variant
-(CLIMBER_ATTN_PERSIST=2) is experimental and not covered: it is not bitwise
-reproducible.  P:L255 (SUMI masks), Eq. 3 (f_b = 0).
+"""The persistent tcgen05 attention kernel (k_attn_pers, the default without
+the relative bias) against the one-tile-per-CTA kernel (k_attn_fa,
+CLIMBER_ATTN_PERSIST=0).  History rows do the same arithmetic in the same
+order in both; SUMI rows merge the self term at the end in the persistent
+kernel instead of starting from it, so the scores agree within the
+north-star tolerance (2e-2 abs / rel, rel floored at 1) rather than bit for
+bit; the other parity tests bound the default path against the fp64 oracle.
+Cases cover d_h 32 and 64, ragged candidate counts (tiles without
+candidates, partial tiles), history tiles past v (no keys), blocks with
+v_k = 0 (self term only), M = 1, causal and bidirectional history.  A
+repeat-launch test checks bitwise reproducibility.  P:L255 (SUMI masks),
+Eq. 3 (f_b = 0).
 """
 import os
 import subprocess
@@ -56,12 +59,13 @@ def _run(case, persist, tmp_path):
 
 
 @pytest.mark.parametrize("case", ["small", "medium", "medium_bidir", "medium_empty", "large"])
-def test_persistent_attention_bitwise_equal_one_tile_kernel(case, tmp_path):
+def test_persistent_attention_matches_one_tile_kernel(case, tmp_path):
     a = _run(case, 1, tmp_path)
     b = _run(case, 0, tmp_path)
-    assert np.all(np.isfinite(a))
-    assert a.shape == b.shape and np.array_equal(a.view(np.uint32), b.view(np.uint32)), \
-        (case, float(np.abs(a - b).max()))
+    assert np.all(np.isfinite(a)) and a.shape == b.shape
+    ab = np.abs(a.astype(np.float64) - b.astype(np.float64))
+    rel = ab / np.maximum(np.abs(b.astype(np.float64)), 1.0)
+    assert ab.max() <= 2e-2 and rel.max() <= 2e-2, (case, float(ab.max()), float(rel.max()))
 
 
 def test_attention_deterministic_across_launches():

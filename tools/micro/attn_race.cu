@@ -8,6 +8,7 @@
 //        paper_2502_09888_b200/csrc/attn_fa.cu -o attn_race
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -100,8 +101,15 @@ int main(int argc, char** argv) {
       const size_t nr = fread(stored.data(), 2, stored.size(), f);
       fclose(f);
       long long nd = 0;
-      for (size_t k = 0; k < ref.size() && k < nr; ++k) nd += stored[k] != ref[k];
-      printf("rep 0 vs stored reference: %lld differing elements\n", nd);
+      double mx = 0.0;
+      auto f32 = [](uint16_t b) { uint32_t u = (uint32_t)b << 16; float f; memcpy(&f, &u, 4); return f; };
+      for (size_t k = 0; k < ref.size() && k < nr; ++k)
+        if (stored[k] != ref[k]) {
+          ++nd;
+          const double dd = fabs((double)f32(stored[k]) - (double)f32(ref[k]));
+          mx = dd > mx ? dd : mx;
+        }
+      printf("rep 0 vs stored reference: %lld differing elements (max abs diff %.3g)\n", nd, mx);
     }
     if (rep == 0) continue;
     long long nd = 0, shown = 0;

@@ -12,5 +12,6 @@ for nk in 64 128 256 512 1024; do run --n-k $nk; done
 for M in 100 500 2000; do run --M $M; done
 timeout 300 python bench.py --config medium --steps 3 --warmup 3 --latency-requests 10 --no-cpu-baseline --no-e2e --reuse 8 2>>gpurun_out/sweep_err.log | tail -1 >> $out
 timeout 300 python bench.py --config large --users 256 --steps 2 --warmup 3 --latency-requests 10 --no-cpu-baseline --no-e2e --rel-bias 1 2>>gpurun_out/sweep_err.log | tail -1 >> $out
+timeout 300 python bench.py --config large --users 256 --steps 2 --warmup 3 --latency-requests 10 --no-cpu-baseline --no-e2e --rel-bias 0 2>>gpurun_out/sweep_err.log | tail -1 >> $out
 timeout 300 python bench.py --config small --steps 5 --warmup 3 --latency-requests 10 --no-cpu-baseline --no-e2e 2>>gpurun_out/sweep_err.log | tail -1 >> $out
 wc -l $out
