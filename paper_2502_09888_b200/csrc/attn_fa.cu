@@ -1251,11 +1251,10 @@ static void ptrace_print(const unsigned long long* buf, long long n_cta) {
   fprintf(stderr, "[fa ptrace] persistent kernel (cycles since CTA start)\n");
   for (int it = 0; it < 4; ++it) {
     const int b = it * 24;
-    fprintf(stderr, "[fa ptrace] tile %d: q %7.0f self %7.0f | S0 %7.0f P0 %7.0f S1 %7.0f P1 %7.0f S2 %7.0f P2 %7.0f "
-                    "S3 %7.0f P3 %7.0f | pv_done %7.0f staged %7.0f released %7.0f | kself %7.0f dot %7.0f vself "
-                    "%7.0f\n",
-            it, m(b), m(b + 1), m(b + 2), m(b + 3), m(b + 4), m(b + 5), m(b + 6), m(b + 7), m(b + 8), m(b + 9),
-            m(b + 10), m(b + 11), m(b + 12), m(b + 13), m(b + 14), m(b + 15));
+    fprintf(stderr, "[fa ptrace] tile %d: q %7.0f | S0 %7.0f P0 %7.0f S1 %7.0f P1 %7.0f S2 %7.0f P2 %7.0f "
+                    "S3 %7.0f P3 %7.0f | self+pv_done %7.0f staged %7.0f released %7.0f\n",
+            it, m(b), m(b + 2), m(b + 3), m(b + 4), m(b + 5), m(b + 6), m(b + 7), m(b + 8), m(b + 9), m(b + 10),
+            m(b + 11), m(b + 12));
   }
   for (int i = 0; i < 16; ++i) fprintf(stderr, "[fa ptrace] QK %2d issued %7.0f%s", i, m(96 + i), i % 4 == 3 ? "\n" : " |");
   for (int i = 0; i < 12; ++i) fprintf(stderr, "[fa ptrace] PV %2d issued %7.0f%s", i, m(112 + i), i % 4 == 3 ? "\n" : " |");
